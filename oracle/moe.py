@@ -1,0 +1,333 @@
+"""fp64 oracle of the expert-parallel MoE block forward — TEST INFRASTRUCTURE ONLY.
+
+Cites PAPER.md (P:<line>) and, for interface details the paper leaves open,
+SPEC.md (S:<line>) through the readings C-amb-n listed in DESIGN.md.
+Nothing here is blocked, fused or reordered beyond the definitions.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+RMS_EPS = 1e-6  # C-amb-5: RMSNorm, eps 1e-6
+
+
+# ---------------------------------------------------------------------------
+# Elementwise / row primitives
+# ---------------------------------------------------------------------------
+
+def rmsnorm(x: np.ndarray, gamma: np.ndarray, eps: float = RMS_EPS) -> np.ndarray:
+    """Pre-norm 'layer-norm' of P:103, read as RMSNorm (C-amb-5):
+    y = x / sqrt(mean(x^2) + eps) * gamma, in fp64."""
+    x = np.asarray(x, np.float64)
+    r = np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + eps)
+    return x / r * np.asarray(gamma, np.float64)
+
+
+def softmax_rows(l: np.ndarray) -> np.ndarray:
+    """Row softmax with max subtraction; the router's s() (C-amb-2)."""
+    l = np.asarray(l, np.float64)
+    z = np.exp(l - l.max(axis=-1, keepdims=True))
+    return z / z.sum(axis=-1, keepdims=True)
+
+
+def silu(z: np.ndarray) -> np.ndarray:
+    """g = SiLU(z) = z / (1 + e^-z) (C-amb-4)."""
+    z = np.asarray(z, np.float64)
+    return z / (1.0 + np.exp(-z))
+
+
+def swiglu(a: np.ndarray, w1: np.ndarray, w2: np.ndarray, w3: np.ndarray) -> np.ndarray:
+    """Gated MLP of P:73-76: MLP(A) = sigma(A W1^T . g(A W2^T)) W3^T with
+    sigma = identity and g = SiLU on the W2 branch (C-amb-4).
+    Shapes: a [B,d], w1,w2 [c,d], w3 [d,c] -> [B,d]."""
+    a = np.asarray(a, np.float64)
+    u = a @ np.asarray(w1, np.float64).T
+    g = silu(a @ np.asarray(w2, np.float64).T)
+    return (u * g) @ np.asarray(w3, np.float64).T
+
+
+# ---------------------------------------------------------------------------
+# Router G(A) = s(A W_R^T)
+# ---------------------------------------------------------------------------
+
+@dataclasses.dataclass
+class RouterOutput:
+    idx: np.ndarray      # int32 [T,k], ascending expert id per token (C-amb-3 slot order)
+    gates: np.ndarray    # fp64 [T,k], renormalised over the selected set (sum 1)
+    logits: np.ndarray   # fp64 [T,E] = xn W_R^T
+    probs: np.ndarray    # fp64 [T,E] = softmax(logits)
+    gap: np.ndarray      # fp64 [T]  l_(k) - l_(k+1) in descending logit order; +inf if k == E
+
+
+def route(xn: np.ndarray, w_router: np.ndarray, top_k: int) -> RouterOutput:
+    """Router of P:96 with s() read as softmax over E, top-k, renormalise (C-amb-2).
+
+    1. l = xn W_R^T (fp64; W_R fp32 widened exactly);
+    2. p = softmax(l);
+    3. S_t = the k largest p, exact ties to the lower expert index (C-amb-3);
+    4. g = p_S / sum(p_S);
+    5. slots ordered by ascending expert id (C-amb-3).
+    Also reports the boundary gap used by the near-tie rule R-1.
+    """
+    E = w_router.shape[0]
+    if not 1 <= top_k <= E:
+        raise ValueError(f"top_k={top_k} outside [1, E={E}]")
+    l = np.asarray(xn, np.float64) @ np.asarray(w_router, np.float64).T
+    p = softmax_rows(l)
+    T = l.shape[0]
+    order = np.argsort(-p, axis=1, kind="stable")          # descending p, ties -> lower index
+    sel = np.sort(order[:, :top_k], axis=1)                # slot order = ascending expert id
+    ps = np.take_along_axis(p, sel, axis=1)
+    gates = ps / ps.sum(axis=1, keepdims=True)
+    ls = -np.sort(-l, axis=1)
+    gap = np.full(T, np.inf) if top_k == E else ls[:, top_k - 1] - ls[:, top_k]
+    return RouterOutput(sel.astype(np.int32), gates, l, p, gap)
+
+
+# ---------------------------------------------------------------------------
+# Permutation maps ("grouped and mapped ... requiring permutation of A"; R_i of P:98-100)
+# ---------------------------------------------------------------------------
+
+@dataclasses.dataclass
+class PermMaps:
+    counts: np.ndarray   # int64 [E]   #{(t,j): idx[t,j] == e}
+    offsets: np.ndarray  # int64 [E+1] exclusive prefix of counts
+    pos: np.ndarray      # int64 [T,k] destination row of copy (t,j) in the expert-sorted buffer
+    src_row: np.ndarray  # int64 [T*k] token whose copy sits in row p
+
+
+def permutation_maps(idx: np.ndarray, n_experts: int) -> PermMaps:
+    """Stable counting sort of the (token, slot) copies by expert (C-amb-11):
+    counts[e]; offsets = exclusive scan; within an expert, copies keep ascending
+    token order, so pos[t,j] = offsets[e] + #{t' < t : e in S_t'}."""
+    idx = np.asarray(idx)
+    T, k = idx.shape
+    flat = idx.reshape(-1)
+    counts = np.zeros(n_experts, np.int64)
+    for e in flat:
+        counts[e] += 1
+    offsets = np.zeros(n_experts + 1, np.int64)
+    offsets[1:] = np.cumsum(counts)
+    pos = np.empty(T * k, np.int64)
+    src_row = np.empty(T * k, np.int64)
+    for e in range(n_experts):
+        members = np.nonzero(flat == e)[0]           # ascending (t, j) flat order -> ascending t
+        rows = offsets[e] + np.arange(members.size)
+        pos[members] = rows
+        src_row[rows] = members // k
+    return PermMaps(counts, offsets, pos.reshape(T, k), src_row)
+
+
+# ---------------------------------------------------------------------------
+# Expert parallel dispatch / combine simulation
+# ---------------------------------------------------------------------------
+
+@dataclasses.dataclass
+class EpLayer:
+    """Full (unsharded) MoE layer parameters as fp64 (bf16 widened exactly)."""
+    gamma: np.ndarray
+    w_router: np.ndarray
+    w1: np.ndarray   # [E, c, d]
+    w2: np.ndarray   # [E, c, d]
+    w3: np.ndarray   # [E, d, c]
+    ws1: Optional[np.ndarray] = None   # [c_s, d]
+    ws2: Optional[np.ndarray] = None
+    ws3: Optional[np.ndarray] = None   # [d, c_s]
+    top_k: int = 1
+
+    @property
+    def n_experts(self) -> int:
+        return self.w1.shape[0]
+
+
+def expert_owner(e: int, n_experts: int, n_ranks: int) -> int:
+    """Contiguous placement: rank p owns experts [p E/P, (p+1) E/P) (C-amb-9)."""
+    return e // (n_experts // n_ranks)
+
+
+def dispatch_sim(xn_per_rank: Sequence[np.ndarray], idx_per_rank: Sequence[np.ndarray],
+                 n_experts: int, n_ranks: int):
+    """Dispatch of P:97-100: A_i = R_i x A placed on rank i.
+
+    Receive layout on rank p (C-amb-11): expert-major over p's local experts,
+    then source rank, then ascending token. Returns per destination rank the
+    receive buffer [R_p, d], the per-local-expert row counts, and for every
+    source rank s the map (dst rank, dst row) of each copy (t, j)."""
+    if n_experts % n_ranks:
+        raise ValueError("E not divisible by n_ranks (C-amb-9 config error)")
+    e_loc = n_experts // n_ranks
+    P = n_ranks
+    # counts matrix cnt[s, e]: how many copies source s sends to expert e
+    cnt = np.zeros((P, n_experts), np.int64)
+    for s in range(P):
+        for e in np.asarray(idx_per_rank[s]).reshape(-1):
+            cnt[s, e] += 1
+    recv_bufs, recv_counts = [], []
+    dst_row = [np.empty(np.asarray(i).shape, np.int64) for i in idx_per_rank]
+    dst_rank = [np.empty(np.asarray(i).shape, np.int64) for i in idx_per_rank]
+    for p in range(P):
+        rows = []
+        local_counts = np.zeros(e_loc, np.int64)
+        r = 0
+        for el in range(e_loc):
+            e = p * e_loc + el
+            for s in range(P):
+                idx = np.asarray(idx_per_rank[s])
+                T, k = idx.shape
+                for t in range(T):
+                    for j in range(k):
+                        if idx[t, j] == e:
+                            rows.append(np.asarray(xn_per_rank[s][t], np.float64))
+                            dst_row[s][t, j] = r
+                            dst_rank[s][t, j] = p
+                            r += 1
+                            local_counts[el] += 1
+        d = np.asarray(xn_per_rank[0]).shape[1]
+        recv_bufs.append(np.array(rows, np.float64).reshape(-1, d))
+        recv_counts.append(local_counts)
+    return recv_bufs, recv_counts, dst_rank, dst_row, cnt
+
+
+def experts_on_rank(recv: np.ndarray, local_counts: np.ndarray, layer: EpLayer, p: int,
+                    n_ranks: int) -> np.ndarray:
+    """Routed expert computation on rank p: each local expert's contiguous row
+    segment through its SwiGLU (P:198 step 6)."""
+    e_loc = layer.n_experts // n_ranks
+    y = np.zeros_like(recv)
+    r = 0
+    for el in range(e_loc):
+        e = p * e_loc + el
+        m = int(local_counts[el])
+        if m:
+            y[r:r + m] = swiglu(recv[r:r + m], layer.w1[e], layer.w2[e], layer.w3[e])
+        r += m
+    return y
+
+
+def combine_sim(y_per_rank: Sequence[np.ndarray], gates: np.ndarray, dst_rank: np.ndarray,
+                dst_row: np.ndarray) -> np.ndarray:
+    """Combine of P:100: the dual all-to-all brings each copy back to its source
+    token, which sums the gate-weighted expert outputs in slot order:
+    routed[t] = sum_j g[t,j] * y_{p(t,j)}[row(t,j)] (C-amb-12: sum starts at 0)."""
+    T, k = gates.shape
+    d = y_per_rank[0].shape[1] if len(y_per_rank[0]) else None
+    if d is None:
+        d = next(y.shape[1] for y in y_per_rank if y.ndim == 2)
+    out = np.zeros((T, d), np.float64)
+    for t in range(T):
+        acc = np.zeros(d, np.float64)
+        for j in range(k):
+            acc = acc + gates[t, j] * y_per_rank[dst_rank[t, j]][dst_row[t, j]]
+        out[t] = acc
+    return out
+
+
+def shared_expert(xn: np.ndarray, layer: EpLayer) -> np.ndarray:
+    """Shared experts 'process all tokens' on the same xn (C-amb-7);
+    n shared experts == one SwiGLU of concatenated width. Width 0 -> exact zeros."""
+    if layer.ws1 is None:
+        return np.zeros(np.asarray(xn).shape, np.float64)
+    return swiglu(xn, layer.ws1, layer.ws2, layer.ws3)
+
+
+def moe_block_ep(x_per_rank: Sequence[np.ndarray], layer: EpLayer, n_ranks: int):
+    """MoE block forward with EP over n_ranks simulated ranks.
+
+    Per rank s: xn = rmsnorm(x_s); router; dispatch; experts; combine.
+    Returns [(shared_out_s, routed_out_s, RouterOutput_s)] for every rank s,
+    shared and routed SEPARATELY."""
+    if len(x_per_rank) != n_ranks:
+        raise ValueError("one token block per rank")
+    xns = [rmsnorm(x, layer.gamma) for x in x_per_rank]
+    routers = [route(xn, layer.w_router, layer.top_k) for xn in xns]
+    recv, rc, dst_rank, dst_row, _ = dispatch_sim(xns, [r.idx for r in routers],
+                                                   layer.n_experts, n_ranks)
+    ys = [experts_on_rank(recv[p], rc[p], layer, p, n_ranks) for p in range(n_ranks)]
+    out = []
+    for s in range(n_ranks):
+        routed = combine_sim(ys, routers[s].gates, dst_rank[s], dst_row[s])
+        out.append((shared_expert(xns[s], layer), routed, routers[s]))
+    return out
+
+
+def moe_block(x: np.ndarray, layer: EpLayer, router: Optional[RouterOutput] = None):
+    """Single-rank MoE block (EP=1) -> (shared_out, routed_out, RouterOutput).
+
+    The gate-weighted routed sum is MoE(A) = sum_j G(A)_j MLP^j(A) over
+    the selected set, evaluated through the expert-sorted permutation
+    and the combine sum in slot order. If ``router`` is given its selection is
+    used (the near-tie adoption rule R-1 of SURVEY §8(c) O-3)."""
+    xn = rmsnorm(x, layer.gamma)
+    r = route(xn, layer.w_router, layer.top_k) if router is None else router
+    maps = permutation_maps(r.idx, layer.n_experts)
+    xs = xn[maps.src_row]
+    y = np.zeros_like(xs)
+    for e in range(layer.n_experts):
+        a, b = maps.offsets[e], maps.offsets[e + 1]
+        if b > a:
+            y[a:b] = swiglu(xs[a:b], layer.w1[e], layer.w2[e], layer.w3[e])
+    T, k = r.idx.shape
+    routed = np.zeros_like(xn)
+    for j in range(k):
+        routed = routed + r.gates[:, j:j + 1] * y[maps.pos[:, j]]
+    return shared_expert(xn, layer), routed, r
+
+
+def moe_block_dense(x: np.ndarray, layer: EpLayer):
+    """Brute force (BASELINE.json north star): every token through every
+    expert, masked by its top-k gates; no permutation, no dispatch."""
+    xn = rmsnorm(x, layer.gamma)
+    r = route(xn, layer.w_router, layer.top_k)
+    T, E = r.logits.shape
+    mask = np.zeros((T, E), np.float64)
+    for j in range(r.idx.shape[1]):
+        mask[np.arange(T), r.idx[:, j]] = r.gates[:, j]
+    routed = np.zeros_like(xn)
+    for e in range(E):
+        routed += mask[:, e:e + 1] * swiglu(xn, layer.w1[e], layer.w2[e], layer.w3[e])
+    return shared_expert(xn, layer), routed, r
+
+
+def adopt_router(layer: EpLayer, x: np.ndarray, gpu_idx: np.ndarray, margin: float = 1e-6):
+    """Near-tie rule R-1: tokens whose oracle boundary gap is
+    below ``margin`` take the GPU's selected set (gates recomputed in fp64 from
+    the oracle's own probabilities). Returns (RouterOutput, excluded_mask)."""
+    xn = rmsnorm(x, layer.gamma)
+    r = route(xn, layer.w_router, layer.top_k)
+    excl = r.gap < margin
+    if excl.any():
+        idx = r.idx.copy()
+        idx[excl] = np.sort(np.asarray(gpu_idx)[excl], axis=1)
+        ps = np.take_along_axis(r.probs, idx.astype(np.int64), axis=1)
+        gates = ps / ps.sum(axis=1, keepdims=True)
+        r = RouterOutput(idx, gates, r.logits, r.probs, r.gap)
+    return r, excl
+
+
+# ---------------------------------------------------------------------------
+# Sub-block outputs in the two wirings (C-amb-12 summation order)
+# ---------------------------------------------------------------------------
+
+def moe_sublayer_blocking(x_in, layer: EpLayer):
+    """Regular MoE sub-block: out = (x_in + shared) + routed (Eq. 6, C-amb-12)."""
+    sh, ro, r = moe_block(x_in, layer)
+    return (np.asarray(x_in, np.float64) + sh) + ro, sh, ro, r
+
+
+def moe_sublayer_farskip(x_in, partial_in, layer: EpLayer):
+    """FarSkip MoE sub-block: partial = partial_in + shared
+    (= attn-in_{k+1}); full = partial + routed (= mlp-in_{k+1} = o_k)."""
+    sh, ro, r = moe_block(x_in, layer)
+    partial = np.asarray(partial_in, np.float64) + sh
+    return partial, partial + ro, sh, ro, r
+
+
+def layer_from_synth(w, top_k: int) -> EpLayer:
+    """Widen a synth.MoeWeights (bf16 bits) to fp64 exactly."""
+    def wid(b):
+        return None if b is None else (np.asarray(b, np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return EpLayer(np.asarray(w.gamma, np.float64), np.asarray(w.w_router, np.float64),
+                   wid(w.w1), wid(w.w2), wid(w.w3), wid(w.ws1), wid(w.ws2), wid(w.ws3), top_k)

@@ -1,0 +1,238 @@
+"""Pins of the fp64 oracle's MoE functions against what the paper and the
+mathematics fix (task rule ③). None of these re-types an oracle formula: each
+check is a closed form, a special case, an invariant, a library routine used
+as an independent definition, or a brute force."""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+from oracle import moe as om
+import synth
+
+
+def rng(s=0):
+    return np.random.default_rng(s)
+
+
+# --------------------------------------------------------------- rmsnorm
+def test_rmsnorm_constant_row_is_sign():
+    x = np.full((2, 8), 3.0)
+    x[1] = -0.25
+    y = om.rmsnorm(x, np.ones(8))
+    # closed form: c / sqrt(c^2 + eps)
+    np.testing.assert_allclose(y[0], 3.0 / math.sqrt(9.0 + 1e-6), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(y[1], -0.25 / math.sqrt(0.0625 + 1e-6), rtol=0, atol=1e-15)
+
+
+def test_rmsnorm_gamma_zero_and_unit_rms():
+    x = rng().standard_normal((4, 64)) * 3
+    assert np.all(om.rmsnorm(x, np.zeros(64)) == 0)
+    y = om.rmsnorm(x, np.ones(64))
+    ms = (x * x).mean(axis=1)
+    # RMS(y) = sqrt(ms / (ms + eps))  (closed form)
+    np.testing.assert_allclose(np.sqrt((y * y).mean(axis=1)), np.sqrt(ms / (ms + 1e-6)), rtol=1e-14)
+    # scale invariance (x -> a x) up to the eps term; exact homogeneity in gamma
+    g = rng(1).standard_normal(64)
+    np.testing.assert_allclose(om.rmsnorm(x, 2 * g), 2 * om.rmsnorm(x, g), rtol=1e-15)
+
+
+# --------------------------------------------------------------- softmax
+def test_softmax_special_cases():
+    np.testing.assert_allclose(om.softmax_rows(np.zeros((1, 3))), [[1 / 3] * 3], rtol=1e-15)
+    s = om.softmax_rows(np.array([[1000.0, 0.0]]))
+    assert abs(s[0, 0] - 1) < 1e-12 and s[0, 1] < 1e-300 + 1e-12
+    l = rng().standard_normal((5, 7))
+    s = om.softmax_rows(l)
+    np.testing.assert_allclose(s.sum(1), 1, atol=1e-12)
+    np.testing.assert_allclose(om.softmax_rows(l + 17.5), s, rtol=1e-13)
+    # two-class softmax is the logistic function
+    a = rng(2).standard_normal(9)
+    two = om.softmax_rows(np.stack([a, np.zeros_like(a)], 1))
+    np.testing.assert_allclose(two[:, 0], 1 / (1 + np.exp(-a)), rtol=1e-14)
+
+
+# --------------------------------------------------------------- SiLU / SwiGLU
+def test_silu_values():
+    assert om.silu(np.array(0.0)) == 0
+    # sigma(1) = 0.7310585786300049 (logistic function table value)
+    assert abs(om.silu(np.array(1.0)) - 0.7310585786300049) < 1e-15
+    assert abs(om.silu(np.array(-1.0)) - (-1 + 0.7310585786300049)) < 1e-15  # silu(-z) = silu(z) - z
+    assert abs(om.silu(np.array(40.0)) - 40.0) < 1e-12
+
+
+def test_swiglu_examples():
+    z = np.zeros((3, 4))
+    assert np.all(om.swiglu(rng().standard_normal((2, 4)), np.zeros((5, 4)), np.zeros((5, 4)), np.zeros((4, 5))) == 0)
+    # d=c=1, A=[[1]], W1=[[2]], W2=[[0]], W3=[[1]] -> g(0)=0 -> 0
+    assert om.swiglu(np.array([[1.0]]), np.array([[2.0]]), np.array([[0.0]]), np.array([[1.0]]))[0, 0] == 0
+    # d=c=1, a=1, W1=2, W2=1, W3=3: U=2, G=silu(1)=sigma(1), out = 2*sigma(1)*3
+    v = om.swiglu(np.array([[1.0]]), np.array([[2.0]]), np.array([[1.0]]), np.array([[3.0]]))[0, 0]
+    assert abs(v - 6 * 0.7310585786300049) < 1e-14
+    # the gate branch is W2 (C-amb-4): swapping W1/W2 changes the result
+    a = rng(3).standard_normal((2, 4)); w1 = rng(4).standard_normal((5, 4)); w2 = rng(5).standard_normal((5, 4))
+    w3 = rng(6).standard_normal((4, 5))
+    assert not np.allclose(om.swiglu(a, w1, w2, w3), om.swiglu(a, w2, w1, w3))
+    # linear in W1 and in W3
+    np.testing.assert_allclose(om.swiglu(a, 3 * w1, w2, w3), 3 * om.swiglu(a, w1, w2, w3), rtol=1e-13)
+    np.testing.assert_allclose(om.swiglu(a, w1, w2, -2 * w3), -2 * om.swiglu(a, w1, w2, w3), rtol=1e-13)
+    # per-row independence and c-additivity (splitting c into halves sums, cf. Eq. 1-2)
+    full = om.swiglu(a, w1, w2, w3)
+    h1 = om.swiglu(a, w1[:2], w2[:2], w3[:, :2]) + om.swiglu(a, w1[2:], w2[2:], w3[:, 2:])
+    np.testing.assert_allclose(full, h1, rtol=1e-13, atol=1e-15)
+
+
+# --------------------------------------------------------------- router
+def test_route_examples():
+    # dense limit: top_k = E -> weights are the full softmax row
+    xn = rng().standard_normal((6, 8)); wr = rng(1).standard_normal((4, 8))
+    r = om.route(xn, wr, 4)
+    assert np.all(r.idx == np.arange(4))
+    np.testing.assert_allclose(r.gates, om.softmax_rows(xn @ wr.T), rtol=1e-14)
+    assert np.all(np.isinf(r.gap))
+    # score row [10,0,0,0], top-1 -> expert 0 with weight 1
+    r = om.route(np.array([[1.0]]), np.array([[10.0], [0.0], [0.0], [0.0]]), 1)
+    assert r.idx[0, 0] == 0 and r.gates[0, 0] == 1.0
+    # equal scores, top-2 -> {0,1}, [0.5, 0.5]
+    r = om.route(np.array([[1.0]]), np.ones((4, 1)), 2)
+    assert list(r.idx[0]) == [0, 1] and list(r.gates[0]) == [0.5, 0.5]
+    # tie at the boundary resolves to the lower index, wherever it sits
+    r = om.route(np.array([[1.0]]), np.array([[0.0], [3.0], [1.0], [3.0], [1.0]]), 3)
+    assert list(r.idx[0]) == [1, 2, 3]
+    with pytest.raises(ValueError):
+        om.route(xn, wr, 5)
+
+
+def test_route_brute_force_and_invariants():
+    g = rng(7)
+    for E, k in [(4, 1), (5, 2), (6, 3), (8, 2)]:
+        xn = g.standard_normal((20, 6)); wr = g.standard_normal((E, 6))
+        r = om.route(xn, wr, k)
+        l = xn @ wr.T
+        for t in range(20):
+            # brute force over all k-subsets: the chosen set maximises the sum of logits
+            best = max(itertools.combinations(range(E), k), key=lambda S: (sum(l[t, list(S)]), [-i for i in S]))
+            assert tuple(r.idx[t]) == tuple(sorted(best))
+            sel = r.idx[t]
+            unsel = [e for e in range(E) if e not in sel]
+            # gates: softmax restricted to the selected logits (closed form identity)
+            ex = np.exp(l[t, sel] - l[t, sel].max())
+            np.testing.assert_allclose(r.gates[t], ex / ex.sum(), rtol=1e-13)
+            assert np.all(r.gates[t] > 0) and abs(r.gates[t].sum() - 1) < 1e-12
+            assert len(set(sel)) == k and np.all(np.diff(sel) > 0)
+            if unsel:
+                assert abs(r.gap[t] - (l[t, sel].min() - l[t, unsel].max())) < 1e-12
+
+
+# --------------------------------------------------------------- permutation
+def test_permutation_maps_vs_stable_sort():
+    g = rng(11)
+    for T, E, k in [(1, 4, 2), (16, 8, 2), (37, 16, 3), (64, 4, 4), (50, 64, 6)]:
+        idx = np.stack([np.sort(g.choice(E, k, replace=False)) for _ in range(T)])
+        m = om.permutation_maps(idx, E)
+        assert m.counts.sum() == T * k                                  # BJ: counts sum to N*k
+        np.testing.assert_array_equal(m.counts, np.bincount(idx.reshape(-1), minlength=E))
+        assert sorted(m.pos.reshape(-1)) == list(range(T * k))           # bijection
+        t_of = np.repeat(np.arange(T), k)
+        order = np.argsort((idx.reshape(-1) * T + t_of), kind="stable")  # library stable sort
+        np.testing.assert_array_equal(m.src_row, order // k)
+        for t in range(T):
+            for j in range(k):
+                p = m.pos[t, j]
+                assert m.src_row[p] == t
+                e = idx[t, j]
+                assert m.offsets[e] <= p < m.offsets[e + 1]
+
+
+# --------------------------------------------------------------- dispatch / combine
+def _layer(T_unused, d, E, k, c, cs, seed=0):
+    g = rng(seed)
+    w = lambda *s: g.standard_normal(s) / math.sqrt(s[-1])  # noqa: E731
+    return om.EpLayer(1 + 0.1 * g.standard_normal(d), w(E, d), w(E, c, d), w(E, c, d), w(E, d, c),
+                      w(cs, d) if cs else None, w(cs, d) if cs else None, w(d, cs) if cs else None, k)
+
+
+def test_dispatch_forced_example():
+    # T=2, E=4, top_1, n_ranks=2, assignments [0,3] -> rank0 {t0}, rank1 {t1}
+    xn = np.array([[1.0, 2.0], [3.0, 4.0]])
+    idx = np.array([[0], [3]])
+    recv, rc, dst_rank, dst_row, cnt = om.dispatch_sim([xn[:2]], [idx], 4, 1)
+    assert recv[0].shape == (2, 2)
+    # two ranks, each holding one of the tokens as its own
+    recv, rc, dst_rank, dst_row, cnt = om.dispatch_sim([xn, xn], [idx, idx], 4, 2)
+    np.testing.assert_array_equal(recv[0], [xn[0], xn[0]])    # token0 from both sources
+    np.testing.assert_array_equal(recv[1], [xn[1], xn[1]])
+    assert list(rc[0]) == [2, 0] and list(rc[1]) == [0, 2]
+    with pytest.raises(ValueError):
+        om.dispatch_sim([xn] * 3, [idx] * 3, 4, 3)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_ep_invariance(P):
+    # random T=16, E=8, top-2; the routed output is identical across n_ranks
+    lay = _layer(16, 12, 8, 2, 10, 6, seed=3)
+    X = rng(5).standard_normal((16 * P, 12))
+    ref = om.moe_block(X, lay)
+    outs = om.moe_block_ep([X[s * 16:(s + 1) * 16] for s in range(P)], lay, P)
+    routed = np.concatenate([o[1] for o in outs])
+    shared = np.concatenate([o[0] for o in outs])
+    np.testing.assert_allclose(routed, ref[1], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(shared, ref[0], rtol=0, atol=1e-12)
+
+
+def test_moe_block_equals_dense_brute_force():
+    for (T, d, E, k, c, cs) in [(32, 64, 4, 2, 128, 0), (40, 16, 8, 3, 24, 32), (9, 8, 6, 6, 4, 0), (7, 8, 5, 1, 4, 4)]:
+        lay = _layer(T, d, E, k, c, cs, seed=T)
+        x = rng(T + 1).standard_normal((T, d))
+        sh, ro, r = om.moe_block(x, lay)
+        sh2, ro2, r2 = om.moe_block_dense(x, lay)
+        np.testing.assert_allclose(ro, ro2, rtol=0, atol=1e-12 * max(1, np.abs(ro2).max()))
+        np.testing.assert_allclose(sh, sh2, rtol=0, atol=0)
+
+
+def test_moe_zero_cases():
+    lay = _layer(8, 16, 4, 2, 8, 0, seed=1)
+    x = rng(2).standard_normal((8, 16))
+    sh, ro, _ = om.moe_block(x, lay)
+    assert np.all(sh == 0)
+    lay.w1[:] = 0; lay.w2[:] = 0; lay.w3[:] = 0
+    sh, ro, _ = om.moe_block(x, lay)
+    assert np.all(ro == 0)
+
+
+def test_moe_single_expert_top1_is_dense_mlp():
+    # E = k = 1: MoE(A) = G(A)_1 MLP^1(A) with G = 1 -> the plain gated MLP of P:73-76
+    lay = _layer(6, 8, 1, 1, 12, 0, seed=9)
+    x = rng(3).standard_normal((6, 8))
+    _, ro, r = om.moe_block(x, lay)
+    assert np.all(r.gates == 1.0)
+    np.testing.assert_allclose(ro, om.swiglu(om.rmsnorm(x, lay.gamma), lay.w1[0], lay.w2[0], lay.w3[0]), rtol=1e-14)
+
+
+def test_near_tie_adoption_rule():
+    lay = _layer(8, 8, 4, 2, 8, 0, seed=4)
+    x = rng(8).standard_normal((8, 8))
+    r0 = om.route(om.rmsnorm(x, lay.gamma), lay.w_router, 2)
+    # a 'GPU' answer that differs from the oracle only on excluded tokens is adopted
+    r, excl = om.adopt_router(lay, x, r0.idx, margin=10.0)   # every token excluded
+    assert excl.all()
+    np.testing.assert_array_equal(r.idx, r0.idx)
+    r, excl = om.adopt_router(lay, x, r0.idx, margin=0.0)
+    assert not excl.any()
+
+
+def test_synth_bf16_roundtrip_and_layer():
+    # bf16 spacing at 1 is 2^-7: 1+2^-7 exact; 1+2^-8 and 1+3*2^-8 are ties -> even mantissa
+    a = np.array([1.0, 1.0078125, 1.00390625, 1.01171875, -3.5, 1e-3], np.float32)
+    b = synth.f32_to_bf16_bits(a)
+    back = synth.bf16_bits_to_f32(b)
+    np.testing.assert_array_equal(back[:5], np.array([1.0, 1.0078125, 1.0, 1.015625, -3.5], np.float32))
+    assert abs(back[5] - 1e-3) / 1e-3 < 2 ** -8
+    w = synth.moe_weights(synth.CONFIGS["tiny"], seed=0)
+    lay = om.layer_from_synth(w, 2)
+    assert lay.w1.shape == (4, 128, 64) and lay.w3.shape == (4, 64, 128)
+    np.testing.assert_array_equal(lay.w1[1], synth.bf16_bits_to_f64(w.w1[1]))
+    # experts regenerate identically when drawn per rank slice
+    w2 = synth.moe_weights(synth.CONFIGS["tiny"], seed=0, e0=2, e_loc=2)
+    np.testing.assert_array_equal(w2.w3, w.w3[2:4])
