@@ -1,0 +1,227 @@
+/*
+ * fsc.h — C ABI of libfsc: the expert-parallel MoE block forward of
+ * FarSkip-Collective (arxiv 2511.11505) for NVIDIA B200 (sm_100a).
+ *
+ * Citations: PAPER.md = the paper text (/root/reference/PAPER.md, "P:<line>"),
+ * readings C-amb-n = DESIGN.md "Readings of the paper".
+ *
+ * The operation:
+ *   xn   = RMSNorm(x_in; gamma)                        ("layer-norm", C-amb-5)
+ *   S,g  = top-k of softmax(xn W_R^T), renormalised    (G(A) = s(A W_R^T), C-amb-2/3)
+ *   Dispatch: copies of xn rows to the ranks owning their experts
+ *   y    = SwiGLU_e(row) = (row W1_e^T * SiLU(row W2_e^T)) W3_e^T  (C-amb-4)
+ *   Combine: y rows back to their source rank, routed[t] = sum_j g_tj y_tj
+ *   shared = SwiGLU_shared(xn) over all tokens
+ *   Regular / blocking (Eq. 6):  out = (x_in + shared) + routed
+ *   FarSkip:  attn-in_{k+1} = partial += shared  (compute starts at once),
+ *                         mlp-in_{k+1}  = partial + routed   (far-skipped, fsc_moe_wait)
+ *
+ * Conventions for every entry point:
+ *  - All tensor pointers are DEVICE pointers owned by the caller, 16-byte
+ *    aligned, row-major, contiguous; fp32 = float, bf16 = uint16 bit patterns.
+ *  - `stream` is a cudaStream_t passed as void*; all work is enqueued on it in
+ *    stream order and the call returns without synchronising, except the
+ *    *_host entry points, which synchronise before returning.
+ *  - Return value: FSC_OK (0) or a negative fsc_status; fsc_last_error() gives
+ *    the message. Validation happens before anything is enqueued. CUDA or
+ *    transport failures are sticky for the context.
+ *  - A context is bound to one process, one GPU and one EP rank; it is not
+ *    thread-safe. The library owns only its workspace (sized once, at
+ *    fsc_init, for max_cfg), its internal streams and events.
+ */
+#ifndef FSC_H_
+#define FSC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FSC_API __attribute__((visibility("default")))
+#else
+#define FSC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fsc_ctx fsc_ctx;
+typedef struct fsc_handle_s* fsc_handle; /* a pending FarSkip combine (cf. P:208 handle dict) */
+
+typedef enum {
+  FSC_OK = 0,
+  FSC_ERR_CONFIG = -1,    /* E % P != 0, k not in [1,E], d % 64, c % 64, T > max_tokens, ... */
+  FSC_ERR_SHAPE = -2,     /* null / misaligned pointer, bad L or modes */
+  FSC_ERR_CUDA = -3,      /* CUDA runtime error (sticky) */
+  FSC_ERR_COMM = -4,      /* EP transport error (sticky) */
+  FSC_ERR_NONFINITE = -5, /* debug finiteness check failed */
+  FSC_ERR_STATE = -6      /* handle misuse: waited twice, FarSkip depth > 1, ... */
+} fsc_status;
+
+/* Per-layer residual wiring. */
+enum { FSC_REGULAR = 0, FSC_HYBRID = 1 };
+/* Stream schedule of the stack (P:103 vs P:198). */
+enum { FSC_BLOCKING = 0, FSC_OVERLAPPED = 1 };
+
+/* MoE layer shape. d % 64 == 0, ffn % 64 == 0, shared_ffn % 64 == 0 (0 = no shared
+ * expert; n shared experts = one SwiGLU of concatenated width, C-amb-7),
+ * 1 <= top_k <= n_experts <= 128, n_experts % ep_size == 0 (C-amb-9). */
+typedef struct {
+  int d;
+  int n_experts;
+  int top_k;
+  int ffn;
+  int shared_ffn;
+  int max_tokens; /* T per rank per call (workspace bound) */
+  float rms_eps;  /* 1e-6 (C-amb-5) */
+} fsc_moe_config;
+
+/* One MoE layer's weights on this rank. Routed experts are this rank's local
+ * experts [rank*E/P, (rank+1)*E/P) (contiguous placement, C-amb-9).
+ *   gamma    fp32 [d]               RMSNorm weight
+ *   w_router fp32 [E, d]            router W_R (replicated on every rank)
+ *   w1       bf16 [E_loc, c, d]     up   (W1 of P:73-76)
+ *   w2       bf16 [E_loc, c, d]     gate (W2; SiLU branch)
+ *   w3       bf16 [E_loc, d, c]     down (W3)
+ *   ws1/ws2  bf16 [c_s, d], ws3 bf16 [d, c_s]   shared expert, or NULL when c_s == 0 */
+typedef struct {
+  const float* gamma;
+  const float* w_router;
+  const void* w1;
+  const void* w2;
+  const void* w3;
+  const void* ws1;
+  const void* ws2;
+  const void* ws3;
+} fsc_moe_weights;
+
+/* Optional outputs for tests (any may be NULL). Shapes per rank:
+ *   topk_idx int32 [T,k] (ascending expert id per token), topk_w fp32 [T,k],
+ *   counts int32 [E] (copies per global expert sent by this rank),
+ *   pos int32 [T,k] (row of copy (t,j) in this rank's expert-sorted send buffer),
+ *   logits fp32 [T,E] (fp32 router logits before near-tie refinement),
+ *   shared_out fp32 [T,d], routed_out fp32 [T,d] (computed separately),
+ *   n_refined int32 [1] device counter of tokens re-selected in fp64 (accumulates). */
+typedef struct {
+  int* topk_idx;
+  float* topk_w;
+  int* counts;
+  int* pos;
+  float* logits;
+  float* shared_out;
+  float* routed_out;
+  int* n_refined;
+} fsc_moe_debug;
+
+/* Caller hook invoked by fsc_moe_forward_farskip while a collective is in flight:
+ * phase 0 = dispatch in flight (enqueue e.g. attention part (b), P:198 step 5),
+ * phase 1 = combine in flight (before the shared expert, P:198 step 8).
+ * `stream` is the compute stream (cudaStream_t as void*). */
+typedef void (*fsc_overlap_cb)(void* user, int phase, void* stream);
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Size in bytes of the transport bootstrap blob each rank exports (0 when ep_size == 1). */
+FSC_API size_t fsc_bootstrap_size(void);
+
+/* Create a context for EP rank `rank` of `ep_size` on CUDA device `device`;
+ * allocates the workspace for max_cfg (worst-case received rows
+ * ep_size * max_tokens * min(top_k, E/ep_size)). For ep_size > 1 the caller then
+ * exchanges blobs: fsc_bootstrap_export on every rank, an all-gather of the
+ * blobs (e.g. torch.distributed), and fsc_bootstrap_import with the P blobs in
+ * rank order. Errors: FSC_ERR_CONFIG for an invalid max_cfg/rank, FSC_ERR_CUDA. */
+FSC_API int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const fsc_moe_config* max_cfg);
+FSC_API int fsc_bootstrap_export(fsc_ctx* ctx, void* blob /* fsc_bootstrap_size() bytes */);
+FSC_API int fsc_bootstrap_import(fsc_ctx* ctx, const void* blobs /* ep_size * fsc_bootstrap_size() bytes */);
+FSC_API int fsc_finalize(fsc_ctx* ctx);
+FSC_API const char* fsc_last_error(const fsc_ctx* ctx);
+/* Persistent-grid size used by the GEMMs (<= 148); lower values leave SMs to
+ * co-running comm kernels ("communication operations only utilizing a
+ * fraction of the total available units"). */
+FSC_API int fsc_set_gemm_ctas(fsc_ctx* ctx, int n);
+
+/* ---------------------------------------------------------------- MoE sub-block */
+
+/* Regular (blocking) MoE sub-block, Eq. 6, P:103 steps 3-6:
+ *   out[T,d] = (x_in + shared(xn)) + routed(xn),  fp32, out may alias x_in.
+ * All collectives are waited on inside, in stream order. */
+FSC_API int fsc_moe_forward_blocking(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, float* out,
+                             const fsc_moe_debug* dbg, void* stream);
+
+/* Same as fsc_moe_forward_blocking but x_in/out are HOST buffers (pinned for
+ * speed): H2D copy, forward, D2H copy, then the stream is synchronised. */
+FSC_API int fsc_moe_forward_blocking_host(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in_host,
+                                  float* out_host, void* stream);
+
+/* FarSkip MoE sub-block (schedule P:198 steps 3-8):
+ *   x_in          = mlp-in_k = o_{k-1}        fp32 [T,d]
+ *   partial_inout = attn-in_{k+1} in progress: on entry (mlp-in_k + attn-out_k),
+ *                   on return (in stream order) += shared-exp-out_k  (C-amb-12)
+ * The routed output stays pending in *h until fsc_moe_wait. At most one
+ * handle may be outstanding per context (FSC_ERR_STATE otherwise). */
+FSC_API int fsc_moe_forward_farskip(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, float* partial_inout,
+                            fsc_overlap_cb cb, void* user, fsc_handle* h, const fsc_moe_debug* dbg, void* stream);
+
+/* Complete a FarSkip handle: waits (in stream order) for its combine and writes
+ *   full_out = partial_in + routed-exp-out_k   (= mlp-in_{k+1} = o_k)
+ * full_out may alias partial_in. FSC_ERR_STATE if h was already waited. */
+FSC_API int fsc_moe_wait(fsc_ctx* ctx, fsc_handle h, const float* partial_in, float* full_out, void* stream);
+
+/* ---------------------------------------------------------------- stack */
+
+/* Attention filler weights (causal GQA + RoPE, C-amb-18):
+ *   gamma fp32 [d]; w_qkv bf16 [(Hq + 2 Hkv) * hd, d] (q heads, k heads, v heads);
+ *   w_o bf16 [d, Hq * hd]; hd in {64, 128}... see DESIGN.md. */
+typedef struct {
+  const float* gamma;
+  const void* w_qkv;
+  const void* w_o;
+  int n_heads;
+  int n_kv_heads;
+  int head_dim;
+  float rope_theta;
+} fsc_attn_weights;
+
+/* Optional per-layer fp32 [T,d] activations; any pointer may be NULL. */
+typedef struct {
+  float* attn_in;
+  float* mlp_in;
+  float* attn_out;
+  float* shared_out;
+  float* routed_out;
+  float* o;
+} fsc_act_cache;
+
+/* L-layer stack o_0 -> o_L (fp32 [T,d]), T tokens packed as sequences of
+ * seq_len (T % seq_len == 0). modes[k] in {FSC_REGULAR, FSC_HYBRID} per layer
+ * (partial conversion allowed); schedule FSC_BLOCKING serialises every
+ * collective, FSC_OVERLAPPED runs the P:198 order with collectives on the comm
+ * stream. attn/moe are arrays of L layers; cache is NULL or an array of L. */
+FSC_API int fsc_layer_stack_forward(fsc_ctx* ctx, const fsc_attn_weights* attn, const fsc_moe_weights* moe, int L, int T,
+                            int seq_len, const int* modes, int schedule, const float* o0, float* oL,
+                            const fsc_act_cache* cache, void* stream);
+
+/* ---------------------------------------------------------------- op-level entry points (tests, bench) */
+
+/* K1: xn bf16 [T,d], topk_idx int32 [T,k], topk_w fp32 [T,k], logits fp32 [T,E] or NULL. */
+FSC_API int fsc_op_router(fsc_ctx* ctx, const float* x, const float* gamma, const float* w_router, int T, int d, int E,
+                  int k, void* xn, int* topk_idx, float* topk_w, float* logits, int* n_refined, void* stream);
+/* K2: counts int32 [E], offsets int32 [E+1], pos int32 [T,k], src_row int32 [T*k]. */
+FSC_API int fsc_op_perm_maps(fsc_ctx* ctx, const int* topk_idx, int T, int k, int E, int* counts, int* offsets, int* pos,
+                     int* src_row, void* stream);
+/* K3: xs[p] = xn[src_row[p]], bf16 rows of d, p < R. */
+FSC_API int fsc_op_permute(fsc_ctx* ctx, const void* xn, const int* src_row, void* xs, int R, int d, void* stream);
+/* K4: grouped GEMM over G groups with device counts [G] (NULL -> one group of m_total rows).
+ *   epi 0: out bf16 [M, N] = A B0_g^T             (B0 [G*N, K])
+ *   epi 1: out bf16 [M, N] = (A B0_g^T) * SiLU(A B1_g^T)   (B0 = W1, B1 = W2, each [G*N, K])
+ *   epi 2: out fp32 [M, N] = resid + A B0_g^T (resid may be NULL -> 0, may alias out) */
+FSC_API int fsc_op_grouped_gemm(fsc_ctx* ctx, int epi, const void* A, long a_rows, const void* B0, const void* B1, int G,
+                        const int* counts, int m_total, int N, int K, void* out, const float* resid, void* stream);
+/* K5: out fp32 [T,d] = resid + sum_j w[t,j] y[pos[t,j]] (resid may be NULL -> 0). */
+FSC_API int fsc_op_unpermute(fsc_ctx* ctx, const void* y, const int* pos, const float* w, const float* resid, float* out,
+                     int T, int k, int d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSC_H_ */

@@ -1,0 +1,70 @@
+// Internal definition of the opaque fsc_ctx (include/fsc.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fsc.h"
+
+struct fsc_handle_s {
+  fsc_ctx* ctx;
+  int T;
+  int live;
+  float* dbg_routed;
+};
+
+struct fsc_peer_state;  // transport.cu
+
+struct fsc_ctx {
+  int rank = 0, ep = 1, device = 0;
+  fsc_moe_config cfg{};
+  int e_loc = 0;
+  long max_recv = 0;
+  int gemm_ctas = 148;
+  int sticky = 0;
+  char err[512] = {0};
+
+  // per-call workspace (device), sized for cfg at fsc_init
+  uint16_t* xn = nullptr;      // bf16 [T, d]        normalised tokens
+  int* topk_idx = nullptr;     // [T, k]
+  float* topk_w = nullptr;     // [T, k]
+  int* pos = nullptr;          // [T, k]             row of copy (t,j) in the send layout
+  int* src_row = nullptr;      // [T*k]              token of send row p
+  int* hist = nullptr;         // [chunks, E]
+  int* base = nullptr;         // [chunks, E]
+  int* counts = nullptr;       // [E]                copies per global expert (this rank)
+  int* offsets = nullptr;      // [E+1]
+  uint16_t* xs = nullptr;      // bf16 [T*k, d]      expert-sorted send buffer
+  uint16_t* h = nullptr;       // bf16 [max_recv, c] SwiGLU activations
+  uint16_t* y = nullptr;       // bf16 [T*k, d]      expert outputs in the send layout (EP=1)
+  uint16_t* hs = nullptr;      // bf16 [T, c_s]      shared-expert activations
+  float* tmp = nullptr;        // fp32 [T, d]
+  float* io_in = nullptr;      // fp32 [T, d]        staging for the *_host entry point
+  float* io_out = nullptr;
+
+  // EP > 1: receive side (transport.cu); symmetric across ranks
+  uint16_t* xr = nullptr;      // bf16 [max_recv, d] received rows, expert-major then source
+  uint16_t* yr = nullptr;      // bf16 [max_recv, d] expert outputs in the receive layout
+  uint16_t* ys = nullptr;      // bf16 [T*k, d]      combined rows back in the send layout
+  int* recv_counts = nullptr;  // [E_loc]            rows received per local expert
+  long recv_rows_cap = 0;
+  fsc_peer_state* peer = nullptr;
+
+  cudaStream_t comm = nullptr;  // high-priority communication stream
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+
+  int pending = 0;
+  fsc_handle_s handle{};
+};
+
+void fsc_set_error(fsc_ctx* c, const char* fmt, ...);
+
+// transport (EP > 1). All return fsc_status.
+size_t fsc_transport_blob_size();
+int fsc_transport_init(fsc_ctx* ctx);
+int fsc_transport_export(fsc_ctx* ctx, void* blob);
+int fsc_transport_import(fsc_ctx* ctx, const void* blobs);
+void fsc_transport_finalize(fsc_ctx* ctx);
+int fsc_transport_dispatch(fsc_ctx* ctx, int T, cudaStream_t s);
+int fsc_transport_dispatch_wait(fsc_ctx* ctx, cudaStream_t s);
+int fsc_transport_combine(fsc_ctx* ctx, int T, cudaStream_t s);
+int fsc_transport_combine_wait(fsc_ctx* ctx, cudaStream_t s);

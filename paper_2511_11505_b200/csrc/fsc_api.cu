@@ -1,0 +1,387 @@
+// libfsc C ABI (include/fsc.h): context, workspace, argument validation and the
+// two MoE schedules of the paper (blocking; FarSkip).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+
+#include "../../include/fsc.h"
+#include "common.cuh"
+#include "ctx.h"
+#include "kernels.h"
+
+using namespace fsc;
+
+// ---------------------------------------------------------------------------- helpers
+
+void fsc_set_error(fsc_ctx* c, const char* fmt, ...) {
+  if (!c) return;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(c->err, sizeof(c->err), fmt, ap);
+  va_end(ap);
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e__ = (call);                                                                 \
+    if (e__ != cudaSuccess) {                                                                 \
+      fsc_set_error(ctx, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e__)); \
+      ctx->sticky = FSC_ERR_CUDA;                                                             \
+      return FSC_ERR_CUDA;                                                                    \
+    }                                                                                         \
+  } while (0)
+
+#define REQUIRE(cond, code, ...)            \
+  do {                                      \
+    if (!(cond)) {                          \
+      fsc_set_error(ctx, __VA_ARGS__);      \
+      return code;                          \
+    }                                       \
+  } while (0)
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static int check_cfg(const fsc_moe_config* c, int ep, char* err, size_t n) {
+  if (!c) { snprintf(err, n, "null config"); return FSC_ERR_CONFIG; }
+  if (c->d <= 0 || c->d % 64) { snprintf(err, n, "d=%d must be a positive multiple of 64", c->d); return FSC_ERR_CONFIG; }
+  if (c->n_experts < 1 || c->n_experts > 128) { snprintf(err, n, "n_experts=%d outside [1,128]", c->n_experts); return FSC_ERR_CONFIG; }
+  if (c->top_k < 1 || c->top_k > c->n_experts) { snprintf(err, n, "top_k=%d outside [1,E]", c->top_k); return FSC_ERR_CONFIG; }
+  if (c->ffn <= 0 || c->ffn % 64) { snprintf(err, n, "ffn=%d must be a positive multiple of 64", c->ffn); return FSC_ERR_CONFIG; }
+  if (c->shared_ffn < 0 || c->shared_ffn % 64) { snprintf(err, n, "shared_ffn=%d must be a multiple of 64", c->shared_ffn); return FSC_ERR_CONFIG; }
+  if (c->max_tokens < 0) { snprintf(err, n, "max_tokens < 0"); return FSC_ERR_CONFIG; }
+  if (ep < 1 || c->n_experts % ep) { snprintf(err, n, "n_experts=%d not divisible by ep_size=%d (C-amb-9)", c->n_experts, ep); return FSC_ERR_CONFIG; }
+  return FSC_OK;
+}
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t n) {
+  if (n == 0) n = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+}
+
+// ---------------------------------------------------------------------------- lifecycle
+
+extern "C" size_t fsc_bootstrap_size(void) { return fsc_transport_blob_size(); }
+
+extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const fsc_moe_config* max_cfg) {
+  if (!out) return FSC_ERR_SHAPE;
+  *out = nullptr;
+  char err[256];
+  int rc = check_cfg(max_cfg, ep_size, err, sizeof(err));
+  if (rc) { fprintf(stderr, "fsc_init: %s\n", err); return rc; }
+  if (rank < 0 || rank >= ep_size) { fprintf(stderr, "fsc_init: rank %d outside [0,%d)\n", rank, ep_size); return FSC_ERR_CONFIG; }
+  fsc_ctx* ctx = new (std::nothrow) fsc_ctx();
+  if (!ctx) return FSC_ERR_CUDA;
+  ctx->rank = rank;
+  ctx->ep = ep_size;
+  ctx->device = device;
+  ctx->cfg = *max_cfg;
+  ctx->e_loc = max_cfg->n_experts / ep_size;
+  ctx->gemm_ctas = kNumSMs;
+  *out = ctx;
+  CK(cudaSetDevice(device));
+  const fsc_moe_config& c = ctx->cfg;
+  const long T = c.max_tokens, d = c.d, k = c.top_k, E = c.n_experts;
+  const long per_src = T * (k < ctx->e_loc ? k : ctx->e_loc);
+  ctx->max_recv = per_src * ep_size;  // worst-case rows received (dropless, C-amb-9)
+  const long nch = perm_chunks((int)T);
+  CK(dalloc(&ctx->xn, T * d));
+  CK(dalloc(&ctx->topk_idx, T * k));
+  CK(dalloc(&ctx->topk_w, T * k));
+  CK(dalloc(&ctx->pos, T * k));
+  CK(dalloc(&ctx->src_row, T * k));
+  CK(dalloc(&ctx->hist, nch * E));
+  CK(dalloc(&ctx->base, nch * E));
+  CK(dalloc(&ctx->counts, E));
+  CK(dalloc(&ctx->offsets, E + 1));
+  CK(dalloc(&ctx->xs, (T * k > ctx->max_recv ? T * k : ctx->max_recv) * d));
+  CK(dalloc(&ctx->h, ctx->max_recv * (long)c.ffn));
+  CK(dalloc(&ctx->y, (T * k > ctx->max_recv ? T * k : ctx->max_recv) * d));
+  if (c.shared_ffn) CK(dalloc(&ctx->hs, T * (long)c.shared_ffn));
+  CK(dalloc(&ctx->tmp, T * d));
+  CK(dalloc(&ctx->io_in, T * d));
+  CK(dalloc(&ctx->io_out, T * d));
+  CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, -5));
+  CK(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
+  rc = fsc_transport_init(ctx);
+  if (rc) return rc;
+  return FSC_OK;
+}
+
+extern "C" int fsc_bootstrap_export(fsc_ctx* ctx, void* blob) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  return fsc_transport_export(ctx, blob);
+}
+
+extern "C" int fsc_bootstrap_import(fsc_ctx* ctx, const void* blobs) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  return fsc_transport_import(ctx, blobs);
+}
+
+extern "C" int fsc_finalize(fsc_ctx* ctx) {
+  if (!ctx) return FSC_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  fsc_transport_finalize(ctx);
+  void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (ctx->comm) cudaStreamDestroy(ctx->comm);
+  if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+  if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+  delete ctx;
+  return FSC_OK;
+}
+
+extern "C" const char* fsc_last_error(const fsc_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+
+extern "C" int fsc_set_gemm_ctas(fsc_ctx* ctx, int n) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(n >= 1 && n <= kNumSMs, FSC_ERR_CONFIG, "gemm ctas %d outside [1,148]", n);
+  ctx->gemm_ctas = n;
+  return FSC_OK;
+}
+
+// ---------------------------------------------------------------------------- MoE pieces
+
+static int validate_call(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, const void* out) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  if (ctx->sticky) return ctx->sticky;
+  REQUIRE(w && w->gamma && w->w_router && w->w1 && w->w2 && w->w3, FSC_ERR_SHAPE, "null weight pointer");
+  REQUIRE(ctx->cfg.shared_ffn == 0 || (w->ws1 && w->ws2 && w->ws3), FSC_ERR_SHAPE, "null shared-expert weight");
+  REQUIRE(T >= 0 && T <= ctx->cfg.max_tokens, FSC_ERR_CONFIG, "T=%d outside [0,max_tokens=%d]", T,
+          ctx->cfg.max_tokens);
+  REQUIRE(T == 0 || (x_in && out), FSC_ERR_SHAPE, "null activation pointer");
+  REQUIRE(aligned16(x_in) && aligned16(out) && aligned16(w->w1) && aligned16(w->w2) && aligned16(w->w3) &&
+              aligned16(w->gamma) && aligned16(w->w_router),
+          FSC_ERR_SHAPE, "pointers must be 16-byte aligned");
+  return FSC_OK;
+}
+
+// Steps 3-4 of P:198 (gate + dispatch start) and 6 (routed experts). On return
+// the routed expert outputs y are complete in this rank's receive layout and,
+// for EP > 1, already pushed back toward their source ranks (combine started).
+static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in,
+                                 const fsc_moe_debug* dbg, cudaStream_t s, fsc_overlap_cb cb, void* user) {
+  const fsc_moe_config& c = ctx->cfg;
+  const int d = c.d, E = c.n_experts, k = c.top_k;
+  RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
+                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr};
+  CK(launch_router(rl, s));
+  PermLaunch pl{ctx->topk_idx, T, k, E, ctx->hist, ctx->base, ctx->counts, ctx->offsets, ctx->pos, ctx->src_row};
+  CK(launch_perm_maps(pl, s));
+  if (dbg) {
+    if (dbg->topk_idx) CK(cudaMemcpyAsync(dbg->topk_idx, ctx->topk_idx, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
+    if (dbg->topk_w) CK(cudaMemcpyAsync(dbg->topk_w, ctx->topk_w, sizeof(float) * T * k, cudaMemcpyDeviceToDevice, s));
+    if (dbg->counts) CK(cudaMemcpyAsync(dbg->counts, ctx->counts, sizeof(int) * E, cudaMemcpyDeviceToDevice, s));
+    if (dbg->pos) CK(cudaMemcpyAsync(dbg->pos, ctx->pos, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
+  }
+  // Dispatch: permute into the expert-sorted send buffer, then move
+  // rows to the owning ranks. At EP=1 the permuted buffer is the receive buffer.
+  const int R = T * k;
+  const uint16_t* recv = ctx->xs;
+  long recv_rows = R;
+  const int* recv_counts = ctx->counts;
+  if (ctx->ep == 1) {
+    CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, s));
+  } else {
+    int rc = fsc_transport_dispatch(ctx, T, s);
+    if (rc) return rc;
+    recv = ctx->xr;
+    recv_rows = ctx->recv_rows_cap;
+    recv_counts = ctx->recv_counts;
+  }
+  if (cb) cb(user, 0, s);  // P:198 step 5: attention part (b) while dispatch is in flight
+  if (ctx->ep > 1) {
+    int rc = fsc_transport_dispatch_wait(ctx, s);
+    if (rc) return rc;
+  }
+  // Routed experts (P:198 step 6): GEMM1 + SwiGLU, GEMM2
+  GemmLaunch g1{};
+  g1.A = recv; g1.a_rows = recv_rows; g1.B0 = w->w1; g1.B1 = w->w2; g1.b_rows = (long)ctx->e_loc * c.ffn;
+  g1.b_group_rows = c.ffn; g1.K = d; g1.N = c.ffn; g1.G = ctx->e_loc; g1.counts = recv_counts; g1.m_total = 0;
+  g1.out = ctx->h; g1.ldo = c.ffn; g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas;
+  CK(launch_grouped_gemm(g1, s));
+  GemmLaunch g2{};
+  g2.A = ctx->h; g2.a_rows = recv_rows; g2.B0 = w->w3; g2.B1 = nullptr; g2.b_rows = (long)ctx->e_loc * d;
+  g2.b_group_rows = d; g2.K = c.ffn; g2.N = d; g2.G = ctx->e_loc; g2.counts = recv_counts; g2.m_total = 0;
+  g2.out = (ctx->ep == 1) ? ctx->y : ctx->yr; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas;
+  CK(launch_grouped_gemm(g2, s));
+  if (ctx->ep > 1) {
+    int rc = fsc_transport_combine(ctx, T, s);  // P:198 step 7: start Combine
+    if (rc) return rc;
+  }
+  return FSC_OK;
+}
+
+// Shared expert (P:100-101, P:198 step 8): out = resid + SwiGLU_shared(xn).
+static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* resid, float* out,
+                      const fsc_moe_debug* dbg, cudaStream_t s) {
+  const fsc_moe_config& c = ctx->cfg;
+  const int d = c.d;
+  if (c.shared_ffn == 0) {
+    if (dbg && dbg->shared_out) CK(cudaMemsetAsync(dbg->shared_out, 0, sizeof(float) * T * (long)d, s));
+    CK(launch_copy_f32(resid, out, (long)T * d, s));
+    return FSC_OK;
+  }
+  GemmLaunch g1{};
+  g1.A = ctx->xn; g1.a_rows = T; g1.B0 = w->ws1; g1.B1 = w->ws2; g1.b_rows = c.shared_ffn; g1.b_group_rows = c.shared_ffn;
+  g1.K = d; g1.N = c.shared_ffn; g1.G = 1; g1.counts = nullptr; g1.m_total = T; g1.out = ctx->hs; g1.ldo = c.shared_ffn;
+  g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas;
+  CK(launch_grouped_gemm(g1, s));
+  GemmLaunch g2{};
+  g2.A = ctx->hs; g2.a_rows = T; g2.B0 = w->ws3; g2.B1 = nullptr; g2.b_rows = d; g2.b_group_rows = d;
+  g2.K = c.shared_ffn; g2.N = d; g2.G = 1; g2.counts = nullptr; g2.m_total = T; g2.out = out; g2.ldo = d;
+  g2.resid = resid; g2.ldr = d; g2.epi = EPI_RESID_F32; g2.num_ctas = ctx->gemm_ctas;
+  CK(launch_grouped_gemm(g2, s));
+  if (dbg && dbg->shared_out) {
+    g2.out = dbg->shared_out; g2.resid = nullptr;
+    CK(launch_grouped_gemm(g2, s));
+  }
+  return FSC_OK;
+}
+
+// Gate-weighted unpermute (+ far-skip residual add), after the combine landed.
+static int moe_finish(fsc_ctx* ctx, int T, const float* resid, float* out, const fsc_moe_debug* dbg, cudaStream_t s) {
+  const fsc_moe_config& c = ctx->cfg;
+  const uint16_t* ysrc = ctx->y;
+  if (ctx->ep > 1) {
+    int rc = fsc_transport_combine_wait(ctx, s);
+    if (rc) return rc;
+    ysrc = ctx->ys;
+  }
+  CK(launch_unpermute(ysrc, ctx->pos, ctx->topk_w, resid, out, T, c.top_k, c.d, s));
+  if (dbg && dbg->routed_out)
+    CK(launch_unpermute(ysrc, ctx->pos, ctx->topk_w, nullptr, dbg->routed_out, T, c.top_k, c.d, s));
+  return FSC_OK;
+}
+
+// ---------------------------------------------------------------------------- MoE entry points
+
+extern "C" int fsc_moe_forward_blocking(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, float* out,
+                                        const fsc_moe_debug* dbg, void* stream) {
+  int rc = validate_call(ctx, w, T, x_in, out);
+  if (rc) return rc;
+  REQUIRE(!ctx->pending, FSC_ERR_STATE, "a FarSkip handle is outstanding");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (T == 0 && ctx->ep == 1) return FSC_OK;
+  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr);
+  if (rc) return rc;
+  // Regular order (C-amb-12): tmp = x_in + shared; out = tmp + routed.
+  rc = moe_shared(ctx, w, T, x_in, ctx->tmp, dbg, s);
+  if (rc) return rc;
+  return moe_finish(ctx, T, ctx->tmp, out, dbg, s);
+}
+
+extern "C" int fsc_moe_forward_blocking_host(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in_host,
+                                             float* out_host, void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(T == 0 || (x_in_host && out_host), FSC_ERR_SHAPE, "null host buffer");
+  REQUIRE(T >= 0 && T <= ctx->cfg.max_tokens, FSC_ERR_CONFIG, "T=%d outside [0,max_tokens]", T);
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t bytes = sizeof(float) * (size_t)T * ctx->cfg.d;
+  CK(cudaMemcpyAsync(ctx->io_in, x_in_host, bytes, cudaMemcpyHostToDevice, s));
+  int rc = fsc_moe_forward_blocking(ctx, w, T, ctx->io_in, ctx->io_out, nullptr, stream);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out_host, ctx->io_out, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return FSC_OK;
+}
+
+extern "C" int fsc_moe_forward_farskip(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in,
+                                       float* partial_inout, fsc_overlap_cb cb, void* user, fsc_handle* h,
+                                       const fsc_moe_debug* dbg, void* stream) {
+  int rc = validate_call(ctx, w, T, x_in, partial_inout);
+  if (rc) return rc;
+  REQUIRE(h, FSC_ERR_SHAPE, "null handle pointer");
+  REQUIRE(!ctx->pending, FSC_ERR_STATE, "FarSkip pipeline depth is 1: wait the outstanding handle first");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, cb, user);
+  if (rc) return rc;
+  if (cb) cb(user, 1, s);  // combine in flight
+  // P:198 step 8 and C-amb-12: attn-in_{k+1} = (mlp-in_k + attn-out_k) + shared-out_k
+  rc = moe_shared(ctx, w, T, partial_inout, partial_inout, dbg, s);
+  if (rc) return rc;
+  ctx->handle.ctx = ctx;
+  ctx->handle.T = T;
+  ctx->handle.live = 1;
+  ctx->handle.dbg_routed = dbg ? dbg->routed_out : nullptr;
+  ctx->pending = 1;
+  *h = &ctx->handle;
+  return FSC_OK;
+}
+
+extern "C" int fsc_moe_wait(fsc_ctx* ctx, fsc_handle h, const float* partial_in, float* full_out, void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(h && h == &ctx->handle, FSC_ERR_STATE, "unknown handle");
+  REQUIRE(h->live && ctx->pending, FSC_ERR_STATE, "handle already waited");
+  REQUIRE(h->T == 0 || (partial_in && full_out), FSC_ERR_SHAPE, "null activation pointer");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  h->live = 0;
+  ctx->pending = 0;
+  fsc_moe_debug dbg{};
+  dbg.routed_out = h->dbg_routed;
+  return moe_finish(ctx, h->T, partial_in, full_out, dbg.routed_out ? &dbg : nullptr, s);
+}
+
+// ---------------------------------------------------------------------------- op-level entry points
+
+extern "C" int fsc_op_router(fsc_ctx* ctx, const float* x, const float* gamma, const float* w_router, int T, int d,
+                             int E, int k, void* xn, int* topk_idx, float* topk_w, float* logits, int* n_refined,
+                             void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(d % 64 == 0 && E >= 1 && E <= 128 && k >= 1 && k <= E, FSC_ERR_CONFIG, "bad router shape");
+  RouterLaunch rl{x, gamma, w_router, T, d, E, k, ctx->cfg.rms_eps, static_cast<uint16_t*>(xn), topk_idx, topk_w,
+                  logits, n_refined};
+  CK(launch_router(rl, static_cast<cudaStream_t>(stream)));
+  return FSC_OK;
+}
+
+extern "C" int fsc_op_perm_maps(fsc_ctx* ctx, const int* topk_idx, int T, int k, int E, int* counts, int* offsets,
+                                int* pos, int* src_row, void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(T <= ctx->cfg.max_tokens && E <= ctx->cfg.n_experts, FSC_ERR_CONFIG, "perm maps beyond workspace");
+  PermLaunch pl{topk_idx, T, k, E, ctx->hist, ctx->base, counts, offsets, pos, src_row};
+  CK(launch_perm_maps(pl, static_cast<cudaStream_t>(stream)));
+  return FSC_OK;
+}
+
+extern "C" int fsc_op_permute(fsc_ctx* ctx, const void* xn, const int* src_row, void* xs, int R, int d, void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(d % 8 == 0, FSC_ERR_CONFIG, "d %% 8");
+  CK(launch_permute_rows(static_cast<const uint16_t*>(xn), src_row, static_cast<uint16_t*>(xs), R, d,
+                         static_cast<cudaStream_t>(stream)));
+  return FSC_OK;
+}
+
+extern "C" int fsc_op_grouped_gemm(fsc_ctx* ctx, int epi, const void* A, long a_rows, const void* B0, const void* B1,
+                                   int G, const int* counts, int m_total, int N, int K, void* out, const float* resid,
+                                   void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(epi >= 0 && epi <= 2, FSC_ERR_CONFIG, "epi");
+  REQUIRE(K % 64 == 0 && K > 0 && gemm_pick_bn(epi, N) > 0, FSC_ERR_CONFIG, "GEMM needs K%%64==0 and N%%64==0");
+  REQUIRE(G >= 1 && G <= 256, FSC_ERR_CONFIG, "G outside [1,256]");
+  REQUIRE(epi != 1 || B1, FSC_ERR_SHAPE, "SwiGLU needs B1");
+  GemmLaunch L{};
+  L.A = A; L.a_rows = a_rows; L.B0 = B0; L.B1 = B1; L.b_rows = (long)G * N; L.b_group_rows = N; L.K = K; L.N = N;
+  L.G = G; L.counts = counts; L.m_total = m_total; L.out = out; L.ldo = N; L.resid = resid; L.ldr = N; L.epi = epi;
+  L.num_ctas = ctx->gemm_ctas;
+  CK(launch_grouped_gemm(L, static_cast<cudaStream_t>(stream)));
+  return FSC_OK;
+}
+
+extern "C" int fsc_op_unpermute(fsc_ctx* ctx, const void* y, const int* pos, const float* w, const float* resid,
+                                float* out, int T, int k, int d, void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(d % 8 == 0, FSC_ERR_CONFIG, "d %% 8");
+  CK(launch_unpermute(static_cast<const uint16_t*>(y), pos, w, resid, out, T, k, d, static_cast<cudaStream_t>(stream)));
+  return FSC_OK;
+}

@@ -1,0 +1,359 @@
+// K4: persistent, warp-specialised tcgen05 grouped GEMM for sm_100a.
+//
+// Computes, for every group g (a local expert, "expert"),
+//   D_g = A_g . B_g^T        A_g = rows [row_off[g], row_off[g]+M_g) of A (bf16, K-major)
+//                            B_g = rows [g*N', (g+1)*N') of B       (bf16, K-major)
+// with fp32 accumulation in TMEM and one of three fused epilogues:
+//   EPI_SWIGLU   : h = U * SiLU(G), U from B0 = W1 (up), G from B1 = W2 (gate)
+//                  (sigma = id, g = SiLU on the W2 branch) -> bf16
+//   EPI_BF16     : plain bf16 store (expert down projection W3, the combine payload)
+//   EPI_RESID_F32: out = resid + D in fp32 (shared-expert down projection / o-proj
+//                  into the fp32 residual stream, PAPER.md:166-175 wiring)
+// M_g comes from device-resident counts (no host sync): every CTA rebuilds the
+// per-group row / tile prefix in shared memory and walks a static tile stride.
+//
+// Roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
+// issuer (one elected lane), warps 2..5 = epilogue (TMEM lane quarter = warp%4).
+// Tiles: BM=128 rows x BN cols, BK=64 (one 128-byte swizzle atom of bf16).
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fsc {
+
+namespace {
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kMaxGroups = 256;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct Cfg {
+  static constexpr int HALF = BN / 2;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + 2 * (kMaxGroups + 1) * 4;
+};
+
+FSC_DEVINL float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+struct TileInfo {
+  int g, mb, nb, row0, rows;
+};
+
+FSC_DEVINL TileInfo decode_tile(int t, int n_tiles, int G, const int* s_row_off, const int* s_tile_off) {
+  TileInfo ti;
+  int mt = t / n_tiles;
+  ti.nb = t - mt * n_tiles;
+  int lo = 0, hi = G;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (s_tile_off[mid] <= mt) lo = mid; else hi = mid;
+  }
+  ti.g = lo;
+  ti.mb = mt - s_tile_off[lo];
+  ti.row0 = s_row_off[lo] + ti.mb * BM;
+  int m = s_row_off[lo + 1] - s_row_off[lo];
+  ti.rows = min(BM, m - ti.mb * BM);
+  return ti;
+}
+}  // namespace
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                        const __grid_constant__ CUtensorMap tmB1, GemmParams p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_row_off = reinterpret_cast<int*>(smem + C::STAGES * C::STAGE_BYTES + 256);
+  int* s_tile_off = s_row_off + (kMaxGroups + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int G = p.G;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB0);
+      tma_prefetch_desc(&tmB1);
+      for (int s = 0; s < C::STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&tfull[a], 1);
+        mbar_init(&tempty[a], 4);
+      }
+      fence_barrier_init();
+    }
+  } else if (warp == 1) {
+    tmem_alloc<C::TMEM_COLS>(s_tmem);
+  } else if (warp == 2) {
+    // per-group row and tile prefix sums from the device-resident counts
+    int run_rows = 0, run_tiles = 0;
+    if (lane == 0) { s_row_off[0] = 0; s_tile_off[0] = 0; }
+    for (int base = 0; base < G; base += 32) {
+      int g = base + lane;
+      int m = 0;
+      if (g < G) m = p.counts ? p.counts[g] : p.m_total;
+      int tl = (m + BM - 1) / BM;
+      int im = m, it = tl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int a = __shfl_up_sync(0xffffffff, im, o);
+        int b = __shfl_up_sync(0xffffffff, it, o);
+        if (lane >= o) { im += a; it += b; }
+      }
+      if (g < G) { s_row_off[g + 1] = run_rows + im; s_tile_off[g + 1] = run_tiles + it; }
+      run_rows += __shfl_sync(0xffffffff, im, 31);
+      run_tiles += __shfl_sync(0xffffffff, it, 31);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  const uint32_t tmem_base = *s_tmem;
+  const int n_tiles = (EPI == EPI_SWIGLU) ? p.N / C::HALF : p.N / BN;
+  const int total = s_tile_off[G] * n_tiles;
+  const int kblocks = p.K / BK;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        TileInfo ti = decode_tile(t, n_tiles, G, s_row_off, s_tile_off);
+        int brow0, brow1;
+        if (EPI == EPI_SWIGLU) {
+          brow0 = ti.g * p.b_group_rows + ti.nb * C::HALF;
+          brow1 = brow0;
+        } else {
+          brow0 = ti.g * p.b_group_rows + ti.nb * BN;
+          brow1 = brow0 + C::HALF;
+        }
+        const CUtensorMap* mb1 = (EPI == EPI_SWIGLU) ? &tmB1 : &tmB0;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, ti.row0, kEvictNormal);
+          uint8_t* b = sB + stage * C::B_BYTES;
+          tma_load_2d(b, &tmB0, &full[stage], kb * BK, brow0, kEvictLast);
+          tma_load_2d(b + C::HALF * BK * 2, mb1, &full[stage], kb * BK, brow1, kEvictLast);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc = idesc_bf16_f32(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
+                         (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps 2..5
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      TileInfo ti = decode_tile(t, n_tiles, G, s_row_off, s_tile_off);
+      const int acc = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const bool valid = r < ti.rows;
+      const long grow = (long)ti.row0 + r;
+      const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (EPI == EPI_SWIGLU) {
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + ti.nb * C::HALF;
+#pragma unroll 1
+        for (int c = 0; c < C::HALF; c += 32) {
+          uint32_t u[32], gv[32];
+          tmem_ld32(tb + c, u);
+          tmem_ld32(tb + C::HALF + c, gv);
+          tmem_ld_wait();
+          if (valid) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float h0 = __uint_as_float(u[2 * i]) * silu_f(__uint_as_float(gv[2 * i]));
+              float h1 = __uint_as_float(u[2 * i + 1]) * silu_f(__uint_as_float(gv[2 * i + 1]));
+              pk[i] = pack_bf16x2(h0, h1);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              st_global_v4(out + c + 8 * i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+          }
+        }
+      } else if (EPI == EPI_BF16) {
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + ti.nb * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tb + c, v);
+          tmem_ld_wait();
+          if (valid) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              st_global_v4(out + c + 8 * i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+          }
+        }
+      } else {
+        float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo + ti.nb * BN;
+        const float* res = p.resid ? p.resid + grow * p.ldr + ti.nb * BN : nullptr;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tb + c, v);
+          tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float4 a = res ? *reinterpret_cast<const float4*>(res + c + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+              a.x += __uint_as_float(v[4 * i]);
+              a.y += __uint_as_float(v[4 * i + 1]);
+              a.z += __uint_as_float(v[4 * i + 2]);
+              a.w += __uint_as_float(v[4 * i + 3]);
+              *reinterpret_cast<float4*>(out + c + 4 * i) = a;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------- host
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, cols] map with a {64 cols x box_rows} box, 128B swizzle.
+static bool make_map(CUtensorMap* m, const void* base, long rows, long cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int EPI>
+static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
+  using C = Cfg<BN>;
+  CUtensorMap ma, mb0, mb1;
+  long a_rows = L.a_rows > 0 ? L.a_rows : 1;
+  if (!make_map(&ma, L.A, a_rows, L.K, BM)) return cudaErrorInvalidValue;
+  if (!make_map(&mb0, L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
+  if (!make_map(&mb1, L.B1 ? L.B1 : L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  GemmParams p;
+  p.counts = L.counts;
+  p.G = L.G;
+  p.m_total = L.m_total;
+  p.N = L.N;
+  p.K = L.K;
+  p.b_group_rows = L.b_group_rows;
+  p.out = L.out;
+  p.ldo = L.ldo;
+  p.resid = L.resid;
+  p.ldr = L.ldr;
+  int grid = L.num_ctas > 0 ? L.num_ctas : kNumSMs;
+  grouped_gemm_kernel<BN, EPI><<<grid, kThreads, C::SMEM, s>>>(ma, mb0, mb1, p);
+  return cudaGetLastError();
+}
+
+int gemm_pick_bn(int epi, int N) {
+  if (epi == EPI_SWIGLU) return (N % 128 == 0) ? 256 : (N % 64 == 0 ? 128 : 0);
+  return (N % 256 == 0) ? 256 : (N % 128 == 0 ? 128 : (N % 64 == 0 ? 64 : 0));
+}
+
+cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s) {
+  if (L.G < 1 || L.G > kMaxGroups || L.K % BK || L.K <= 0) return cudaErrorInvalidValue;
+  int bn = gemm_pick_bn(L.epi, L.N);
+  if (!bn) return cudaErrorInvalidValue;
+  if (L.a_rows == 0) return cudaSuccess;
+#define FSC_GEMM_CASE(BNV, EV) \
+  if (bn == BNV && L.epi == EV) return launch_t<BNV, EV>(L, s);
+  FSC_GEMM_CASE(256, EPI_SWIGLU)
+  FSC_GEMM_CASE(128, EPI_SWIGLU)
+  FSC_GEMM_CASE(256, EPI_BF16)
+  FSC_GEMM_CASE(128, EPI_BF16)
+  FSC_GEMM_CASE(64, EPI_BF16)
+  FSC_GEMM_CASE(256, EPI_RESID_F32)
+  FSC_GEMM_CASE(128, EPI_RESID_F32)
+  FSC_GEMM_CASE(64, EPI_RESID_F32)
+#undef FSC_GEMM_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fsc

@@ -1,0 +1,86 @@
+// Internal launch interface of the libfsc kernels (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fsc {
+
+enum { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_RESID_F32 = 2 };
+
+struct GemmParams {
+  const int* counts;  // [G] rows per group (device) or nullptr -> one group of m_total rows
+  int G;
+  int m_total;
+  int N;              // output columns (h columns for SwiGLU)
+  int K;
+  int b_group_rows;   // rows of B0/B1 per group
+  void* out;
+  long ldo;
+  const float* resid;
+  long ldr;
+};
+
+struct GemmLaunch {
+  const void* A;      // bf16 [a_rows, K]
+  long a_rows;
+  const void* B0;     // bf16 [b_rows, K]  (W1 for SwiGLU, else the only B)
+  const void* B1;     // bf16 [b_rows, K]  (W2 for SwiGLU) or nullptr
+  long b_rows;
+  int b_group_rows;
+  int K, N, G;
+  const int* counts;
+  int m_total;
+  void* out;
+  long ldo;
+  const float* resid;
+  long ldr;
+  int epi;
+  int num_ctas;       // persistent grid (<= 148); 0 = all SMs
+};
+
+cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s);
+int gemm_pick_bn(int epi, int N);
+
+// K1: RMSNorm + fp32 router logits + top-k + renormalised gates (+ fp64 near-tie refinement)
+struct RouterLaunch {
+  const float* x;        // [T, d]
+  const float* gamma;    // [d]
+  const float* w_router; // [E, d]
+  int T, d, E, k;
+  float eps;
+  uint16_t* xn;          // bf16 [T, d]
+  int* topk_idx;         // [T, k]
+  float* topk_w;         // [T, k]
+  float* logits;         // optional [T, E]
+  int* n_refined;        // optional device counter
+};
+cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s);
+
+// K2: deterministic histogram / scan / positions
+//   hist   [n_chunks, E] per 32-token chunk; base [n_chunks, E]
+//   counts [E], offsets [E+1], pos [T,k], src_row [T*k]
+struct PermLaunch {
+  const int* topk_idx;
+  int T, k, E;
+  int* hist;
+  int* base;
+  int* counts;
+  int* offsets;
+  int* pos;
+  int* src_row;
+};
+cudaError_t launch_perm_maps(const PermLaunch& L, cudaStream_t s);
+inline int perm_chunks(int T) { return (T + 31) / 32; }
+
+// K3: xs[p] = xn[src_row[p]]  (bf16 rows of d)
+cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t* xs, int R, int d,
+                                cudaStream_t s);
+
+// K5: out[t] = resid[t] + sum_j w[t,j] * y[pos[t,j]]   (fp32 out, bf16 y, slot order)
+cudaError_t launch_unpermute(const uint16_t* y, const int* pos, const float* w, const float* resid,
+                             float* out, int T, int k, int d, cudaStream_t s);
+
+// elementwise helpers
+cudaError_t launch_copy_f32(const float* src, float* dst, long n, cudaStream_t s);
+
+}  // namespace fsc

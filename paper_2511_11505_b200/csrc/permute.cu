@@ -1,0 +1,192 @@
+// K2 (histogram / scan / positions), K3 (permute) and K5 (gate-weighted
+// unpermute + far-skip residual add) of the MoE dispatch path.
+//
+// K2 computes the expert-sorted permutation of the (token, slot) copies that
+// the Dispatch of PAPER.md:96-100 needs ("grouped and mapped ... requiring
+// permutation of A"), deterministically: within an expert, copies keep
+// ascending token order (C-amb-11). Each 32-token chunk is one warp; a warp
+// builds, per expert, the 32-bit mask of its lanes that selected the expert
+// (atomicOr is order independent), so a copy's rank inside its chunk is
+// popc(mask & lanes_below), chunk totals are popc(mask), and a column scan over
+// chunks gives every chunk's base. No result depends on atomic ordering.
+//
+// K5: out[t] = resid[t] + (sum_j w[t,j] * y[pos[t,j]]) with the inner sum
+// started at 0 and taken in slot order (C-amb-12), fp32. In the FarSkip wiring
+// resid = attn-in_{k+1} and out = mlp-in_{k+1} = o_k.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fsc {
+
+namespace {
+constexpr int kMaxE = 256;
+}
+
+__global__ void __launch_bounds__(256) perm_hist_kernel(const int* __restrict__ idx, int T, int k, int E,
+                                                        int* __restrict__ hist, int n_chunks) {
+  __shared__ uint32_t mask[8][kMaxE];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 8 + w;
+  for (int e = lane; e < E; e += 32) mask[w][e] = 0;
+  __syncwarp();
+  if (c >= n_chunks) return;
+  const int t = c * 32 + lane;
+  if (t < T)
+    for (int j = 0; j < k; ++j) atomicOr(&mask[w][idx[(long)t * k + j]], 1u << lane);
+  __syncwarp();
+  for (int e = lane; e < E; e += 32) hist[(long)c * E + e] = __popc(mask[w][e]);
+}
+
+__global__ void __launch_bounds__(256) perm_scan_kernel(const int* __restrict__ hist, int* __restrict__ base,
+                                                        int* __restrict__ counts, int* __restrict__ offsets,
+                                                        int n_chunks, int E) {
+  __shared__ int s_tot[kMaxE];
+  __shared__ int s_off[kMaxE + 1];
+  const int e = threadIdx.x;
+  int run = 0;
+  if (e < E) {
+    for (int c = 0; c < n_chunks; ++c) {
+      const int h = hist[(long)c * E + e];
+      base[(long)c * E + e] = run;
+      run += h;
+    }
+    s_tot[e] = run;
+  }
+  __syncthreads();
+  if (e == 0) {
+    int acc = 0;
+    for (int i = 0; i < E; ++i) { s_off[i] = acc; acc += s_tot[i]; }
+    s_off[E] = acc;
+  }
+  __syncthreads();
+  if (e < E) {
+    counts[e] = s_tot[e];
+    offsets[e] = s_off[e];
+    if (e == 0) offsets[E] = s_off[E];
+    const int o = s_off[e];
+    for (int c = 0; c < n_chunks; ++c) base[(long)c * E + e] += o;
+  }
+}
+
+__global__ void __launch_bounds__(256) perm_pos_kernel(const int* __restrict__ idx, int T, int k, int E,
+                                                       const int* __restrict__ base, int* __restrict__ pos,
+                                                       int* __restrict__ src_row, int n_chunks) {
+  __shared__ uint32_t mask[8][kMaxE];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 8 + w;
+  for (int e = lane; e < E; e += 32) mask[w][e] = 0;
+  __syncwarp();
+  if (c >= n_chunks) return;
+  const int t = c * 32 + lane;
+  if (t < T)
+    for (int j = 0; j < k; ++j) atomicOr(&mask[w][idx[(long)t * k + j]], 1u << lane);
+  __syncwarp();
+  if (t < T) {
+    const uint32_t below = (1u << lane) - 1u;
+    for (int j = 0; j < k; ++j) {
+      const int e = idx[(long)t * k + j];
+      const int p = base[(long)c * E + e] + __popc(mask[w][e] & below);
+      pos[(long)t * k + j] = p;
+      src_row[p] = t;
+    }
+  }
+}
+
+cudaError_t launch_perm_maps(const PermLaunch& L, cudaStream_t s) {
+  if (L.E > kMaxE || L.E < 1) return cudaErrorInvalidValue;
+  const int nc = perm_chunks(L.T);
+  if (nc == 0) {
+    cudaError_t e = cudaMemsetAsync(L.counts, 0, sizeof(int) * L.E, s);
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(L.offsets, 0, sizeof(int) * (L.E + 1), s);
+  }
+  const int blocks = (nc + 7) / 8;
+  perm_hist_kernel<<<blocks, 256, 0, s>>>(L.topk_idx, L.T, L.k, L.E, L.hist, nc);
+  perm_scan_kernel<<<1, 256, 0, s>>>(L.hist, L.base, L.counts, L.offsets, nc, L.E);
+  perm_pos_kernel<<<blocks, 256, 0, s>>>(L.topk_idx, L.T, L.k, L.E, L.base, L.pos, L.src_row, nc);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K3 permute
+__global__ void __launch_bounds__(256) permute_rows_kernel(const uint4* __restrict__ xn,
+                                                           const int* __restrict__ src_row,
+                                                           uint4* __restrict__ xs, int R, int dv) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long r = (long)blockIdx.x * 8 + w;
+  if (r >= R) return;
+  const long src = src_row[r];
+  const uint4* a = xn + src * dv;
+  uint4* b = xs + r * dv;
+  for (int i = lane; i < dv; i += 32) b[i] = a[i];
+}
+
+cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t* xs, int R, int d,
+                                cudaStream_t s) {
+  if (R == 0) return cudaSuccess;
+  const int dv = d / 8;
+  permute_rows_kernel<<<(R + 7) / 8, 256, 0, s>>>(reinterpret_cast<const uint4*>(xn), src_row,
+                                                  reinterpret_cast<uint4*>(xs), R, dv);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K5 unpermute
+__global__ void __launch_bounds__(256) unpermute_kernel(const uint4* __restrict__ y, const int* __restrict__ pos,
+                                                        const float* __restrict__ w,
+                                                        const float* __restrict__ resid, float* __restrict__ out,
+                                                        long items, int dv, int k) {
+  for (long it = (long)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (long)gridDim.x * blockDim.x) {
+    const long t = it / dv;
+    const int c = (int)(it - t * dv);
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const long p = pos[t * k + j];
+      const float g = w[t * k + j];
+      const uint4 v = y[p * dv + c];
+      acc[0] = fmaf(g, bf16lo(v.x), acc[0]);
+      acc[1] = fmaf(g, bf16hi(v.x), acc[1]);
+      acc[2] = fmaf(g, bf16lo(v.y), acc[2]);
+      acc[3] = fmaf(g, bf16hi(v.y), acc[3]);
+      acc[4] = fmaf(g, bf16lo(v.z), acc[4]);
+      acc[5] = fmaf(g, bf16hi(v.z), acc[5]);
+      acc[6] = fmaf(g, bf16lo(v.w), acc[6]);
+      acc[7] = fmaf(g, bf16hi(v.w), acc[7]);
+    }
+    const float4* rr = reinterpret_cast<const float4*>(resid + t * (long)dv * 8 + c * 8);
+    float4* oo = reinterpret_cast<float4*>(out + t * (long)dv * 8 + c * 8);
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (resid) { a = rr[0]; b = rr[1]; }
+    a.x += acc[0]; a.y += acc[1]; a.z += acc[2]; a.w += acc[3];
+    b.x += acc[4]; b.y += acc[5]; b.z += acc[6]; b.w += acc[7];
+    oo[0] = a;
+    oo[1] = b;
+  }
+}
+
+cudaError_t launch_unpermute(const uint16_t* y, const int* pos, const float* w, const float* resid, float* out,
+                             int T, int k, int d, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int dv = d / 8;
+  const long items = (long)T * dv;
+  long blocks = (items + 255) / 256;
+  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+  unpermute_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, resid, out, items, dv, k);
+  return cudaGetLastError();
+}
+
+__global__ void copy_f32_kernel(const float4* __restrict__ a, float4* __restrict__ b, long n4) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+cudaError_t launch_copy_f32(const float* src, float* dst, long n, cudaStream_t s) {
+  if (n == 0 || src == dst) return cudaSuccess;
+  long n4 = n / 4;
+  long blocks = (n4 + 255) / 256;
+  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  copy_f32_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst),
+                                             n4);
+  return cudaGetLastError();
+}
+
+}  // namespace fsc
