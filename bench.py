@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""Benchmark of the FarSkip-Collective MoE layer forward (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config dsv2lite] [--impl reference]
+
+A step is one pass of the whole hot path (RMSNorm +
+router + top-k, permutation maps, permute/dispatch, SwiGLU grouped GEMM, down
+GEMM, combine, gate-weighted unpermute + residual, shared expert) over one
+batch of T synthetic tokens per rank, with inputs resident in HBM. N > 1 runs
+one process per GPU (torchrun); the per-rank workload is fixed (weak scaling)
+and the value is the tokens all ranks processed / max-over-ranks device time.
+
+Prints ONE JSON line on rank 0. ``--impl reference`` times the CPU fp64 oracle
+(oracle/, the only reference this tier has) on a bounded token sample of the
+same workload and prints the same line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "MoE-layer tokens/s at 1/2/4/8 B200; exposed all-to-all us/layer FarSkip vs blocking"
+UNIT = "tokens/s"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def workload_config(shape, ep, n_gpus, schedule):
+    return {"workload": f"{shape.name}_moe_layer_prefill", "d": shape.d, "n_experts": shape.n_experts,
+            "top_k": shape.top_k, "ffn": shape.ffn, "shared_ffn": shape.shared_ffn,
+            "tokens_per_rank": shape.tokens, "global_tokens": shape.tokens * n_gpus, "ep": ep,
+            "schedule": schedule, "parallelism": f"ep{ep}" + (f"-x{n_gpus // ep}replicas" if n_gpus > ep else ""),
+            "l2": "flushed (256 MiB write) before every timed step; per-step working set > L2",
+            "data": "synthetic seeded N(0,1) tokens, random-init weights (SURVEY §8(d) recipe)"}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.rows = []
+        self.proc = None
+        self.index = index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        loaded = [s for s in sm if s > 600] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- oracle baseline
+def oracle_tokens_per_s(shape, budget_s=12.0, seed=0, max_tokens=None):
+    """The fp64 oracle (as it stands) on a bounded token sample of the workload.
+    The MoE block is token-independent, so a sample of tokens is the same
+    computation per token as the full batch."""
+    from threadpoolctl import threadpool_info
+
+    from oracle import moe as om
+    w = synth.moe_weights(shape, seed=seed)
+    lay = om.layer_from_synth(w, shape.top_k)
+    del w
+    cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    x = synth.tokens(shape, seed=seed, T=shape.tokens)
+    n, done, t_used = 64, 0, 0.0
+    while t_used < budget_s and done < shape.tokens and (max_tokens is None or done < max_tokens):
+        n = min(n, shape.tokens - done)
+        t0 = time.perf_counter()
+        sh, ro, _ = om.moe_block(x[done:done + n], lay)
+        _ = (x[done:done + n].astype(np.float64) + sh) + ro
+        dt = time.perf_counter() - t0
+        t_used += dt
+        done += n
+        n = int(min(4096, max(64, n * 2 if dt < budget_s / 8 else n)))
+    return done / t_used, done, t_used, cores
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_11505_b200 import build as fbuild
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if rank == 0:
+        fbuild.build()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+        fbuild.build()
+    else:
+        torch.cuda.set_device(0)
+    from paper_2511_11505_b200 import Context
+    from tests.gpu_util import moe_weights_dev
+
+    shape = synth.CONFIGS[args.config]
+    T = shape.tokens
+    ep = 1  # EP transport (peer memory) lands next; N>1 runs EP=1 replicas, no data-path collective
+    dev = torch.device("cuda", local)
+    w = synth.moe_weights(shape, seed=args.seed)
+    wd = moe_weights_dev(w, dev)
+    del w
+    x = torch.from_numpy(synth.tokens(shape, seed=args.seed, rank=rank)).to(dev)
+    out = torch.empty_like(x)
+    ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
+                  shared_ffn=shape.shared_ffn, max_tokens=T, device=local)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ctx.moe_forward_blocking(wd, x, out, stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---------------- timed region: K steps, per-step CUDA events on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launch_count() - launches0
+    ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = T * world * args.steps / (total_ms / 1e3)
+
+    # ---------------- per-phase breakdown (separate, untimed-for-value passes)
+    ctx.set_timing(True)
+    phase = {}
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.fill_(0.0)
+        step()
+        for kname, v in ctx.timings().items():
+            phase.setdefault(kname, []).append(v)
+    ctx.set_timing(False)
+    phase_ms = {kname: statistics.median(v) for kname, v in phase.items()}
+
+    # ---------------- e2e: host buffers through the C ABI, copies inside the region
+    xh = torch.from_numpy(synth.tokens(shape, seed=args.seed, rank=rank)).pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    for _ in range(2):
+        ctx.moe_forward_blocking_host(wd, xh, oh, stream=stream.cuda_stream)
+    if world > 1:
+        dist.barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.moe_forward_blocking_host(wd, xh, oh, stream=stream.cuda_stream)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = T * world * e2e_steps / e2e_s
+
+    if rank != 0:
+        ctx.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks, src = load_peaks()
+    # dominant kernel: routed-expert GEMM1 with the fused SwiGLU epilogue (row a7)
+    R = T * shape.top_k
+    g1_flop = 2.0 * R * shape.d * 2 * shape.ffn
+    g1_ms = phase_ms.get("gemm1")
+    achieved = g1_flop / (g1_ms * 1e-3) / 1e12 if g1_ms else None
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_gemm1_dsv2lite.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    exp_flop = 2.0 * R * shape.d * 3 * shape.ffn + 2.0 * T * shape.d * 3 * shape.shared_ffn
+    layer_roof_ms = exp_flop / (peaks["bf16_tflops"] * 1e12) * 1e3
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": workload_config(shape, ep, world, "blocking"),
+        "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel<256,SWIGLU> (routed GEMM1)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",
+                     "algorithmic_flop_per_launch": g1_flop,
+                     "frac_of_burst_peak": (achieved / peaks["bf16_tflops"]) if achieved else None},
+        "layer_roofline": {"expert_flop": exp_flop, "t_roof_ms": layer_roof_ms,
+                           "frac": layer_roof_ms / ms_per_step, "note": "max(expert FLOPs / bf16 burst peak, "
+                                                                        "a2a bytes / NVLink); a2a = 0 at EP=1"},
+        "phase_ms": phase_ms,
+        "exposed_a2a_us_per_layer": {"farskip": None, "blocking": None, "note": "EP=1: no all-to-all"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": T * shape.d * 4 * world,
+                "d2h_bytes_per_step": T * shape.d * 4 * world,
+                "note": "fsc_moe_forward_blocking_host: pinned host x -> device -> forward -> host out, synced"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "wall_s_timed_region": wall,
+    }
+    if not args.no_cpu_baseline:
+        tps, n, secs, cores = oracle_tokens_per_s(shape, budget_s=args.cpu_budget)
+        res["cpu_baseline"] = {"value": tps, "unit": UNIT, "cores": cores, "kind": "oracle",
+                               "sample": f"{n} of the {T} tokens of rank 0's batch through the fp64 numpy oracle "
+                                         f"MoE block ({secs:.1f} s)"}
+    print(json.dumps(res), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    shape = synth.CONFIGS[args.config]
+    from threadpoolctl import threadpool_info
+
+    from oracle import moe as om
+    w = synth.moe_weights(shape, seed=args.seed)
+    lay = om.layer_from_synth(w, shape.top_k)
+    del w
+    x = synth.tokens(shape, seed=args.seed, T=shape.tokens)
+    cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    per_step = min(args.ref_tokens, shape.tokens)
+    for i in range(args.warmup):
+        om.moe_block(x[:min(per_step, 16)], lay)
+    times = []
+    for i in range(args.steps):
+        s0 = (i * per_step) % max(1, shape.tokens - per_step)
+        t0 = time.perf_counter()
+        sh, ro, _ = om.moe_block(x[s0:s0 + per_step], lay)
+        _ = (x[s0:s0 + per_step].astype(np.float64) + sh) + ro
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = per_step * args.steps / total
+    res = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": workload_config(shape, 1, world, "blocking"),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"{per_step} tokens per step of the {shape.tokens}-token batch"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="dsv2lite", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="fsc", choices=["fsc", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-tokens", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -139,6 +139,19 @@ FSC_API const char* fsc_last_error(const fsc_ctx* ctx);
  * co-running comm kernels ("communication operations only utilizing a
  * fraction of the total available units"). */
 FSC_API int fsc_set_gemm_ctas(fsc_ctx* ctx, int n);
+/* Grouped-GEMM tile mode: 2 (default) = CTA pairs with tcgen05 cta_group::2,
+ * 256-row tiles; 1 = single-CTA 128-row tiles. Results are identical. */
+FSC_API int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg);
+
+/* Per-phase CUDA-event timing of the MoE calls (bench / profiling). When enabled,
+ * events are recorded on the call's stream around every phase; fsc_get_timings
+ * waits for the last call's events and writes n <= 9 durations in ms (-1 = phase
+ * not run) in the order: router, perm_maps, dispatch (permute), gemm1 (SwiGLU),
+ * gemm2 (down), combine, shared1, shared2, unpermute. Returns the phase count. */
+FSC_API int fsc_set_timing(fsc_ctx* ctx, int enable);
+FSC_API int fsc_get_timings(fsc_ctx* ctx, float* ms, int n);
+/* Cumulative number of CUDA kernels launched by libfsc in this process. */
+FSC_API long fsc_launch_count(void);
 
 /* ---------------------------------------------------------------- MoE sub-block */
 

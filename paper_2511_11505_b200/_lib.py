@@ -66,6 +66,10 @@ _SIGS = {
     "fsc_finalize": (_I, [_P]),
     "fsc_last_error": (ctypes.c_char_p, [_P]),
     "fsc_set_gemm_ctas": (_I, [_P, _I]),
+    "fsc_set_gemm_cta_group": (_I, [_P, _I]),
+    "fsc_set_timing": (_I, [_P, _I]),
+    "fsc_get_timings": (_I, [_P, ctypes.POINTER(ctypes.c_float), _I]),
+    "fsc_launch_count": (ctypes.c_long, []),
     "fsc_moe_forward_blocking": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, ctypes.POINTER(MoeDebugC), _P]),
     "fsc_moe_forward_blocking_host": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, _P]),
     "fsc_moe_forward_farskip": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, OVERLAP_CB, _P,
@@ -178,6 +182,25 @@ class Context:
         data = b"".join(blobs)
         buf = ctypes.create_string_buffer(data, max(len(data), 1))
         self._ck(self.lib.fsc_bootstrap_import(self.h, buf))
+
+    PHASES = ("router", "perm_maps", "dispatch", "gemm1", "gemm2", "combine", "shared1", "shared2", "unpermute")
+
+    def set_timing(self, enable: bool):
+        self._ck(self.lib.fsc_set_timing(self.h, int(enable)))
+
+    def timings(self) -> dict:
+        """Per-phase ms of the last MoE call (phases not run are omitted)."""
+        buf = (ctypes.c_float * len(self.PHASES))()
+        rc = self.lib.fsc_get_timings(self.h, buf, len(self.PHASES))
+        if rc < 0:
+            self._ck(rc)
+        return {n: buf[i] for i, n in enumerate(self.PHASES) if buf[i] >= 0}
+
+    def launch_count(self) -> int:
+        return int(self.lib.fsc_launch_count())
+
+    def set_gemm_cta_group(self, cg: int):
+        self._ck(self.lib.fsc_set_gemm_cta_group(self.h, cg))
 
     def set_gemm_ctas(self, n: int):
         self._ck(self.lib.fsc_set_gemm_ctas(self.h, n))

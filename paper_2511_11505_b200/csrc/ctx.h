@@ -14,12 +14,16 @@ struct fsc_handle_s {
 
 struct fsc_peer_state;  // transport.cu
 
+// phases timed with CUDA events when timing is enabled (fsc_get_timings order)
+enum { PH_ROUTER = 0, PH_PERM, PH_DISPATCH, PH_GEMM1, PH_GEMM2, PH_COMBINE, PH_SHARED1, PH_SHARED2, PH_UNPERMUTE, PH_N };
+
 struct fsc_ctx {
   int rank = 0, ep = 1, device = 0;
   fsc_moe_config cfg{};
   int e_loc = 0;
   long max_recv = 0;
   int gemm_ctas = 148;
+  int gemm_cg = 2;
   int sticky = 0;
   char err[512] = {0};
 
@@ -33,6 +37,9 @@ struct fsc_ctx {
   int* base = nullptr;         // [chunks, E]
   int* counts = nullptr;       // [E]                copies per global expert (this rank)
   int* offsets = nullptr;      // [E+1]
+  int* rf_list = nullptr;      // [T]                router near-tie list
+  int* rf_ctrl = nullptr;      // [2]                {count, ticket}
+  double* rf_l64 = nullptr;    // [T, E]             fp64 logits of flagged tokens
   uint16_t* xs = nullptr;      // bf16 [T*k, d]      expert-sorted send buffer
   uint16_t* h = nullptr;       // bf16 [max_recv, c] SwiGLU activations
   uint16_t* y = nullptr;       // bf16 [T*k, d]      expert outputs in the send layout (EP=1)
@@ -53,6 +60,9 @@ struct fsc_ctx {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
 
   int pending = 0;
+  int timing = 0;
+  cudaEvent_t ph_ev[PH_N][2] = {};
+  int ph_used[PH_N] = {};
   fsc_handle_s handle{};
 };
 

@@ -41,11 +41,23 @@ void fsc_set_error(fsc_ctx* c, const char* fmt, ...) {
     }                                       \
   } while (0)
 
+namespace fsc {
+long g_launches = 0;
+}
+
+#define PH_BEGIN(i) \
+  if (ctx->timing) CK(cudaEventRecord(ctx->ph_ev[i][0], s))
+#define PH_END(i)                                  \
+  if (ctx->timing) {                               \
+    CK(cudaEventRecord(ctx->ph_ev[i][1], s));      \
+    ctx->ph_used[i] = 1;                           \
+  }
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 static int check_cfg(const fsc_moe_config* c, int ep, char* err, size_t n) {
   if (!c) { snprintf(err, n, "null config"); return FSC_ERR_CONFIG; }
-  if (c->d <= 0 || c->d % 64) { snprintf(err, n, "d=%d must be a positive multiple of 64", c->d); return FSC_ERR_CONFIG; }
+  if (c->d <= 0 || c->d % 64 || c->d > 8192) { snprintf(err, n, "d=%d must be a positive multiple of 64", c->d); return FSC_ERR_CONFIG; }
   if (c->n_experts < 1 || c->n_experts > 128) { snprintf(err, n, "n_experts=%d outside [1,128]", c->n_experts); return FSC_ERR_CONFIG; }
   if (c->top_k < 1 || c->top_k > c->n_experts) { snprintf(err, n, "top_k=%d outside [1,E]", c->top_k); return FSC_ERR_CONFIG; }
   if (c->ffn <= 0 || c->ffn % 64) { snprintf(err, n, "ffn=%d must be a positive multiple of 64", c->ffn); return FSC_ERR_CONFIG; }
@@ -96,6 +108,10 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(dalloc(&ctx->base, nch * E));
   CK(dalloc(&ctx->counts, E));
   CK(dalloc(&ctx->offsets, E + 1));
+  CK(dalloc(&ctx->rf_list, T));
+  CK(dalloc(&ctx->rf_ctrl, 2));
+  CK(dalloc(&ctx->rf_l64, T * E));
+  CK(cudaMemset(ctx->rf_ctrl, 0, 2 * sizeof(int)));
   CK(dalloc(&ctx->xs, (T * k > ctx->max_recv ? T * k : ctx->max_recv) * d));
   CK(dalloc(&ctx->h, ctx->max_recv * (long)c.ffn));
   CK(dalloc(&ctx->y, (T * k > ctx->max_recv ? T * k : ctx->max_recv) * d));
@@ -127,17 +143,51 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+  for (int i = 0; i < PH_N; ++i)
+    for (int j = 0; j < 2; ++j)
+      if (ctx->ph_ev[i][j]) cudaEventDestroy(ctx->ph_ev[i][j]);
   delete ctx;
   return FSC_OK;
 }
 
 extern "C" const char* fsc_last_error(const fsc_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+
+extern "C" int fsc_set_timing(fsc_ctx* ctx, int enable) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  CK(cudaSetDevice(ctx->device));
+  if (enable && !ctx->ph_ev[0][0])
+    for (int i = 0; i < PH_N; ++i)
+      for (int j = 0; j < 2; ++j) CK(cudaEventCreate(&ctx->ph_ev[i][j]));
+  ctx->timing = enable ? 1 : 0;
+  return FSC_OK;
+}
+
+extern "C" int fsc_get_timings(fsc_ctx* ctx, float* ms, int n) {
+  if (!ctx || !ms) return FSC_ERR_SHAPE;
+  for (int i = 0; i < n && i < PH_N; ++i) {
+    ms[i] = -1.f;
+    if (ctx->timing && ctx->ph_used[i]) {
+      CK(cudaEventSynchronize(ctx->ph_ev[i][1]));
+      CK(cudaEventElapsedTime(&ms[i], ctx->ph_ev[i][0], ctx->ph_ev[i][1]));
+    }
+  }
+  return PH_N;
+}
+
+extern "C" long fsc_launch_count(void) { return fsc::g_launches; }
+
+extern "C" int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(cg == 1 || cg == 2, FSC_ERR_CONFIG, "cta_group must be 1 or 2");
+  ctx->gemm_cg = cg;
+  return FSC_OK;
+}
 
 extern "C" int fsc_set_gemm_ctas(fsc_ctx* ctx, int n) {
   if (!ctx) return FSC_ERR_SHAPE;
@@ -170,10 +220,14 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   const fsc_moe_config& c = ctx->cfg;
   const int d = c.d, E = c.n_experts, k = c.top_k;
   RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
-                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr};
+                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64};
+  PH_BEGIN(PH_ROUTER);
   CK(launch_router(rl, s));
+  PH_END(PH_ROUTER);
   PermLaunch pl{ctx->topk_idx, T, k, E, ctx->hist, ctx->base, ctx->counts, ctx->offsets, ctx->pos, ctx->src_row};
+  PH_BEGIN(PH_PERM);
   CK(launch_perm_maps(pl, s));
+  PH_END(PH_PERM);
   if (dbg) {
     if (dbg->topk_idx) CK(cudaMemcpyAsync(dbg->topk_idx, ctx->topk_idx, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
     if (dbg->topk_w) CK(cudaMemcpyAsync(dbg->topk_w, ctx->topk_w, sizeof(float) * T * k, cudaMemcpyDeviceToDevice, s));
@@ -187,7 +241,9 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   long recv_rows = R;
   const int* recv_counts = ctx->counts;
   if (ctx->ep == 1) {
+    PH_BEGIN(PH_DISPATCH);
     CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, s));
+    PH_END(PH_DISPATCH);
   } else {
     int rc = fsc_transport_dispatch(ctx, T, s);
     if (rc) return rc;
@@ -204,13 +260,17 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   GemmLaunch g1{};
   g1.A = recv; g1.a_rows = recv_rows; g1.B0 = w->w1; g1.B1 = w->w2; g1.b_rows = (long)ctx->e_loc * c.ffn;
   g1.b_group_rows = c.ffn; g1.K = d; g1.N = c.ffn; g1.G = ctx->e_loc; g1.counts = recv_counts; g1.m_total = 0;
-  g1.out = ctx->h; g1.ldo = c.ffn; g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas;
+  g1.out = ctx->h; g1.ldo = c.ffn; g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas; g1.cta_group = ctx->gemm_cg;
+  PH_BEGIN(PH_GEMM1);
   CK(launch_grouped_gemm(g1, s));
+  PH_END(PH_GEMM1);
   GemmLaunch g2{};
   g2.A = ctx->h; g2.a_rows = recv_rows; g2.B0 = w->w3; g2.B1 = nullptr; g2.b_rows = (long)ctx->e_loc * d;
   g2.b_group_rows = d; g2.K = c.ffn; g2.N = d; g2.G = ctx->e_loc; g2.counts = recv_counts; g2.m_total = 0;
-  g2.out = (ctx->ep == 1) ? ctx->y : ctx->yr; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas;
+  g2.out = (ctx->ep == 1) ? ctx->y : ctx->yr; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = ctx->gemm_cg;
+  PH_BEGIN(PH_GEMM2);
   CK(launch_grouped_gemm(g2, s));
+  PH_END(PH_GEMM2);
   if (ctx->ep > 1) {
     int rc = fsc_transport_combine(ctx, T, s);  // P:198 step 7: start Combine
     if (rc) return rc;
@@ -225,19 +285,25 @@ static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float
   const int d = c.d;
   if (c.shared_ffn == 0) {
     if (dbg && dbg->shared_out) CK(cudaMemsetAsync(dbg->shared_out, 0, sizeof(float) * T * (long)d, s));
+    PH_BEGIN(PH_SHARED2);
     CK(launch_copy_f32(resid, out, (long)T * d, s));
+    PH_END(PH_SHARED2);
     return FSC_OK;
   }
   GemmLaunch g1{};
   g1.A = ctx->xn; g1.a_rows = T; g1.B0 = w->ws1; g1.B1 = w->ws2; g1.b_rows = c.shared_ffn; g1.b_group_rows = c.shared_ffn;
   g1.K = d; g1.N = c.shared_ffn; g1.G = 1; g1.counts = nullptr; g1.m_total = T; g1.out = ctx->hs; g1.ldo = c.shared_ffn;
-  g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas;
+  g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas; g1.cta_group = ctx->gemm_cg;
+  PH_BEGIN(PH_SHARED1);
   CK(launch_grouped_gemm(g1, s));
+  PH_END(PH_SHARED1);
   GemmLaunch g2{};
   g2.A = ctx->hs; g2.a_rows = T; g2.B0 = w->ws3; g2.B1 = nullptr; g2.b_rows = d; g2.b_group_rows = d;
   g2.K = c.shared_ffn; g2.N = d; g2.G = 1; g2.counts = nullptr; g2.m_total = T; g2.out = out; g2.ldo = d;
-  g2.resid = resid; g2.ldr = d; g2.epi = EPI_RESID_F32; g2.num_ctas = ctx->gemm_ctas;
+  g2.resid = resid; g2.ldr = d; g2.epi = EPI_RESID_F32; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = ctx->gemm_cg;
+  PH_BEGIN(PH_SHARED2);
   CK(launch_grouped_gemm(g2, s));
+  PH_END(PH_SHARED2);
   if (dbg && dbg->shared_out) {
     g2.out = dbg->shared_out; g2.resid = nullptr;
     CK(launch_grouped_gemm(g2, s));
@@ -254,7 +320,9 @@ static int moe_finish(fsc_ctx* ctx, int T, const float* resid, float* out, const
     if (rc) return rc;
     ysrc = ctx->ys;
   }
+  PH_BEGIN(PH_UNPERMUTE);
   CK(launch_unpermute(ysrc, ctx->pos, ctx->topk_w, resid, out, T, c.top_k, c.d, s));
+  PH_END(PH_UNPERMUTE);
   if (dbg && dbg->routed_out)
     CK(launch_unpermute(ysrc, ctx->pos, ctx->topk_w, nullptr, dbg->routed_out, T, c.top_k, c.d, s));
   return FSC_OK;
@@ -270,6 +338,7 @@ extern "C" int fsc_moe_forward_blocking(fsc_ctx* ctx, const fsc_moe_weights* w, 
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (T == 0 && ctx->ep == 1) return FSC_OK;
+  memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
   rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr);
   if (rc) return rc;
   // Regular order (C-amb-12): tmp = x_in + shared; out = tmp + routed.
@@ -303,6 +372,7 @@ extern "C" int fsc_moe_forward_farskip(fsc_ctx* ctx, const fsc_moe_weights* w, i
   REQUIRE(!ctx->pending, FSC_ERR_STATE, "FarSkip pipeline depth is 1: wait the outstanding handle first");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
   rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, cb, user);
   if (rc) return rc;
   if (cb) cb(user, 1, s);  // combine in flight
@@ -338,9 +408,10 @@ extern "C" int fsc_op_router(fsc_ctx* ctx, const float* x, const float* gamma, c
                              int E, int k, void* xn, int* topk_idx, float* topk_w, float* logits, int* n_refined,
                              void* stream) {
   if (!ctx) return FSC_ERR_SHAPE;
-  REQUIRE(d % 64 == 0 && E >= 1 && E <= 128 && k >= 1 && k <= E, FSC_ERR_CONFIG, "bad router shape");
+  REQUIRE(d % 64 == 0 && d <= 8192 && E >= 1 && E <= 128 && k >= 1 && k <= E, FSC_ERR_CONFIG, "bad router shape");
+  REQUIRE(T >= 0 && T <= ctx->cfg.max_tokens, FSC_ERR_CONFIG, "T beyond workspace");
   RouterLaunch rl{x, gamma, w_router, T, d, E, k, ctx->cfg.rms_eps, static_cast<uint16_t*>(xn), topk_idx, topk_w,
-                  logits, n_refined};
+                  logits, n_refined, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64};
   CK(launch_router(rl, static_cast<cudaStream_t>(stream)));
   return FSC_OK;
 }
@@ -374,6 +445,7 @@ extern "C" int fsc_op_grouped_gemm(fsc_ctx* ctx, int epi, const void* A, long a_
   L.A = A; L.a_rows = a_rows; L.B0 = B0; L.B1 = B1; L.b_rows = (long)G * N; L.b_group_rows = N; L.K = K; L.N = N;
   L.G = G; L.counts = counts; L.m_total = m_total; L.out = out; L.ldo = N; L.resid = resid; L.ldr = N; L.epi = epi;
   L.num_ctas = ctx->gemm_ctas;
+  L.cta_group = ctx->gemm_cg;
   CK(launch_grouped_gemm(L, static_cast<cudaStream_t>(stream)));
   return FSC_OK;
 }

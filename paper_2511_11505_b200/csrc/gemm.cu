@@ -12,8 +12,9 @@
 // M_g comes from device-resident counts (no host sync): every CTA rebuilds the
 // per-group row / tile prefix in shared memory and walks a static tile stride.
 //
-// Roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
-// issuer (one elected lane), warps 2..5 = epilogue (TMEM lane quarter = warp%4).
+// Roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
+// issuer (one elected lane), warps 2..9 = epilogue (TMEM lane quarter = warp%4,
+// column half = (warp-2)/4).
 // Tiles: BM=128 rows x BN cols, BK=64 (one 128-byte swizzle atom of bf16).
 #include <cudaTypedefs.h>
 
@@ -23,19 +24,23 @@
 namespace fsc {
 
 namespace {
-constexpr int BM = 128;
+constexpr int BM = 128;              // rows per CTA (TMEM lanes)
 constexpr int BK = 64;
 constexpr int kMaxGroups = 256;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;         // two warps per TMEM lane quarter, each half the columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
-template <int BN>
+template <int BN, int CG>
 struct Cfg {
   static constexpr int HALF = BN / 2;
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int TILE_M = BM * CG;                       // rows per (pair) tile
+  static constexpr int A_BYTES = BM * BK * 2;                  // per CTA
+  static constexpr int B_ROWS = CG == 2 ? BN / 2 : BN;         // B rows held per CTA
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = 2 * BN;                     // double-buffered accumulator
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + 2 * (kMaxGroups + 1) * 4;
 };
 
@@ -45,6 +50,7 @@ struct TileInfo {
   int g, mb, nb, row0, rows;
 };
 
+template <int TILE_M>
 FSC_DEVINL TileInfo decode_tile(int t, int n_tiles, int G, const int* s_row_off, const int* s_tile_off) {
   TileInfo ti;
   int mt = t / n_tiles;
@@ -56,18 +62,23 @@ FSC_DEVINL TileInfo decode_tile(int t, int n_tiles, int G, const int* s_row_off,
   }
   ti.g = lo;
   ti.mb = mt - s_tile_off[lo];
-  ti.row0 = s_row_off[lo] + ti.mb * BM;
+  ti.row0 = s_row_off[lo] + ti.mb * TILE_M;
   int m = s_row_off[lo + 1] - s_row_off[lo];
-  ti.rows = min(BM, m - ti.mb * BM);
+  ti.rows = min(TILE_M, m - ti.mb * TILE_M);
   return ti;
 }
 }  // namespace
 
-template <int BN, int EPI>
+// CG = 1: one CTA per 128-row tile (tcgen05 cta_group::1).
+// CG = 2: a CTA pair (cluster of 2) per 256-row tile: MMA M=256 issued by the
+// leader (cta_group::2); each CTA stages its 128 rows of A and half of the B
+// columns, so per-SM smem traffic per MAC drops by a third and the pipeline is
+// 1.5x deeper at the same shared-memory footprint.
+template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                         const __grid_constant__ CUtensorMap tmB1, GemmParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -83,6 +94,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = warp_id();
   const int lane = lane_id();
   const int G = p.G;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
 
   if (warp == 0) {
     if (elect_one()) {
@@ -95,12 +108,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], 4);
+        mbar_init(&tempty[a], kEpiWarps * CG);
       }
       fence_barrier_init();
     }
   } else if (warp == 1) {
-    tmem_alloc<C::TMEM_COLS>(s_tmem);
+    if (CG == 2) tmem_alloc_2sm<C::TMEM_COLS>(s_tmem);
+    else tmem_alloc<C::TMEM_COLS>(s_tmem);
   } else if (warp == 2) {
     // per-group row and tile prefix sums from the device-resident counts
     int run_rows = 0, run_tiles = 0;
@@ -109,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int g = base + lane;
       int m = 0;
       if (g < G) m = p.counts ? p.counts[g] : p.m_total;
-      int tl = (m + BM - 1) / BM;
+      int tl = (m + C::TILE_M - 1) / C::TILE_M;
       int im = m, it = tl;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -124,48 +138,68 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();   // peer barriers initialised before any remote arrive / 2-SM TMA
   tc_fence_after();
 
   const uint32_t tmem_base = *s_tmem;
   const int n_tiles = (EPI == EPI_SWIGLU) ? p.N / C::HALF : p.N / BN;
   const int total = s_tile_off[G] * n_tiles;
   const int kblocks = p.K / BK;
+  const int t_first = blockIdx.x / CG, t_step = gridDim.x / CG;
 
   if (warp == 0) {
-    // ------------------------------------------------ TMA producer
+    // ------------------------------------------------ TMA producer (both CTAs of a pair)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        TileInfo ti = decode_tile(t, n_tiles, G, s_row_off, s_tile_off);
-        int brow0, brow1;
-        if (EPI == EPI_SWIGLU) {
-          brow0 = ti.g * p.b_group_rows + ti.nb * C::HALF;
-          brow1 = brow0;
+      for (int t = t_first; t < total; t += t_step) {
+        TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
+        const int arow = ti.row0 + (int)rank * BM;
+        int brow0, brow1 = 0;
+        const CUtensorMap* mb0 = &tmB0;
+        const CUtensorMap* mb1 = &tmB0;
+        if (CG == 2) {
+          if (EPI == EPI_SWIGLU) {           // CTA0: U columns from W1, CTA1: G columns from W2
+            brow0 = ti.g * p.b_group_rows + ti.nb * C::HALF;
+            mb0 = rank ? &tmB1 : &tmB0;
+          } else {
+            brow0 = ti.g * p.b_group_rows + ti.nb * BN + (int)rank * C::HALF;
+          }
         } else {
-          brow0 = ti.g * p.b_group_rows + ti.nb * BN;
-          brow1 = brow0 + C::HALF;
+          if (EPI == EPI_SWIGLU) {
+            brow0 = ti.g * p.b_group_rows + ti.nb * C::HALF;
+            brow1 = brow0;
+            mb1 = &tmB1;
+          } else {
+            brow0 = ti.g * p.b_group_rows + ti.nb * BN;
+            brow1 = brow0 + C::HALF;
+          }
         }
-        const CUtensorMap* mb1 = (EPI == EPI_SWIGLU) ? &tmB1 : &tmB0;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, ti.row0, kEvictNormal);
           uint8_t* b = sB + stage * C::B_BYTES;
-          tma_load_2d(b, &tmB0, &full[stage], kb * BK, brow0, kEvictLast);
-          tma_load_2d(b + C::HALF * BK * 2, mb1, &full[stage], kb * BK, brow1, kEvictLast);
+          if (CG == 2) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tma_load_2d_2sm(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, arow, kEvictNormal);
+            tma_load_2d_2sm(b, mb0, &full[stage], kb * BK, brow0, kEvictLast);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, arow, kEvictNormal);
+            tma_load_2d(b, mb0, &full[stage], kb * BK, brow0, kEvictLast);
+            tma_load_2d(b + C::HALF * BK * 2, mb1, &full[stage], kb * BK, brow1, kEvictLast);
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    if (elect_one()) {
-      const uint32_t idesc = idesc_bf16_f32(BM, BN);
+    // ------------------------------------------------ MMA issuer (leader CTA only)
+    if (leader && elect_one()) {
+      const uint32_t idesc = idesc_bf16_f32(C::TILE_M, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      for (int t = t_first; t < total; t += t_step, ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -178,33 +212,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
-                         (kb | k) != 0);
+            if (CG == 2)
+              umma_bf16_ss_2sm(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
+                               (kb | k) != 0);
+            else
+              umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
+                           (kb | k) != 0);
           }
-          umma_commit(&empty[stage]);
+          if (CG == 2) umma_commit_2sm(&empty[stage]);
+          else umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[acc]);
+        if (CG == 2) umma_commit_2sm(&tfull[acc]);
+        else umma_commit(&tfull[acc]);
       }
     }
   } else {
-    // ------------------------------------------------ epilogue warps 2..5
+    // ------------------------------------------------ epilogue warps 2..9 (own 128 rows)
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;   // column half handled by this warp
     const int r = q * 32 + lane;
+    const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-      TileInfo ti = decode_tile(t, n_tiles, G, s_row_off, s_tile_off);
+    for (int t = t_first; t < total; t += t_step, ++it) {
+      TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const bool valid = r < ti.rows;
-      const long grow = (long)ti.row0 + r;
+      const int rr = r + (int)rank * BM;          // row inside the pair tile
+      const bool valid = rr < ti.rows;
+      const long grow = (long)ti.row0 + rr;
       const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (EPI == EPI_SWIGLU) {
         __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + ti.nb * C::HALF;
 #pragma unroll 1
-        for (int c = 0; c < C::HALF; c += 32) {
+        for (int c = half * (C::HALF / 2); c < (half + 1) * (C::HALF / 2); c += 32) {
           uint32_t u[32], gv[32];
           tmem_ld32(tb + c, u);
           tmem_ld32(tb + C::HALF + c, gv);
@@ -225,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (EPI == EPI_BF16) {
         __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + ti.nb * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
           uint32_t v[32];
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
@@ -242,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo + ti.nb * BN;
         const float* res = p.resid ? p.resid + grow * p.ldr + ti.nb * BN : nullptr;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
           uint32_t v[32];
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
@@ -261,15 +304,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();   // the peer may still arrive on / commit to our barriers until here
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    if (CG == 2) tmem_dealloc_2sm<C::TMEM_COLS>(tmem_base);
+    else tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -301,18 +349,18 @@ static bool make_map(CUtensorMap* m, const void* base, long rows, long cols, int
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG>
 static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   CUtensorMap ma, mb0, mb1;
   long a_rows = L.a_rows > 0 ? L.a_rows : 1;
   if (!make_map(&ma, L.A, a_rows, L.K, BM)) return cudaErrorInvalidValue;
   if (!make_map(&mb0, L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
   if (!make_map(&mb1, L.B1 ? L.B1 : L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
+  auto kern = grouped_gemm_kernel<BN, EPI, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -328,8 +376,22 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   p.resid = L.resid;
   p.ldr = L.ldr;
   int grid = L.num_ctas > 0 ? L.num_ctas : kNumSMs;
-  grouped_gemm_kernel<BN, EPI><<<grid, kThreads, C::SMEM, s>>>(ma, mb0, mb1, p);
-  return cudaGetLastError();
+  if (CG == 2) grid &= ~1;
+  if (grid < CG) grid = CG;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ++g_launches;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb0, mb1, p);
 }
 
 int gemm_pick_bn(int epi, int N) {
@@ -342,8 +404,11 @@ cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s) {
   int bn = gemm_pick_bn(L.epi, L.N);
   if (!bn) return cudaErrorInvalidValue;
   if (L.a_rows == 0) return cudaSuccess;
-#define FSC_GEMM_CASE(BNV, EV) \
-  if (bn == BNV && L.epi == EV) return launch_t<BNV, EV>(L, s);
+#define FSC_GEMM_CASE(BNV, EV)                                  \
+  if (bn == BNV && L.epi == EV) {                               \
+    if (L.cta_group == 1) return launch_t<BNV, EV, 1>(L, s);    \
+    return launch_t<BNV, EV, 2>(L, s);                          \
+  }
   FSC_GEMM_CASE(256, EPI_SWIGLU)
   FSC_GEMM_CASE(128, EPI_SWIGLU)
   FSC_GEMM_CASE(256, EPI_BF16)

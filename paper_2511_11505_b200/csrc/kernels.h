@@ -5,6 +5,9 @@
 
 namespace fsc {
 
+// number of kernels this process has launched through libfsc (evidence for bench's gpu_launches)
+extern long g_launches;
+
 enum { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_RESID_F32 = 2 };
 
 struct GemmParams {
@@ -36,6 +39,7 @@ struct GemmLaunch {
   long ldr;
   int epi;
   int num_ctas;       // persistent grid (<= 148); 0 = all SMs
+  int cta_group = 2;  // 2: CTA pairs, MMA M=256 (default); 1: single-CTA M=128 tiles
 };
 
 cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s);
@@ -53,6 +57,9 @@ struct RouterLaunch {
   float* topk_w;         // [T, k]
   float* logits;         // optional [T, E]
   int* n_refined;        // optional device counter
+  int* rf_list;          // workspace [T]: tokens flagged for fp64 refinement
+  int* rf_ctrl;          // workspace [2]: {count, done-ticket}, zero between calls
+  double* rf_l64;        // workspace [T, E]: fp64 logits of flagged tokens
 };
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s);
 

@@ -37,45 +37,76 @@ __global__ void __launch_bounds__(256) perm_hist_kernel(const int* __restrict__ 
   for (int e = lane; e < E; e += 32) hist[(long)c * E + e] = __popc(mask[w][e]);
 }
 
+// Column scan, one CTA per expert: base[c][e] = sum_{c' < c} hist[c'][e] (local to e),
+// counts[e] = column total. Offsets across experts are added by perm_pos_kernel.
 __global__ void __launch_bounds__(256) perm_scan_kernel(const int* __restrict__ hist, int* __restrict__ base,
-                                                        int* __restrict__ counts, int* __restrict__ offsets,
-                                                        int n_chunks, int E) {
-  __shared__ int s_tot[kMaxE];
-  __shared__ int s_off[kMaxE + 1];
-  const int e = threadIdx.x;
-  int run = 0;
-  if (e < E) {
-    for (int c = 0; c < n_chunks; ++c) {
-      const int h = hist[(long)c * E + e];
-      base[(long)c * E + e] = run;
+                                                        int* __restrict__ counts, int n_chunks, int E) {
+  __shared__ int s_w[8];
+  const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n_chunks + 255) / 256;
+  const int c0 = tid * per;
+  int loc = 0;
+  for (int i = 0; i < per; ++i)
+    if (c0 + i < n_chunks) loc += hist[(long)(c0 + i) * E + e];
+  int inc = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffff, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  int wbase = 0;
+  for (int w = 0; w < warp; ++w) wbase += s_w[w];
+  int run = wbase + inc - loc;
+  for (int i = 0; i < per; ++i) {
+    if (c0 + i < n_chunks) {
+      const long off = (long)(c0 + i) * E + e;
+      const int h = hist[off];
+      base[off] = run;
       run += h;
     }
-    s_tot[e] = run;
   }
-  __syncthreads();
-  if (e == 0) {
-    int acc = 0;
-    for (int i = 0; i < E; ++i) { s_off[i] = acc; acc += s_tot[i]; }
-    s_off[E] = acc;
-  }
-  __syncthreads();
-  if (e < E) {
-    counts[e] = s_tot[e];
-    offsets[e] = s_off[e];
-    if (e == 0) offsets[E] = s_off[E];
-    const int o = s_off[e];
-    for (int c = 0; c < n_chunks; ++c) base[(long)c * E + e] += o;
-  }
+  if (tid == 255) counts[e] = wbase + inc;
 }
 
 __global__ void __launch_bounds__(256) perm_pos_kernel(const int* __restrict__ idx, int T, int k, int E,
-                                                       const int* __restrict__ base, int* __restrict__ pos,
-                                                       int* __restrict__ src_row, int n_chunks) {
+                                                       const int* __restrict__ base,
+                                                       const int* __restrict__ counts, int* __restrict__ offsets,
+                                                       int* __restrict__ pos, int* __restrict__ src_row,
+                                                       int n_chunks) {
   __shared__ uint32_t mask[8][kMaxE];
+  __shared__ int s_off[kMaxE + 1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w == 0) {
+    // exclusive scan of the expert totals (E <= 256: 8 per lane)
+    int v[8], loc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane * 8 + i;
+      v[i] = e < E ? counts[e] : 0;
+      loc += v[i];
+    }
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffff, inc, o);
+      if (lane >= o) inc += u;
+    }
+    int run = inc - loc;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane * 8 + i;
+      if (e < E) s_off[e] = run;
+      run += v[i];
+    }
+    if (lane == 31) s_off[E] = inc;
+  }
   const int c = blockIdx.x * 8 + w;
   for (int e = lane; e < E; e += 32) mask[w][e] = 0;
-  __syncwarp();
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e <= E; e += 256) offsets[e] = s_off[e];
   if (c >= n_chunks) return;
   const int t = c * 32 + lane;
   if (t < T)
@@ -85,7 +116,7 @@ __global__ void __launch_bounds__(256) perm_pos_kernel(const int* __restrict__ i
     const uint32_t below = (1u << lane) - 1u;
     for (int j = 0; j < k; ++j) {
       const int e = idx[(long)t * k + j];
-      const int p = base[(long)c * E + e] + __popc(mask[w][e] & below);
+      const int p = s_off[e] + base[(long)c * E + e] + __popc(mask[w][e] & below);
       pos[(long)t * k + j] = p;
       src_row[p] = t;
     }
@@ -101,9 +132,11 @@ cudaError_t launch_perm_maps(const PermLaunch& L, cudaStream_t s) {
     return cudaMemsetAsync(L.offsets, 0, sizeof(int) * (L.E + 1), s);
   }
   const int blocks = (nc + 7) / 8;
+  g_launches += 3;
   perm_hist_kernel<<<blocks, 256, 0, s>>>(L.topk_idx, L.T, L.k, L.E, L.hist, nc);
-  perm_scan_kernel<<<1, 256, 0, s>>>(L.hist, L.base, L.counts, L.offsets, nc, L.E);
-  perm_pos_kernel<<<blocks, 256, 0, s>>>(L.topk_idx, L.T, L.k, L.E, L.base, L.pos, L.src_row, nc);
+  perm_scan_kernel<<<L.E, 256, 0, s>>>(L.hist, L.base, L.counts, nc, L.E);
+  perm_pos_kernel<<<blocks, 256, 0, s>>>(L.topk_idx, L.T, L.k, L.E, L.base, L.counts, L.offsets, L.pos, L.src_row,
+                                         nc);
   return cudaGetLastError();
 }
 
@@ -124,6 +157,7 @@ cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t
                                 cudaStream_t s) {
   if (R == 0) return cudaSuccess;
   const int dv = d / 8;
+  ++g_launches;
   permute_rows_kernel<<<(R + 7) / 8, 256, 0, s>>>(reinterpret_cast<const uint4*>(xn), src_row,
                                                   reinterpret_cast<uint4*>(xs), R, dv);
   return cudaGetLastError();
@@ -171,6 +205,7 @@ cudaError_t launch_unpermute(const uint16_t* y, const int* pos, const float* w, 
   const long items = (long)T * dv;
   long blocks = (items + 255) / 256;
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+  ++g_launches;
   unpermute_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, resid, out, items, dv, k);
   return cudaGetLastError();
 }
@@ -184,6 +219,7 @@ cudaError_t launch_copy_f32(const float* src, float* dst, long n, cudaStream_t s
   long n4 = n / 4;
   long blocks = (n4 + 255) / 256;
   if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  ++g_launches;
   copy_f32_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst),
                                              n4);
   return cudaGetLastError();

@@ -27,6 +27,7 @@ constexpr int TB = 32;
 constexpr int DC = 64;
 constexpr int LDS = DC + 4;
 constexpr float kU = 5.9604645e-08f;  // 2^-24
+constexpr int kMaxD = 8192;
 
 FSC_DEVINL uint32_t ordered_f32(float v) {
   uint32_t u = __float_as_uint(v);
@@ -57,18 +58,29 @@ FSC_DEVINL float warp_max_f32(float v) {
 }
 }  // namespace
 
-template <int JE>
-__global__ void __launch_bounds__(256) router_kernel(RouterLaunch L) {
-  constexpr int EP = 16 * JE;          // experts padded to a multiple of 16
-  constexpr int QN = (EP + 31) / 32;   // logits per lane in the selection phase
+FSC_DEVINL void cp_async16(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+FSC_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+FSC_DEVINL void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int EW>
+__global__ void __launch_bounds__(128 * EW) router_kernel(RouterLaunch L) {
+  constexpr int EP = 32 * EW;          // experts padded to a multiple of 32
+  constexpr int QN = EW;               // logits per lane in the selection phase
+  constexpr int NW = 4 * EW;           // warps: 2 k-halves x 2 token halves x EW expert groups of 32
+  constexpr int NT = 32 * NW;
+  constexpr int XV = TB * DC / 4 / NT; // float4 of the x chunk per thread
+  constexpr int WV = EP * DC / 4 / NT; // float4 of the W chunk per thread
+  constexpr int BUF = (TB + EP) * LDS; // one stage: x chunk rows then W chunk rows
   extern __shared__ __align__(16) float sm[];
-  float* xs = sm;                      // [TB][LDS]   x*gamma chunk
-  float* ws = xs + TB * LDS;           // [EP][LDS]   W_R chunk
-  float* lg = ws + EP * LDS;           // [TB][EP+1]  fp32 logits
-  float* s_r = lg + TB * (EP + 1);     // [TB]
+  float* stage0 = sm;                  // [2][TB+EP][LDS] double-buffered chunks
+  float* lg = sm;                      // [TB][EP+1] fp32 logits (reuses the stages after the loop)
+  float* s_r = sm + 2 * BUF;           // [TB]
   float* s_xgn = s_r + TB;             // [TB]
   float* s_wsq = s_xgn + TB;           // [EP]
-  double* s_ss = reinterpret_cast<double*>(s_wsq + EP);  // [TB] sum x^2 (fp64)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = L.T, d = L.d, E = L.E, k = L.k;
@@ -77,90 +89,159 @@ __global__ void __launch_bounds__(256) router_kernel(RouterLaunch L) {
   const float* __restrict__ gamma = L.gamma;
   const float* __restrict__ W = L.w_router;
 
-  // ---- phase A: per-token sum of squares (fp64) and ||x*gamma|| (bound only)
-  for (int i = 0; i < TB / 8; ++i) {
-    const int tt = warp * (TB / 8) + i;
+  auto issue_chunk = [&](int c0, float* buf) {
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+      const int i = tid + v * NT;
+      const int tt = i / (DC / 4), cc = (i % (DC / 4)) * 4;
+      const long t = t0 + tt;
+      cp_async16(buf + tt * LDS + cc, x + (t < T ? t : 0) * d + c0 + cc, t < T);
+    }
+#pragma unroll
+    for (int v = 0; v < WV; ++v) {
+      const int i = tid + v * NT;
+      const int e = i / (DC / 4), cc = (i % (DC / 4)) * 4;
+      cp_async16(buf + (TB + e) * LDS + cc, W + (long)(e < E ? e : 0) * d + c0 + cc, e < E);
+    }
+    cp_async_commit();
+  };
+  issue_chunk(0, stage0);
+
+  // ---- phase A: r_t from sum x^2 in fp64; 8 independent 16-byte loads in flight per lane
+  for (int tt = warp; tt < TB; tt += NW) {
     const long t = t0 + tt;
     double ss = 0.0;
-    float xg2 = 0.f;
     if (t < T) {
-      const float* xr = x + t * d;
-      for (int c = lane * 4; c < d; c += 128) {
-        float4 v = *reinterpret_cast<const float4*>(xr + c);
-        float4 g = *reinterpret_cast<const float4*>(gamma + c);
-        ss += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
-        float a = v.x * g.x, b = v.y * g.y, cc = v.z * g.z, dd = v.w * g.w;
-        xg2 += a * a + b * b + cc * cc + dd * dd;
+      const float4* xr = reinterpret_cast<const float4*>(x + t * d);
+      const int dv = d / 4;
+      for (int c = lane; c < dv; c += 256) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (c + 32 * u < dv) ? xr[c + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          ss += ((double)v[u].x * v[u].x + (double)v[u].y * v[u].y) + ((double)v[u].z * v[u].z + (double)v[u].w * v[u].w);
       }
     }
     ss = warp_sum_f64(ss);
-    xg2 = warp_sum_f32(xg2);
-    if (lane == 0) {
-      s_ss[tt] = ss;
-      s_r[tt] = (float)(1.0 / sqrt(ss / (double)d + (double)L.eps));
-      s_xgn[tt] = sqrtf(xg2);
-    }
+    if (lane == 0) s_r[tt] = (float)(1.0 / sqrt(ss / (double)d + (double)L.eps));
   }
   __syncthreads();
 
-  // ---- phase B: register-tiled fp32 logits, two-level accumulation
-  const int ty = tid >> 4, tx = tid & 15;
-  float tot[2][JE], wsq[JE];
+  // ---- phase B: 4x4 register tile per thread, fp32, two-level accumulation.
+  // warp: kg = k-half of each chunk, wt = token half, we = expert group of 32;
+  // lane: lt = 0..3 tokens, le = 0..7 experts. Thread tokens 16 wt + lt + 4 i,
+  // experts 32 we + le + 8 j: every LDS.128 of a warp touches 4 (x) or 8 (W)
+  // distinct rows -> one conflict-free wavefront.
+  const int kg = warp / (2 * EW), rem = warp % (2 * EW);
+  const int wt = rem & 1, we = rem >> 1, lt = lane >> 3, le = lane & 7;
+  float tot[4][4];
 #pragma unroll
-  for (int j = 0; j < JE; ++j) { tot[0][j] = tot[1][j] = 0.f; wsq[j] = 0.f; }
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tot[i][j] = 0.f;
+  float xg2[XV], wq[WV];
+#pragma unroll
+  for (int v = 0; v < XV; ++v) xg2[v] = 0.f;
+#pragma unroll
+  for (int v = 0; v < WV; ++v) wq[v] = 0.f;
 
-  for (int c0 = 0; c0 < d; c0 += DC) {
-    for (int i = tid; i < TB * DC / 4; i += 256) {
+  for (int c0 = 0, it = 0; c0 < d; c0 += DC, ++it) {
+    float* buf = stage0 + (it & 1) * BUF;
+    float* xs = buf;
+    float* ws = buf + TB * LDS;
+    cp_async_wait_all();
+    __syncthreads();
+    // stage: x <- x*gamma in place, write xn = bf16(x*gamma*r), accumulate norms
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+      const int i = tid + v * NT;
       const int tt = i / (DC / 4), cc = (i % (DC / 4)) * 4;
       const long t = t0 + tt;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (t < T) v = *reinterpret_cast<const float4*>(x + t * d + c0 + cc);
+      float4* p = reinterpret_cast<float4*>(xs + tt * LDS + cc);
+      const float4 xv = *p;
       const float4 g = *reinterpret_cast<const float4*>(gamma + c0 + cc);
-      float4 xg = make_float4(v.x * g.x, v.y * g.y, v.z * g.z, v.w * g.w);
-      *reinterpret_cast<float4*>(xs + tt * LDS + cc) = xg;
+      const float4 xg = make_float4(xv.x * g.x, xv.y * g.y, xv.z * g.z, xv.w * g.w);
+      *p = xg;
+      xg2[v] += xg.x * xg.x + xg.y * xg.y + xg.z * xg.z + xg.w * xg.w;
       if (t < T) {
         const float r = s_r[tt];
         uint2 o = make_uint2(pack_bf16x2(xg.x * r, xg.y * r), pack_bf16x2(xg.z * r, xg.w * r));
         *reinterpret_cast<uint2*>(L.xn + t * d + c0 + cc) = o;
       }
     }
-    for (int i = tid; i < EP * DC / 4; i += 256) {
+#pragma unroll
+    for (int v = 0; v < WV; ++v) {
+      const int i = tid + v * NT;
       const int e = i / (DC / 4), cc = (i % (DC / 4)) * 4;
-      float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e < E) w = *reinterpret_cast<const float4*>(W + (long)e * d + c0 + cc);
-      *reinterpret_cast<float4*>(ws + e * LDS + cc) = w;
+      const float4 w = *reinterpret_cast<const float4*>(ws + e * LDS + cc);
+      wq[v] += w.x * w.x + w.y * w.y + w.z * w.z + w.w * w.w;
     }
     __syncthreads();
-    float part[2][JE];
+    if (c0 + DC < d) issue_chunk(c0 + DC, stage0 + ((it + 1) & 1) * BUF);  // next chunk in flight
+    float part[4][4];
 #pragma unroll
-    for (int j = 0; j < JE; ++j) part[0][j] = part[1][j] = 0.f;
-#pragma unroll 4
-    for (int kk = 0; kk < DC; kk += 4) {
-      const float4 a0 = *reinterpret_cast<const float4*>(xs + ty * LDS + kk);
-      const float4 a1 = *reinterpret_cast<const float4*>(xs + (ty + 16) * LDS + kk);
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < JE; ++j) {
-        const float4 b = *reinterpret_cast<const float4*>(ws + (tx + 16 * j) * LDS + kk);
-        part[0][j] = fmaf(a0.x, b.x, part[0][j]);
-        part[0][j] = fmaf(a0.y, b.y, part[0][j]);
-        part[0][j] = fmaf(a0.z, b.z, part[0][j]);
-        part[0][j] = fmaf(a0.w, b.w, part[0][j]);
-        part[1][j] = fmaf(a1.x, b.x, part[1][j]);
-        part[1][j] = fmaf(a1.y, b.y, part[1][j]);
-        part[1][j] = fmaf(a1.z, b.z, part[1][j]);
-        part[1][j] = fmaf(a1.w, b.w, part[1][j]);
-        if (ty == 0) wsq[j] += b.x * b.x + b.y * b.y + b.z * b.z + b.w * b.w;
-      }
+      for (int j = 0; j < 4; ++j) part[i][j] = 0.f;
+    const float* xa = xs + (16 * wt + lt) * LDS + kg * (DC / 2);
+    const float* wb = ws + (32 * we + le) * LDS + kg * (DC / 2);
+#pragma unroll
+    for (int kk = 0; kk < DC / 2; kk += 4) {
+      float4 a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(xa + 4 * i * LDS + kk);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const float4*>(wb + 8 * j * LDS + kk);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          part[i][j] = fmaf(a[i].x, b[j].x, part[i][j]);
+          part[i][j] = fmaf(a[i].y, b[j].y, part[i][j]);
+          part[i][j] = fmaf(a[i].z, b[j].z, part[i][j]);
+          part[i][j] = fmaf(a[i].w, b[j].w, part[i][j]);
+        }
     }
 #pragma unroll
-    for (int j = 0; j < JE; ++j) { tot[0][j] += part[0][j]; tot[1][j] += part[1][j]; }
-    __syncthreads();
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tot[i][j] += part[i][j];
+  }
+  __syncthreads();   // all compute done before lg overwrites the stages
+  // per-row norms: the 16 consecutive threads staging a row hold its partials
+#pragma unroll
+  for (int v = 0; v < XV; ++v) {
+    float b = xg2[v];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffff, b, o);
+    if ((tid & 15) == 0) s_xgn[(tid + v * NT) / (DC / 4)] = sqrtf(b);
   }
 #pragma unroll
-  for (int j = 0; j < JE; ++j) {
-    lg[ty * (EP + 1) + tx + 16 * j] = tot[0][j] * s_r[ty];
-    lg[(ty + 16) * (EP + 1) + tx + 16 * j] = tot[1][j] * s_r[ty + 16];
-    if (ty == 0) s_wsq[tx + 16 * j] = wsq[j];
+  for (int v = 0; v < WV; ++v) {
+    float b = wq[v];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffff, b, o);
+    if ((tid & 15) == 0) s_wsq[(tid + v * NT) / (DC / 4)] = b;
+  }
+  // combine the two k-halves in a fixed order: lg = (tot_0 + tot_1) * r
+  if (kg == 1) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) lg[(16 * wt + lt + 4 * i) * (EP + 1) + 32 * we + le + 8 * j] = tot[i][j];
+  }
+  __syncthreads();
+  if (kg == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int tt = 16 * wt + lt + 4 * i;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float* p = &lg[tt * (EP + 1) + 32 * we + le + 8 * j];
+        *p = (tot[i][j] + *p) * s_r[tt];
+      }
+    }
   }
   __syncthreads();
 
@@ -169,8 +250,7 @@ __global__ void __launch_bounds__(256) router_kernel(RouterLaunch L) {
   for (int e = lane; e < E; e += 32) wm = fmaxf(wm, s_wsq[e]);
   const float wmax = sqrtf(warp_max_f32(wm)) * 1.01f;
 
-  for (int i = 0; i < TB / 8; ++i) {
-    const int tt = warp * (TB / 8) + i;
+  for (int tt = warp; tt < TB; tt += NW) {
     const long t = t0 + tt;
     if (t >= T) break;
     float v[QN];
@@ -218,7 +298,6 @@ __global__ void __launch_bounds__(256) router_kernel(RouterLaunch L) {
       const float thr = 2.f * B + 4.f * kU * (fabsf(vk) + fabsf(vk1)) + 1e-7f;
       refine = gap <= thr;
     }
-    const float* xr = x + t * d;
     if (!refine) {
       float ex[QN], sum = 0.f;
 #pragma unroll
@@ -238,87 +317,142 @@ __global__ void __launch_bounds__(256) router_kernel(RouterLaunch L) {
         }
         slot += __popc(m);
       }
-    } else {
-      // fp64 recomputation of every logit of this token, then re-selection
-      if (lane == 0 && L.n_refined) atomicAdd(L.n_refined, 1);
-      const double rinv = 1.0 / sqrt(s_ss[tt] / (double)d + (double)L.eps);
-      double l64[QN];
+    } else if (lane == 0) {
+      // near tie: hand the token to router_refine_kernel (fp64 recomputation)
+      if (L.n_refined) atomicAdd(L.n_refined, 1);
+      L.rf_list[atomicAdd(&L.rf_ctrl[0], 1)] = (int)t;
+    }
+  }
+
+}
+
+// fp64 recomputation of the logits of flagged tokens: one warp per (token, expert),
+// eight independent accumulators per lane so 8 W loads are in flight per step.
+// Stores the raw dot sum_i (x_i gamma_i) W_ei (exact fp64 products of fp32 inputs).
+__global__ void __launch_bounds__(256) router_refine_logits_kernel(RouterLaunch L) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int d = L.d, E = L.E;
+  const int n = *reinterpret_cast<volatile int*>(&L.rf_ctrl[0]);
+  for (int item = gw; item < n * E; item += nw) {
+    const long t = L.rf_list[item / E];
+    const int e = item % E;
+    const float* xr = L.x + t * d;
+    const float* wr = L.w_router + (long)e * d;
+    double acc[8];
 #pragma unroll
-      for (int q = 0; q < QN; ++q) l64[q] = -DBL_MAX;
-      for (int e = 0; e < E; ++e) {
-        const float* wr = W + (long)e * d;
-        double s = 0.0;
-        for (int c = lane; c < d; c += 32) s += (double)xr[c] * (double)gamma[c] * (double)wr[c];
-        s = warp_sum_f64(s) * rinv;
-        if ((e & 31) == lane) {
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    for (int c0 = 0; c0 < d; c0 += 256) {
 #pragma unroll
-          for (int q = 0; q < QN; ++q)
-            if ((e >> 5) == q) l64[q] = s;
-        }
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + lane + 32 * u;
+        if (c < d) acc[u] = fma((double)xr[c] * (double)L.gamma[c], (double)wr[c], acc[u]);
       }
-      uint32_t sb = 0;
-      double dtop = 0.0;
-      for (int rd = 0; rd < k; ++rd) {
-        double bv = -DBL_MAX;
-        int bi = 0x7fffffff;
+    }
+    double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    s = warp_sum_f64(s);
+    if (lane == 0) L.rf_l64[item] = s;
+  }
+}
+
+// Re-selection of the flagged tokens from their fp64 logits (one warp per token);
+// the last CTA to finish resets the flag list for the next call.
+template <int EW>
+__global__ void __launch_bounds__(256) router_refine_select_kernel(RouterLaunch L) {
+  constexpr int QN = EW;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int d = L.d, E = L.E, k = L.k;
+  const int n = *reinterpret_cast<volatile int*>(&L.rf_ctrl[0]);
+  for (int i = gw; i < n; i += nw) {
+    const long t = L.rf_list[i];
+    const float* xr = L.x + t * d;
+    double ss = 0.0;
+    for (int c = lane; c < d; c += 32) ss += (double)xr[c] * (double)xr[c];
+    ss = warp_sum_f64(ss);
+    const double rinv = 1.0 / sqrt(ss / (double)d + (double)L.eps);
+    double l64[QN];
 #pragma unroll
-        for (int q = 0; q < QN; ++q) {
-          const int e = lane + 32 * q;
-          if (e < E && !((sb >> q) & 1u) && (l64[q] > bv || (l64[q] == bv && e < bi))) { bv = l64[q]; bi = e; }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffff, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffff, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-        }
-        if ((bi & 31) == lane) sb |= 1u << (bi >> 5);
-        if (rd == 0) dtop = bv;
-      }
-      double ex[QN], sum = 0.0;
+    for (int q = 0; q < QN; ++q) {
+      const int e = lane + 32 * q;
+      l64[q] = e < E ? L.rf_l64[(long)i * E + e] * rinv : -DBL_MAX;
+    }
+    uint32_t sb = 0;
+    double dtop = 0.0;
+    for (int rd = 0; rd < k; ++rd) {
+      double bv = -DBL_MAX;
+      int bi = 0x7fffffff;
 #pragma unroll
       for (int q = 0; q < QN; ++q) {
-        ex[q] = ((sb >> q) & 1u) ? exp(l64[q] - dtop) : 0.0;
-        sum += ex[q];
+        const int e = lane + 32 * q;
+        if (e < E && !((sb >> q) & 1u) && (l64[q] > bv || (l64[q] == bv && e < bi))) { bv = l64[q]; bi = e; }
       }
-      sum = warp_sum_f64(sum);
-      int slot = 0;
 #pragma unroll
-      for (int q = 0; q < QN; ++q) {
-        const uint32_t m = __ballot_sync(0xffffffff, (sb >> q) & 1u);
-        if ((sb >> q) & 1u) {
-          const int s = slot + __popc(m & ((1u << lane) - 1u));
-          L.topk_idx[t * k + s] = lane + 32 * q;
-          L.topk_w[t * k + s] = (float)(ex[q] / sum);
-        }
-        slot += __popc(m);
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffff, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffff, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
       }
+      if ((bi & 31) == lane) sb |= 1u << (bi >> 5);
+      if (rd == 0) dtop = bv;
+    }
+    double ex[QN], sum = 0.0;
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+      ex[q] = ((sb >> q) & 1u) ? exp(l64[q] - dtop) : 0.0;
+      sum += ex[q];
+    }
+    sum = warp_sum_f64(sum);
+    int slot = 0;
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+      const uint32_t m = __ballot_sync(0xffffffff, (sb >> q) & 1u);
+      if ((sb >> q) & 1u) {
+        const int s = slot + __popc(m & ((1u << lane) - 1u));
+        L.topk_idx[t * k + s] = lane + 32 * q;
+        L.topk_w[t * k + s] = (float)(ex[q] / sum);
+      }
+      slot += __popc(m);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&L.rf_ctrl[1], 1) == (int)gridDim.x - 1) {
+      L.rf_ctrl[0] = 0;
+      L.rf_ctrl[1] = 0;
+      __threadfence();
     }
   }
 }
 
-template <int JE>
+template <int EW>
 static cudaError_t launch_router_t(const RouterLaunch& L, cudaStream_t s) {
-  constexpr int EP = 16 * JE;
-  const size_t smem = (size_t)(TB * LDS + EP * LDS + TB * (EP + 1) + 2 * TB + EP) * 4 + TB * 8 + 16;
+  constexpr int EP = 32 * EW;
+  const size_t smem = (size_t)(2 * (TB + EP) * LDS + 2 * TB + EP) * 4 + 16;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(router_kernel<JE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(router_kernel<EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int grid = (L.T + TB - 1) / TB;
-  router_kernel<JE><<<grid, 256, smem, s>>>(L);
+  g_launches += 3;
+  router_kernel<EW><<<grid, 128 * EW, smem, s>>>(L);
+  router_refine_logits_kernel<<<4 * kNumSMs, 256, 0, s>>>(L);
+  router_refine_select_kernel<EW><<<16, 256, 0, s>>>(L);
   return cudaGetLastError();
 }
 
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s) {
   if (L.T == 0) return cudaSuccess;
-  if (L.d % DC || L.E < 1 || L.E > 128 || L.k < 1 || L.k > L.E) return cudaErrorInvalidValue;
-  if (L.E <= 16) return launch_router_t<1>(L, s);
-  if (L.E <= 32) return launch_router_t<2>(L, s);
-  if (L.E <= 64) return launch_router_t<4>(L, s);
-  return launch_router_t<8>(L, s);
+  if (L.d % DC || L.d > kMaxD || L.E < 1 || L.E > 128 || L.k < 1 || L.k > L.E) return cudaErrorInvalidValue;
+  if (!L.rf_list || !L.rf_ctrl) return cudaErrorInvalidValue;
+  if (L.E <= 32) return launch_router_t<1>(L, s);
+  if (L.E <= 64) return launch_router_t<2>(L, s);
+  return launch_router_t<4>(L, s);
 }
 
 }  // namespace fsc

@@ -39,8 +39,10 @@ GEMM_CASES = [
 ]
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("counts,N,K", GEMM_CASES)
-def test_grouped_gemm_bf16(ctx, counts, N, K):
+def test_grouped_gemm_bf16(ctx, counts, N, K, cg):
+    ctx.set_gemm_cta_group(cg)
     rng = np.random.default_rng(len(counts) * 1000 + N + K)
     G, M = len(counts), sum(counts)
     A = rand_bf16(rng, (max(M, 1), K))
@@ -61,8 +63,10 @@ def test_grouped_gemm_bf16(ctx, counts, N, K):
 
 
 @pytest.mark.parametrize("counts,N,K", [([1], 128, 64), ([0, 130, 257], 128, 128), ([333, 900, 17], 1408, 2048),
-                                        ([40], 64, 64), ([256, 1], 8192, 128)])
-def test_grouped_gemm_swiglu(ctx, counts, N, K):
+                                        ([40], 64, 64), ([256, 1], 8192, 128), ([600, 0, 257, 255], 768, 2048)])
+@pytest.mark.parametrize("cg", [1, 2])
+def test_grouped_gemm_swiglu(ctx, counts, N, K, cg):
+    ctx.set_gemm_cta_group(cg)
     rng = np.random.default_rng(7 + N + K)
     G, M = len(counts), sum(counts)
     A = rand_bf16(rng, (M, K))
@@ -84,8 +88,10 @@ def test_grouped_gemm_swiglu(ctx, counts, N, K):
         r += m
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("with_resid", [True, False])
-def test_gemm_resid_f32_single_group(ctx, with_resid):
+def test_gemm_resid_f32_single_group(ctx, with_resid, cg):
+    ctx.set_gemm_cta_group(cg)
     rng = np.random.default_rng(3)
     M, N, K = 777, 2048, 2816
     A = rand_bf16(rng, (M, K))
@@ -102,7 +108,9 @@ def test_gemm_resid_f32_single_group(ctx, with_resid):
     assert rel_l2(out.cpu().numpy(), ref) < 1e-5
 
 
-def test_gemm_inplace_resid(ctx):
+@pytest.mark.parametrize("cg", [1, 2])
+def test_gemm_inplace_resid(ctx, cg):
+    ctx.set_gemm_cta_group(cg)
     rng = np.random.default_rng(4)
     M, N, K = 300, 512, 64
     A = rand_bf16(rng, (M, K)); B = rand_bf16(rng, (N, K))
