@@ -138,6 +138,14 @@ class AttnWeights:
         self.c = AttnWeightsC(ptr(gamma), ptr(w_qkv), ptr(w_o), n_heads, n_kv_heads, head_dim, rope_theta)
 
 
+def exchange_blobs(blob: bytes, group=None):
+    """All-gather one bytes blob per rank, returned in rank order (torch.distributed)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, blob, group=group)
+    return out
+
+
 class Context:
     """One EP rank's libfsc context."""
 
@@ -177,6 +185,13 @@ class Context:
         buf = ctypes.create_string_buffer(max(n, 1))
         self._ck(self.lib.fsc_bootstrap_export(self.h, buf))
         return buf.raw[:n]
+
+    def connect(self, group=None):
+        """Bootstrap the EP transport: every rank exports its peer-region handle,
+        the handles are all-gathered in rank order over torch.distributed (host
+        plumbing only), and every rank maps its peers'."""
+        blob = self.bootstrap_export()
+        self.bootstrap_import(exchange_blobs(blob, group))
 
     def bootstrap_import(self, blobs: Sequence[bytes]):
         data = b"".join(blobs)

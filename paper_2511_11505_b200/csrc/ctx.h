@@ -78,3 +78,4 @@ int fsc_transport_dispatch(fsc_ctx* ctx, int T, cudaStream_t s);
 int fsc_transport_dispatch_wait(fsc_ctx* ctx, cudaStream_t s);
 int fsc_transport_combine(fsc_ctx* ctx, int T, cudaStream_t s);
 int fsc_transport_combine_wait(fsc_ctx* ctx, cudaStream_t s);
+void fsc_transport_scatter_target(fsc_ctx* ctx, const int** ret, void** peer_out);

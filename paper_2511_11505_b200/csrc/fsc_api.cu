@@ -45,13 +45,15 @@ namespace fsc {
 long g_launches = 0;
 }
 
-#define PH_BEGIN(i) \
-  if (ctx->timing) CK(cudaEventRecord(ctx->ph_ev[i][0], s))
-#define PH_END(i)                                  \
+#define PH_BEGIN_ON(i, st) \
+  if (ctx->timing) CK(cudaEventRecord(ctx->ph_ev[i][0], st))
+#define PH_END_ON(i, st)                           \
   if (ctx->timing) {                               \
-    CK(cudaEventRecord(ctx->ph_ev[i][1], s));      \
+    CK(cudaEventRecord(ctx->ph_ev[i][1], st));     \
     ctx->ph_used[i] = 1;                           \
   }
+#define PH_BEGIN(i) PH_BEGIN_ON(i, s)
+#define PH_END(i) PH_END_ON(i, s)
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -216,7 +218,8 @@ static int validate_call(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const fl
 // the routed expert outputs y are complete in this rank's receive layout and,
 // for EP > 1, already pushed back toward their source ranks (combine started).
 static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in,
-                                 const fsc_moe_debug* dbg, cudaStream_t s, fsc_overlap_cb cb, void* user) {
+                                 const fsc_moe_debug* dbg, cudaStream_t s, fsc_overlap_cb cb, void* user,
+                                 bool overlap) {
   const fsc_moe_config& c = ctx->cfg;
   const int d = c.d, E = c.n_experts, k = c.top_k;
   RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
@@ -234,29 +237,38 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     if (dbg->counts) CK(cudaMemcpyAsync(dbg->counts, ctx->counts, sizeof(int) * E, cudaMemcpyDeviceToDevice, s));
     if (dbg->pos) CK(cudaMemcpyAsync(dbg->pos, ctx->pos, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
   }
-  // Dispatch: permute into the expert-sorted send buffer, then move
-  // rows to the owning ranks. At EP=1 the permuted buffer is the receive buffer.
+  // Dispatch: permute into the expert-sorted order and, for EP > 1,
+  // straight into the owning ranks' receive buffers. In the FarSkip schedule the
+  // counts exchange and dispatch run on the comm stream (P:198 step 4) while the
+  // caller's attention part (b) runs on the compute stream (step 5).
   const int R = T * k;
   const uint16_t* recv = ctx->xs;
   long recv_rows = R;
   const int* recv_counts = ctx->counts;
+  cudaStream_t cs = overlap ? ctx->comm : s;
   if (ctx->ep == 1) {
     PH_BEGIN(PH_DISPATCH);
     CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, s));
     PH_END(PH_DISPATCH);
   } else {
-    int rc = fsc_transport_dispatch(ctx, T, s);
+    if (overlap) {
+      CK(cudaEventRecord(ctx->ev_a, s));
+      CK(cudaStreamWaitEvent(cs, ctx->ev_a, 0));
+    }
+    PH_BEGIN_ON(PH_DISPATCH, cs);
+    int rc = fsc_transport_dispatch(ctx, T, cs);
     if (rc) return rc;
+    rc = fsc_transport_dispatch_wait(ctx, cs);
+    if (rc) return rc;
+    PH_END_ON(PH_DISPATCH, cs);
+    if (overlap) CK(cudaEventRecord(ctx->ev_b, cs));
     recv = ctx->xr;
     recv_rows = ctx->recv_rows_cap;
     recv_counts = ctx->recv_counts;
   }
   if (cb) cb(user, 0, s);  // P:198 step 5: attention part (b) while dispatch is in flight
-  if (ctx->ep > 1) {
-    int rc = fsc_transport_dispatch_wait(ctx, s);
-    if (rc) return rc;
-  }
-  // Routed experts (P:198 step 6): GEMM1 + SwiGLU, GEMM2
+  if (ctx->ep > 1 && overlap) CK(cudaStreamWaitEvent(s, ctx->ev_b, 0));  // step 6: sync Dispatch
+  // Routed experts (P:198 step 6): GEMM1 + SwiGLU, GEMM2 (+ fused Combine for EP > 1)
   GemmLaunch g1{};
   g1.A = recv; g1.a_rows = recv_rows; g1.B0 = w->w1; g1.B1 = w->w2; g1.b_rows = (long)ctx->e_loc * c.ffn;
   g1.b_group_rows = c.ffn; g1.K = d; g1.N = c.ffn; g1.G = ctx->e_loc; g1.counts = recv_counts; g1.m_total = 0;
@@ -267,13 +279,16 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   GemmLaunch g2{};
   g2.A = ctx->h; g2.a_rows = recv_rows; g2.B0 = w->w3; g2.B1 = nullptr; g2.b_rows = (long)ctx->e_loc * d;
   g2.b_group_rows = d; g2.K = c.ffn; g2.N = d; g2.G = ctx->e_loc; g2.counts = recv_counts; g2.m_total = 0;
-  g2.out = (ctx->ep == 1) ? ctx->y : ctx->yr; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = ctx->gemm_cg;
+  g2.out = ctx->y; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = ctx->gemm_cg;
+  if (ctx->ep > 1) fsc_transport_scatter_target(ctx, &g2.ret, g2.peer_out);  // P:100 Combine, fused
   PH_BEGIN(PH_GEMM2);
   CK(launch_grouped_gemm(g2, s));
   PH_END(PH_GEMM2);
   if (ctx->ep > 1) {
-    int rc = fsc_transport_combine(ctx, T, s);  // P:198 step 7: start Combine
+    PH_BEGIN(PH_COMBINE);
+    int rc = fsc_transport_combine(ctx, T, s);  // P:198 step 7: Combine completes asynchronously
     if (rc) return rc;
+    PH_END(PH_COMBINE);
   }
   return FSC_OK;
 }
@@ -339,7 +354,7 @@ extern "C" int fsc_moe_forward_blocking(fsc_ctx* ctx, const fsc_moe_weights* w, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (T == 0 && ctx->ep == 1) return FSC_OK;
   memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
-  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr);
+  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false);
   if (rc) return rc;
   // Regular order (C-amb-12): tmp = x_in + shared; out = tmp + routed.
   rc = moe_shared(ctx, w, T, x_in, ctx->tmp, dbg, s);
@@ -373,7 +388,7 @@ extern "C" int fsc_moe_forward_farskip(fsc_ctx* ctx, const fsc_moe_weights* w, i
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
-  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, cb, user);
+  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, cb, user, true);
   if (rc) return rc;
   if (cb) cb(user, 1, s);  // combine in flight
   // P:198 step 8 and C-amb-12: attn-in_{k+1} = (mlp-in_k + attn-out_k) + shared-out_k

@@ -266,7 +266,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else if (EPI == EPI_BF16) {
-        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + ti.nb * BN;
+        __nv_bfloat16* out;
+        if (p.ret) {     // fused combine: write the row straight into its source rank's buffer
+          const int v = valid ? p.ret[grow] : 0;
+          out = reinterpret_cast<__nv_bfloat16*>(p.peer_out[(uint32_t)v >> 24]) + (long)(v & 0xFFFFFF) * p.ldo +
+                ti.nb * BN;
+        } else {
+          out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + ti.nb * BN;
+        }
 #pragma unroll 1
         for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
           uint32_t v[32];
@@ -375,6 +382,8 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   p.ldo = L.ldo;
   p.resid = L.resid;
   p.ldr = L.ldr;
+  p.ret = L.ret;
+  for (int i = 0; i < 8; ++i) p.peer_out[i] = L.peer_out[i];
   int grid = L.num_ctas > 0 ? L.num_ctas : kNumSMs;
   if (CG == 2) grid &= ~1;
   if (grid < CG) grid = CG;

@@ -21,6 +21,10 @@ struct GemmParams {
   long ldo;
   const float* resid;
   long ldr;
+  // EPI_BF16 scatter (fused combine): row r of the tile goes to rank
+  // (ret[r] >> 24), row (ret[r] & 0xFFFFFF) of peer_out[rank]; nullptr = local store
+  const int* ret;
+  void* peer_out[8];
 };
 
 struct GemmLaunch {
@@ -40,6 +44,8 @@ struct GemmLaunch {
   int epi;
   int num_ctas;       // persistent grid (<= 148); 0 = all SMs
   int cta_group = 2;  // 2: CTA pairs, MMA M=256 (default); 1: single-CTA M=128 tiles
+  const int* ret = nullptr;           // scatter map (see GemmParams)
+  void* peer_out[8] = {};
 };
 
 cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s);

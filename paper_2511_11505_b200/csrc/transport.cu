@@ -1,18 +1,306 @@
-// EP transport (dispatch / combine between ranks). Round-1 state: EP == 1 only;
-// the peer-memory path is built next.
-#include "ctx.h"
+// EP transport: Dispatch / Combine between the P ranks of an expert-parallel
+// group (§2 "Dispatch" and "Combine"), device-initiated over
+// peer memory. Every rank exports one symmetric region (CUDA IPC handle) that
+// the others map; all data movement and synchronisation then happens inside
+// kernels, with no host round trip:
+//
+//   counts  (a5): each source s writes its per-expert counts into row s of every
+//                 peer's cnt matrix [P][E], raises flag_cnt[s] there, and waits
+//                 until all P rows of its own matrix are in. Every rank then
+//                 knows the full matrix and derives, without further exchange,
+//                 where its rows land in each destination's receive buffer.
+//   dispatch(a6): the permute kernel writes each copy (t, j) of xn straight into
+//                 the owning rank's receive buffer xr (expert-major, then source
+//                 rank, then token: C-amb-11) plus the return address of the row;
+//                 the last CTA raises flag_disp[s] at every destination.
+//   combine (a9): fused into the down-projection GEMM's epilogue (gemm.cu,
+//                 EPI_BF16 with a scatter map): each output row is stored into its
+//                 source rank's ys buffer at the row it was sent from; a signal
+//                 kernel then raises flag_comb at every source.
+// Flags carry a per-call epoch, so nothing is ever reset. The same code serves
+// P processes on one GPU (tests) and one process per GPU over NVLink/NVSwitch.
+#include <string.h>
 
-size_t fsc_transport_blob_size() { return 0; }
+#include "common.cuh"
+#include "ctx.h"
+#include "kernels.h"
+
+using namespace fsc;
+
+namespace {
+constexpr int kMaxP = 8;
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+struct Layout {  // byte offsets inside every rank's symmetric region
+  size_t flags, cnt, ret, xr, ys, total;
+};
+
+Layout layout_for(const fsc_ctx* c) {
+  Layout L{};
+  const size_t P = c->ep, E = c->cfg.n_experts, d = c->cfg.d;
+  const size_t Tk = (size_t)c->cfg.max_tokens * c->cfg.top_k;
+  L.flags = 0;                                       // int [3][kMaxP]
+  L.cnt = align_up(L.flags + 3 * kMaxP * sizeof(int));
+  L.ret = align_up(L.cnt + P * E * sizeof(int));     // int [max_recv]
+  L.xr = align_up(L.ret + (size_t)c->max_recv * sizeof(int));
+  L.ys = align_up(L.xr + (size_t)c->max_recv * d * 2);
+  L.total = align_up(L.ys + Tk * d * 2);
+  return L;
+}
+
+struct Peers {
+  char* base[kMaxP];
+};
+
+enum { FLAG_CNT = 0, FLAG_DISP = 1, FLAG_COMB = 2 };
+
+FSC_DEVINL int* flag_ptr(char* base, int slot, int src) {
+  return reinterpret_cast<int*>(base) + slot * kMaxP + src;
+}
+FSC_DEVINL void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+FSC_DEVINL int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+FSC_DEVINL void wait_flags(char* mybase, int slot, int P, int epoch) {
+  for (int s = 0; s < P; ++s) {
+    const int* f = flag_ptr(mybase, slot, s);
+    while (ld_acquire_sys(f) - epoch < 0) __nanosleep(64);
+  }
+}
+}  // namespace
+
+struct fsc_peer_state {
+  char* local = nullptr;          // my symmetric region
+  Layout lay{};
+  Peers peers{};                  // mapped regions of every rank (peers.base[rank] == local)
+  cudaIpcMemHandle_t my_handle{};
+  bool opened[kMaxP] = {};
+  int* send_base = nullptr;       // [E]   first row of my expert-e rows in the owner's xr
+  int* ticket = nullptr;          // [1]   dispatch-kernel completion ticket
+  int epoch = 0;
+};
+
+// ----------------------------------------------------------------------------- kernels
+
+// a5: counts all-gather through peer stores + receive-side bookkeeping.
+__global__ void __launch_bounds__(256) ep_counts_kernel(Peers peers, int rank, int P, int E, int e_loc, int epoch,
+                                                        size_t off_cnt, const int* __restrict__ counts,
+                                                        int* __restrict__ send_base, int* __restrict__ recv_counts) {
+  __shared__ int cnt[kMaxP * 128];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < P * E; i += blockDim.x) {
+    const int p = i / E, e = i % E;
+    reinterpret_cast<int*>(peers.base[p] + off_cnt)[rank * E + e] = counts[e];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (tid < P) st_release_sys(flag_ptr(peers.base[tid], FLAG_CNT, rank), epoch);
+  if (tid == 0) wait_flags(peers.base[rank], FLAG_CNT, P, epoch);
+  __syncthreads();
+  const int* my = reinterpret_cast<const int*>(peers.base[rank] + off_cnt);
+  for (int i = tid; i < P * E; i += blockDim.x) cnt[i] = ld_acquire_sys(my + i);
+  __syncthreads();
+  // send_base[e]: where my copies for expert e start inside its owner's receive
+  // buffer = rows of the owner's earlier local experts (all sources) + rows of
+  // expert e from lower-ranked sources (C-amb-11 layout).
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int p = e / e_loc;
+    int b = 0;
+    for (int e2 = p * e_loc; e2 < e; ++e2)
+      for (int s = 0; s < P; ++s) b += cnt[s * E + e2];
+    for (int s = 0; s < rank; ++s) b += cnt[s * E + e];
+    send_base[e] = b;
+  }
+  for (int el = tid; el < e_loc; el += blockDim.x) {
+    int m = 0;
+    for (int s = 0; s < P; ++s) m += cnt[s * E + rank * e_loc + el];
+    recv_counts[el] = m;
+  }
+}
+
+// a4 + a6: permute-and-dispatch. One warp per send row q (expert-sorted order).
+__global__ void __launch_bounds__(256) ep_dispatch_kernel(Peers peers, int rank, int P, int R, int d, int E,
+                                                          int e_loc, int epoch, size_t off_xr, size_t off_ret,
+                                                          const uint4* __restrict__ xn, const int* __restrict__ src_row,
+                                                          const int* __restrict__ offsets,
+                                                          const int* __restrict__ send_base, int* ticket) {
+  __shared__ int s_off[129];
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) s_off[i] = offsets[i];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dv = d / 8;
+  for (long q = (long)blockIdx.x * 8 + w; q < R; q += (long)gridDim.x * 8) {
+    int lo = 0, hi = E;                    // expert of send row q
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[mid] <= q) lo = mid; else hi = mid;
+    }
+    const int e = lo, p = e / e_loc;
+    const long dst = send_base[e] + (q - s_off[e]);
+    const uint4* a = xn + (long)src_row[q] * dv;
+    uint4* b = reinterpret_cast<uint4*>(peers.base[p] + off_xr) + dst * dv;
+    for (int i = lane; i < dv; i += 32) b[i] = a[i];
+    if (lane == 0) reinterpret_cast<int*>(peers.base[p] + off_ret)[dst] = (rank << 24) | (int)q;
+  }
+  // last CTA out raises the dispatch flag at every destination
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(ticket, 1) == (int)gridDim.x - 1) {
+      *ticket = 0;
+      __threadfence_system();
+      for (int p = 0; p < P; ++p) st_release_sys(flag_ptr(peers.base[p], FLAG_DISP, rank), epoch);
+    }
+  }
+}
+
+__global__ void ep_signal_kernel(Peers peers, int rank, int P, int slot, int epoch) {
+  __threadfence_system();
+  if (threadIdx.x < P) st_release_sys(flag_ptr(peers.base[threadIdx.x], slot, rank), epoch);
+}
+
+__global__ void ep_wait_kernel(char* mybase, int slot, int P, int epoch) {
+  if (threadIdx.x == 0) wait_flags(mybase, slot, P, epoch);
+  __syncthreads();
+}
+
+// ----------------------------------------------------------------------------- host side
+
+size_t fsc_transport_blob_size() { return sizeof(cudaIpcMemHandle_t); }
+
+#define TCK(call)                                                                                 \
+  do {                                                                                            \
+    cudaError_t e__ = (call);                                                                     \
+    if (e__ != cudaSuccess) {                                                                     \
+      fsc_set_error(ctx, "transport %s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e__)); \
+      ctx->sticky = FSC_ERR_COMM;                                                                 \
+      return FSC_ERR_COMM;                                                                        \
+    }                                                                                             \
+  } while (0)
 
 int fsc_transport_init(fsc_ctx* ctx) {
   if (ctx->ep == 1) return FSC_OK;
-  fsc_set_error(ctx, "ep_size > 1 transport not available in this build");
-  return FSC_ERR_COMM;
+  if (ctx->ep > kMaxP) {
+    fsc_set_error(ctx, "ep_size %d > %d", ctx->ep, kMaxP);
+    return FSC_ERR_CONFIG;
+  }
+  fsc_peer_state* st = new fsc_peer_state();
+  ctx->peer = st;
+  st->lay = layout_for(ctx);
+  TCK(cudaMalloc(&st->local, st->lay.total));
+  TCK(cudaMemset(st->local, 0, st->lay.flags + 3 * kMaxP * sizeof(int)));
+  TCK(cudaIpcGetMemHandle(&st->my_handle, st->local));
+  TCK(cudaMalloc(&st->send_base, sizeof(int) * ctx->cfg.n_experts));
+  TCK(cudaMalloc(&st->ticket, sizeof(int)));
+  TCK(cudaMemset(st->ticket, 0, sizeof(int)));
+  TCK(cudaMalloc(&ctx->recv_counts, sizeof(int) * ctx->e_loc));
+  ctx->xr = reinterpret_cast<uint16_t*>(st->local + st->lay.xr);
+  ctx->ys = reinterpret_cast<uint16_t*>(st->local + st->lay.ys);
+  ctx->recv_rows_cap = ctx->max_recv;
+  st->peers.base[ctx->rank] = st->local;
+  TCK(cudaDeviceSynchronize());
+  return FSC_OK;
 }
-int fsc_transport_export(fsc_ctx* ctx, void*) { return ctx->ep == 1 ? FSC_OK : FSC_ERR_COMM; }
-int fsc_transport_import(fsc_ctx* ctx, const void*) { return ctx->ep == 1 ? FSC_OK : FSC_ERR_COMM; }
-void fsc_transport_finalize(fsc_ctx*) {}
-int fsc_transport_dispatch(fsc_ctx*, int, cudaStream_t) { return FSC_ERR_COMM; }
-int fsc_transport_dispatch_wait(fsc_ctx*, cudaStream_t) { return FSC_ERR_COMM; }
-int fsc_transport_combine(fsc_ctx*, int, cudaStream_t) { return FSC_ERR_COMM; }
-int fsc_transport_combine_wait(fsc_ctx*, cudaStream_t) { return FSC_ERR_COMM; }
+
+int fsc_transport_export(fsc_ctx* ctx, void* blob) {
+  if (ctx->ep == 1) return FSC_OK;
+  memcpy(blob, &ctx->peer->my_handle, sizeof(cudaIpcMemHandle_t));
+  return FSC_OK;
+}
+
+int fsc_transport_import(fsc_ctx* ctx, const void* blobs) {
+  if (ctx->ep == 1) return FSC_OK;
+  fsc_peer_state* st = ctx->peer;
+  TCK(cudaSetDevice(ctx->device));
+  for (int p = 0; p < ctx->ep; ++p) {
+    if (p == ctx->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const char*>(blobs) + p * sizeof(cudaIpcMemHandle_t), sizeof(h));
+    void* ptr = nullptr;
+    TCK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    st->peers.base[p] = static_cast<char*>(ptr);
+    st->opened[p] = true;
+  }
+  return FSC_OK;
+}
+
+void fsc_transport_finalize(fsc_ctx* ctx) {
+  fsc_peer_state* st = ctx->peer;
+  if (!st) return;
+  for (int p = 0; p < kMaxP; ++p)
+    if (st->opened[p]) cudaIpcCloseMemHandle(st->peers.base[p]);
+  if (st->local) cudaFree(st->local);
+  if (st->send_base) cudaFree(st->send_base);
+  if (st->ticket) cudaFree(st->ticket);
+  if (ctx->recv_counts) cudaFree(ctx->recv_counts);
+  delete st;
+  ctx->peer = nullptr;
+}
+
+static bool connected(fsc_ctx* ctx) {
+  for (int p = 0; p < ctx->ep; ++p)
+    if (!ctx->peer->peers.base[p]) return false;
+  return true;
+}
+
+// counts exchange + permute-and-dispatch on stream s (the caller picks compute or comm stream)
+int fsc_transport_dispatch(fsc_ctx* ctx, int T, cudaStream_t s) {
+  fsc_peer_state* st = ctx->peer;
+  if (!connected(ctx)) {
+    fsc_set_error(ctx, "EP transport not bootstrapped (fsc_bootstrap_export/import)");
+    return FSC_ERR_STATE;
+  }
+  const fsc_moe_config& c = ctx->cfg;
+  st->epoch += 1;
+  const int E = c.n_experts, P = ctx->ep;
+  ++g_launches;
+  ep_counts_kernel<<<1, 256, 0, s>>>(st->peers, ctx->rank, P, E, ctx->e_loc, st->epoch, st->lay.cnt, ctx->counts,
+                                     st->send_base, ctx->recv_counts);
+  TCK(cudaGetLastError());
+  const int R = T * c.top_k;
+  int blocks = (R + 7) / 8;
+  if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
+  if (blocks < 1) blocks = 1;
+  ++g_launches;
+  ep_dispatch_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, P, R, c.d, E, ctx->e_loc, st->epoch, st->lay.xr,
+                                            st->lay.ret, reinterpret_cast<const uint4*>(ctx->xn), ctx->src_row,
+                                            ctx->offsets, st->send_base, st->ticket);
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+int fsc_transport_dispatch_wait(fsc_ctx* ctx, cudaStream_t s) {
+  ++g_launches;
+  ep_wait_kernel<<<1, 32, 0, s>>>(ctx->peer->local, FLAG_DISP, ctx->ep, ctx->peer->epoch);
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+// the combine payload itself is written by the GEMM2 epilogue (fsc_transport_scatter_target);
+// this raises the per-source completion flags once that GEMM is done.
+int fsc_transport_combine(fsc_ctx* ctx, int, cudaStream_t s) {
+  ++g_launches;
+  ep_signal_kernel<<<1, 32, 0, s>>>(ctx->peer->peers, ctx->rank, ctx->ep, FLAG_COMB, ctx->peer->epoch);
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+int fsc_transport_combine_wait(fsc_ctx* ctx, cudaStream_t s) {
+  ++g_launches;
+  ep_wait_kernel<<<1, 32, 0, s>>>(ctx->peer->local, FLAG_COMB, ctx->ep, ctx->peer->epoch);
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+// scatter map + per-rank destination pointers for the fused GEMM2 -> combine epilogue
+void fsc_transport_scatter_target(fsc_ctx* ctx, const int** ret, void** peer_out) {
+  fsc_peer_state* st = ctx->peer;
+  *ret = reinterpret_cast<const int*>(st->local + st->lay.ret);
+  for (int p = 0; p < kMaxP; ++p)
+    peer_out[p] = (p < ctx->ep && st->peers.base[p]) ? st->peers.base[p] + st->lay.ys : nullptr;
+}
