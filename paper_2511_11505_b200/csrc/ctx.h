@@ -60,6 +60,14 @@ struct fsc_ctx {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
 
   int pending = 0;
+  int no_overlap = 0;          // FarSkip call made under the BLOCKING stack schedule
+
+  // layer-stack workspace (stack.cu), allocated on first use
+  uint16_t* hn = nullptr;      // bf16 [T, d]           normalised attention input
+  uint16_t* qkv = nullptr;     // bf16 [T, (Hq+2Hkv)hd]
+  uint16_t* ao = nullptr;      // bf16 [T, Hq hd]       attention core output
+  float* rbuf[3] = {nullptr, nullptr, nullptr};  // fp32 [T, d] rotating residual buffers
+  long stack_cap_qkv = 0, stack_cap_ao = 0;
   int timing = 0;
   cudaEvent_t ph_ev[PH_N][2] = {};
   int ph_used[PH_N] = {};

@@ -145,7 +145,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -388,7 +388,7 @@ extern "C" int fsc_moe_forward_farskip(fsc_ctx* ctx, const fsc_moe_weights* w, i
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
-  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, cb, user, true);
+  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, cb, user, !ctx->no_overlap);
   if (rc) return rc;
   if (cb) cb(user, 1, s);  // combine in flight
   // P:198 step 8 and C-amb-12: attn-in_{k+1} = (mlp-in_k + attn-out_k) + shared-out_k

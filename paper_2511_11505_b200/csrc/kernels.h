@@ -93,6 +93,14 @@ cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t
 cudaError_t launch_unpermute(const uint16_t* y, const int* pos, const float* w, const float* resid,
                              float* out, int T, int k, int d, cudaStream_t s);
 
+// attention filler (attention.cu)
+cudaError_t launch_rmsnorm_bf16(const float* x, const float* gamma, uint16_t* y, int T, int d, float eps,
+                                cudaStream_t s);
+cudaError_t launch_rope(uint16_t* qkv, int T, int n_heads, int n_kv_heads, int hd, int seq_len, float theta,
+                        cudaStream_t s);
+cudaError_t launch_flash_attn(const uint16_t* qkv, uint16_t* out, int T, int Hq, int Hkv, int hd, int seq_len,
+                              cudaStream_t s);
+
 // elementwise helpers
 cudaError_t launch_copy_f32(const float* src, float* dst, long n, cudaStream_t s);
 

@@ -71,7 +71,14 @@ def test_sass_is_blackwell_native(lib):
     elf = subprocess.run([cuobjdump, "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in elf
     sass = subprocess.run([cuobjdump, "-sass", so], capture_output=True, text=True).stdout
-    assert "UTCHMMA" in sass or "UTCMMA" in sass, "tcgen05.mma missing"
-    assert "UTMALDG" in sass, "TMA load missing"
-    assert "LDTM" in sass, "tcgen05.ld missing"
-    assert " HMMA" not in sass, "legacy mma.sync path present"
+    # split per function; the grouped GEMM (every expert / shared / projection GEMM)
+    # must be tcgen05 + TMA, with no legacy mma.sync
+    funcs = re.split(r"\n\s*Function : ", sass)
+    gemm = [f for f in funcs if f.startswith("_ZN3fsc19grouped_gemm_kernel")]
+    assert len(gemm) >= 16, len(gemm)
+    for f in gemm:
+        name = f.split()[0]
+        assert "UTCHMMA" in f or "UTCMMA" in f, f"tcgen05.mma missing in {name}"
+        assert "UTMALDG" in f, f"TMA load missing in {name}"
+        assert "LDTM" in f, f"tcgen05.ld missing in {name}"
+        assert not re.search(r"\bHMMA\b", f), f"legacy mma.sync in {name}"
