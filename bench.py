@@ -155,15 +155,20 @@ def run_gpu(args):
 
     shape = synth.CONFIGS[args.config]
     T = shape.tokens
-    ep = 1  # EP transport (peer memory) lands next; N>1 runs EP=1 replicas, no data-path collective
+    # EP = N when the experts shard evenly (C-amb-9), else independent EP=1 replicas
+    ep = world if (world > 1 and shape.n_experts % world == 0) else 1
+    e_loc = shape.n_experts // ep
+    erank = rank if ep > 1 else 0
     dev = torch.device("cuda", local)
-    w = synth.moe_weights(shape, seed=args.seed)
+    w = synth.moe_weights(shape, seed=args.seed, e0=erank * e_loc, e_loc=e_loc)
     wd = moe_weights_dev(w, dev)
     del w
     x = torch.from_numpy(synth.tokens(shape, seed=args.seed, rank=rank)).to(dev)
     out = torch.empty_like(x)
     ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
-                  shared_ffn=shape.shared_ffn, max_tokens=T, device=local)
+                  shared_ffn=shape.shared_ffn, max_tokens=T, rank=erank, ep_size=ep, device=local)
+    if ep > 1:
+        ctx.connect()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -230,6 +235,11 @@ def run_gpu(args):
         e2e_s = float(t.item())
     e2e_value = T * world * e2e_steps / e2e_s
 
+    stack = None
+    if args.stack_layers > 0:
+        stack = stack_measure(ctx, shape, wd, x, args.stack_layers, max(3, min(args.steps, 8)), world, dev,
+                              rank, args.seed)
+
     if rank != 0:
         ctx.close()
         if world > 1:
@@ -239,7 +249,7 @@ def run_gpu(args):
     peaks, src = load_peaks()
     # dominant kernel: routed-expert GEMM1 with the fused SwiGLU epilogue (row a7)
     R = T * shape.top_k
-    g1_flop = 2.0 * R * shape.d * 2 * shape.ffn
+    g1_flop = 2.0 * R * shape.d * 2 * shape.ffn  # balanced routing: rows received per rank = T*k
     g1_ms = phase_ms.get("gemm1")
     achieved = g1_flop / (g1_ms * 1e-3) / 1e12 if g1_ms else None
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
@@ -251,7 +261,8 @@ def run_gpu(args):
         except Exception:
             traffic = None
     exp_flop = 2.0 * R * shape.d * 3 * shape.ffn + 2.0 * T * shape.d * 3 * shape.shared_ffn
-    layer_roof_ms = exp_flop / (peaks["bf16_tflops"] * 1e12) * 1e3
+    a2a_bytes = 2.0 * 2 * R * shape.d * (ep - 1) / ep          # dispatch + combine bytes leaving a rank
+    layer_roof_ms = max(exp_flop / (peaks["bf16_tflops"] * 1e12), a2a_bytes / 770e9) * 1e3
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -264,10 +275,13 @@ def run_gpu(args):
                      "algorithmic_flop_per_launch": g1_flop,
                      "frac_of_burst_peak": (achieved / peaks["bf16_tflops"]) if achieved else None},
         "layer_roofline": {"expert_flop": exp_flop, "t_roof_ms": layer_roof_ms,
-                           "frac": layer_roof_ms / ms_per_step, "note": "max(expert FLOPs / bf16 burst peak, "
-                                                                        "a2a bytes / NVLink); a2a = 0 at EP=1"},
+                           "a2a_bytes": a2a_bytes, "frac": layer_roof_ms / ms_per_step,
+                           "note": "max(expert FLOPs / bf16 burst peak, a2a bytes / 770 GB/s measured NVLink "
+                                   "peer bandwidth); a2a = 0 at EP=1"},
         "phase_ms": phase_ms,
-        "exposed_a2a_us_per_layer": {"farskip": None, "blocking": None, "note": "EP=1: no all-to-all"},
+        "exposed_a2a_us_per_layer": (stack or {}).get("exposed_a2a_us_per_layer",
+                                                       {"farskip": None, "blocking": None}),
+        "stack": stack,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": T * shape.d * 4 * world,
                 "d2h_bytes_per_step": T * shape.d * 4 * world,
                 "note": "fsc_moe_forward_blocking_host: pinned host x -> device -> forward -> host out, synced"},
@@ -284,6 +298,65 @@ def run_gpu(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- stack (FarSkip vs blocking)
+def stack_measure(ctx, shape, wd, x, L, steps, world, dev, rank, seed):
+    """L-layer Hybrid (FarSkip-wired) stack with the attention filler, timed in the
+    BLOCKING and OVERLAPPED schedules (same kernels, same numbers). Exposed
+    all-to-all per layer = compute-stream time spent in communication:
+    blocking: dispatch (counts exchange + dispatch copy + wait) + combine wait;
+    FarSkip: dispatch stall of the compute stream + combine wait. The MoE weights
+    of layer 0 are reused for every layer (timing only)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_11505_b200 import FSC_BLOCKING, FSC_HYBRID, FSC_OVERLAPPED
+    from tests.gpu_util import attn_weights_dev
+    aw = attn_weights_dev(synth.attn_weights(shape, seed=seed), dev)
+    o0 = x
+    oL = torch.empty_like(x)
+    res = {}
+    stream = torch.cuda.current_stream(dev)
+    for name, sched in (("blocking", FSC_BLOCKING), ("farskip", FSC_OVERLAPPED)):
+        def run():
+            ctx.layer_stack_forward([aw] * L, [wd] * L, shape.tokens, shape.seq_len, [FSC_HYBRID] * L, sched, o0, oL,
+                                    stream=stream.cuda_stream)
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            run()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        t = a.elapsed_time(b) / steps
+        ctx.set_timing(True)
+        for _ in range(steps):
+            run()
+        log = ctx.timing_log(4096)
+        ctx.set_timing(False)
+        comm = {"dispatch": 0.0, "dispatch_stall": 0.0, "combine_wait": 0.0}
+        for ph, ms in log:
+            if ph in comm:
+                comm[ph] += ms
+        exposed = (comm["dispatch"] if name == "blocking" else comm["dispatch_stall"]) + comm["combine_wait"]
+        vals = torch.tensor([t, exposed / steps / L], device=dev)
+        if world > 1:
+            dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        res[name] = {"ms_per_stack": float(vals[0]), "ms_per_layer": float(vals[0]) / L,
+                     "exposed_comm_us_per_layer": float(vals[1]) * 1e3,
+                     "phase_ms_per_layer": {k: v / steps / L for k, v in comm.items()}}
+    blk, fs = res["blocking"]["exposed_comm_us_per_layer"], res["farskip"]["exposed_comm_us_per_layer"]
+    return {"layers": L, "modes": "hybrid", "attention": f"GQA {shape.n_heads}/{shape.n_kv_heads}x{shape.head_dim},"
+                                                         f" seq {shape.seq_len}",
+            "blocking": res["blocking"], "farskip": res["farskip"],
+            "speedup_farskip_vs_blocking": res["blocking"]["ms_per_stack"] / res["farskip"]["ms_per_stack"],
+            "exposed_a2a_us_per_layer": {"farskip": fs, "blocking": blk,
+                                         "farskip_frac_of_blocking": (fs / blk) if blk > 0 else None}}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -334,6 +407,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stack-layers", type=int, default=4, help="0 disables the FarSkip-vs-blocking stack timing")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -147,9 +147,14 @@ FSC_API int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg);
  * events are recorded on the call's stream around every phase; fsc_get_timings
  * waits for the last call's events and writes n <= 9 durations in ms (-1 = phase
  * not run) in the order: router, perm_maps, dispatch (permute), gemm1 (SwiGLU),
- * gemm2 (down), combine, shared1, shared2, unpermute. Returns the phase count. */
+ * gemm2 (down), combine, shared1, shared2, unpermute, dispatch_stall, combine_wait.
+ * Returns the phase count. */
 FSC_API int fsc_set_timing(fsc_ctx* ctx, int enable);
 FSC_API int fsc_get_timings(fsc_ctx* ctx, float* ms, int n);
+/* Every timed phase instance since fsc_set_timing (phase ids as above, then
+ * 9 = dispatch stall of the compute stream, 10 = combine wait); waits for the
+ * events, writes up to cap (phase, ms) pairs, returns the count and clears the log. */
+FSC_API int fsc_timing_log(fsc_ctx* ctx, int* phase, float* ms, int cap);
 /* Cumulative number of CUDA kernels launched by libfsc in this process. */
 FSC_API long fsc_launch_count(void);
 

@@ -70,6 +70,7 @@ _SIGS = {
     "fsc_set_timing": (_I, [_P, _I]),
     "fsc_get_timings": (_I, [_P, ctypes.POINTER(ctypes.c_float), _I]),
     "fsc_launch_count": (ctypes.c_long, []),
+    "fsc_timing_log": (_I, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_float), _I]),
     "fsc_moe_forward_blocking": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, ctypes.POINTER(MoeDebugC), _P]),
     "fsc_moe_forward_blocking_host": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, _P]),
     "fsc_moe_forward_farskip": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, OVERLAP_CB, _P,
@@ -198,7 +199,8 @@ class Context:
         buf = ctypes.create_string_buffer(data, max(len(data), 1))
         self._ck(self.lib.fsc_bootstrap_import(self.h, buf))
 
-    PHASES = ("router", "perm_maps", "dispatch", "gemm1", "gemm2", "combine", "shared1", "shared2", "unpermute")
+    PHASES = ("router", "perm_maps", "dispatch", "gemm1", "gemm2", "combine", "shared1", "shared2", "unpermute",
+              "dispatch_stall", "combine_wait")
 
     def set_timing(self, enable: bool):
         self._ck(self.lib.fsc_set_timing(self.h, int(enable)))
@@ -210,6 +212,15 @@ class Context:
         if rc < 0:
             self._ck(rc)
         return {n: buf[i] for i, n in enumerate(self.PHASES) if buf[i] >= 0}
+
+    def timing_log(self, cap: int = 1024):
+        """[(phase_name, ms)] for every timed phase instance since set_timing(True)."""
+        ph = (ctypes.c_int * cap)()
+        ms = (ctypes.c_float * cap)()
+        n = self.lib.fsc_timing_log(self.h, ph, ms, cap)
+        if n < 0:
+            self._ck(n)
+        return [(self.PHASES[ph[i]], ms[i]) for i in range(n)]
 
     def launch_count(self) -> int:
         return int(self.lib.fsc_launch_count())

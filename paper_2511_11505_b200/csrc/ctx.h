@@ -15,7 +15,9 @@ struct fsc_handle_s {
 struct fsc_peer_state;  // transport.cu
 
 // phases timed with CUDA events when timing is enabled (fsc_get_timings order)
-enum { PH_ROUTER = 0, PH_PERM, PH_DISPATCH, PH_GEMM1, PH_GEMM2, PH_COMBINE, PH_SHARED1, PH_SHARED2, PH_UNPERMUTE, PH_N };
+enum { PH_ROUTER = 0, PH_PERM, PH_DISPATCH, PH_GEMM1, PH_GEMM2, PH_COMBINE, PH_SHARED1, PH_SHARED2, PH_UNPERMUTE,
+       PH_DISPATCH_STALL, PH_COMBINE_WAIT, PH_N };
+constexpr int kLogEvents = 2048;
 
 struct fsc_ctx {
   int rank = 0, ep = 1, device = 0;
@@ -71,6 +73,10 @@ struct fsc_ctx {
   int timing = 0;
   cudaEvent_t ph_ev[PH_N][2] = {};
   int ph_used[PH_N] = {};
+  // timing log: every phase instance since the last reset (bench: per-layer exposure)
+  cudaEvent_t log_ev[kLogEvents] = {};
+  int log_phase[kLogEvents / 2] = {};
+  int log_n = 0;
   fsc_handle_s handle{};
 };
 

@@ -45,12 +45,19 @@ namespace fsc {
 long g_launches = 0;
 }
 
-#define PH_BEGIN_ON(i, st) \
-  if (ctx->timing) CK(cudaEventRecord(ctx->ph_ev[i][0], st))
-#define PH_END_ON(i, st)                           \
-  if (ctx->timing) {                               \
-    CK(cudaEventRecord(ctx->ph_ev[i][1], st));     \
-    ctx->ph_used[i] = 1;                           \
+#define PH_BEGIN_ON(i, st)                                                         \
+  if (ctx->timing) {                                                               \
+    CK(cudaEventRecord(ctx->ph_ev[i][0], st));                                     \
+    if (ctx->log_n < kLogEvents / 2) CK(cudaEventRecord(ctx->log_ev[2 * ctx->log_n], st)); \
+  }
+#define PH_END_ON(i, st)                                                           \
+  if (ctx->timing) {                                                               \
+    CK(cudaEventRecord(ctx->ph_ev[i][1], st));                                     \
+    ctx->ph_used[i] = 1;                                                           \
+    if (ctx->log_n < kLogEvents / 2) {                                             \
+      CK(cudaEventRecord(ctx->log_ev[2 * ctx->log_n + 1], st));                    \
+      ctx->log_phase[ctx->log_n++] = i;                                            \
+    }                                                                              \
   }
 #define PH_BEGIN(i) PH_BEGIN_ON(i, s)
 #define PH_END(i) PH_END_ON(i, s)
@@ -154,6 +161,8 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   for (int i = 0; i < PH_N; ++i)
     for (int j = 0; j < 2; ++j)
       if (ctx->ph_ev[i][j]) cudaEventDestroy(ctx->ph_ev[i][j]);
+  for (int i = 0; i < kLogEvents; ++i)
+    if (ctx->log_ev[i]) cudaEventDestroy(ctx->log_ev[i]);
   delete ctx;
   return FSC_OK;
 }
@@ -163,10 +172,13 @@ extern "C" const char* fsc_last_error(const fsc_ctx* ctx) { return ctx ? ctx->er
 extern "C" int fsc_set_timing(fsc_ctx* ctx, int enable) {
   if (!ctx) return FSC_ERR_SHAPE;
   CK(cudaSetDevice(ctx->device));
-  if (enable && !ctx->ph_ev[0][0])
+  if (enable && !ctx->ph_ev[0][0]) {
     for (int i = 0; i < PH_N; ++i)
       for (int j = 0; j < 2; ++j) CK(cudaEventCreate(&ctx->ph_ev[i][j]));
+    for (int i = 0; i < kLogEvents; ++i) CK(cudaEventCreate(&ctx->log_ev[i]));
+  }
   ctx->timing = enable ? 1 : 0;
+  ctx->log_n = 0;
   return FSC_OK;
 }
 
@@ -183,6 +195,18 @@ extern "C" int fsc_get_timings(fsc_ctx* ctx, float* ms, int n) {
 }
 
 extern "C" long fsc_launch_count(void) { return fsc::g_launches; }
+
+extern "C" int fsc_timing_log(fsc_ctx* ctx, int* phase, float* ms, int cap) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  const int n = ctx->log_n < cap ? ctx->log_n : cap;
+  for (int i = 0; i < n; ++i) {
+    CK(cudaEventSynchronize(ctx->log_ev[2 * i + 1]));
+    if (phase) phase[i] = ctx->log_phase[i];
+    if (ms) CK(cudaEventElapsedTime(&ms[i], ctx->log_ev[2 * i], ctx->log_ev[2 * i + 1]));
+  }
+  ctx->log_n = 0;
+  return n;
+}
 
 extern "C" int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg) {
   if (!ctx) return FSC_ERR_SHAPE;
@@ -267,7 +291,11 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     recv_counts = ctx->recv_counts;
   }
   if (cb) cb(user, 0, s);  // P:198 step 5: attention part (b) while dispatch is in flight
-  if (ctx->ep > 1 && overlap) CK(cudaStreamWaitEvent(s, ctx->ev_b, 0));  // step 6: sync Dispatch
+  if (ctx->ep > 1 && overlap) {  // step 6: sync Dispatch (the compute stream stalls only if it is late)
+    PH_BEGIN(PH_DISPATCH_STALL);
+    CK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
+    PH_END(PH_DISPATCH_STALL);
+  }
   // Routed experts (P:198 step 6): GEMM1 + SwiGLU, GEMM2 (+ fused Combine for EP > 1)
   GemmLaunch g1{};
   g1.A = recv; g1.a_rows = recv_rows; g1.B0 = w->w1; g1.B1 = w->w2; g1.b_rows = (long)ctx->e_loc * c.ffn;
@@ -331,8 +359,10 @@ static int moe_finish(fsc_ctx* ctx, int T, const float* resid, float* out, const
   const fsc_moe_config& c = ctx->cfg;
   const uint16_t* ysrc = ctx->y;
   if (ctx->ep > 1) {
+    PH_BEGIN(PH_COMBINE_WAIT);
     int rc = fsc_transport_combine_wait(ctx, s);
     if (rc) return rc;
+    PH_END(PH_COMBINE_WAIT);
     ysrc = ctx->ys;
   }
   PH_BEGIN(PH_UNPERMUTE);

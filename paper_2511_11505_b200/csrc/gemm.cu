@@ -238,11 +238,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], aphase);
-      tc_fence_after();
       const int rr = r + (int)rank * BM;          // row inside the pair tile
       const bool valid = rr < ti.rows;
       const long grow = (long)ti.row0 + rr;
+      if (EPI != EPI_RESID_F32) {
+        mbar_wait(&tfull[acc], aphase);
+        tc_fence_after();
+      }
       const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (EPI == EPI_SWIGLU) {
         __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + ti.nb * C::HALF;
@@ -290,16 +292,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo + ti.nb * BN;
-        const float* res = p.resid ? p.resid + grow * p.ldr + ti.nb * BN : nullptr;
+        const float* res = (p.resid && valid) ? p.resid + grow * p.ldr + ti.nb * BN : nullptr;
+        const int c_beg = half * (BN / 2), c_end = (half + 1) * (BN / 2);
+        float4 pre[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pre[i] = res ? *reinterpret_cast<const float4*>(res + c_beg + 4 * i)
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        mbar_wait(&tfull[acc], aphase);   // first residual chunk loads overlap the MMA tail
+        tc_fence_after();
 #pragma unroll 1
-        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+        for (int c = c_beg; c < c_end; c += 32) {
           uint32_t v[32];
           tmem_ld32(tb + c, v);
+          float4 cur[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) cur[i] = pre[i];
+          if (res && c + 32 < c_end) {   // residual of the next chunk in flight while this one drains
+#pragma unroll
+            for (int i = 0; i < 8; ++i) pre[i] = *reinterpret_cast<const float4*>(res + c + 32 + 4 * i);
+          }
           tmem_ld_wait();
           if (valid) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              float4 a = res ? *reinterpret_cast<const float4*>(res + c + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+              float4 a = cur[i];
               a.x += __uint_as_float(v[4 * i]);
               a.y += __uint_as_float(v[4 * i + 1]);
               a.z += __uint_as_float(v[4 * i + 2]);
