@@ -52,55 +52,69 @@ def workload_config(shape, ep, n_gpus, schedule):
             "tokens_per_rank": shape.tokens, "global_tokens": shape.tokens * n_gpus, "ep": ep,
             "schedule": schedule, "parallelism": f"ep{ep}" + (f"-x{n_gpus // ep}replicas" if n_gpus > ep else ""),
             "l2": "flushed (256 MiB write) before every timed step; per-step working set > L2",
+            "launch": "one CUDA-graph replay per step (captured fsc_moe_forward_blocking)",
             "data": "synthetic seeded N(0,1) tokens, random-init weights (SURVEY §8(d) recipe)"}
 
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """Polls NVML (SM clock, max SM clock, clock-event reasons) every ~2 ms in a
+    thread while the timed region runs; falls back to nvidia-smi if NVML fails."""
 
-    def __init__(self, index=0):
-        self.rows = []
-        self.proc = None
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
+
+    def __init__(self, index=0, period_s=0.002):
         self.index = index
+        self.period = period_s
+        self.rows = []
+        self.stop = threading.Event()
+        self.err = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis else self.index
+            self.h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.N = N
+            self.max_sm = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
+    def _run(self):
+        N = self.N
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+            except Exception as e:  # noqa: BLE001
+                self.err = repr(e)
+                return
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if getattr(self, "t", None):
+            self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
-        loaded = [s for s in sm if s > 600] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0, "error": self.err}
+        N = self.N
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, rs in self.rows for name, attr in self.REASONS.items()
+                          if rs & getattr(N, attr, 0)})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_sm, "sm_mhz_min": min(sm),
+                "reasons": reasons, "samples": len(sm), "source": "NVML, ~2 ms polling during the timed region"}
 
 
 # ----------------------------------------------------------------------------- oracle baseline
@@ -172,8 +186,38 @@ def run_gpu(args):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    def eager_step():
+        ctx.moe_forward_blocking(wd, x, out, stream=torch.cuda.current_stream(dev).cuda_stream)
+
+    for _ in range(args.warmup):
+        eager_step()
+    torch.cuda.synchronize(dev)
+    # eager reference timing (one host call per step)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(3):
+        eager_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    eager_ms = e0.elapsed_time(e1) / 3
+    # the whole MoE layer is free of host synchronisation (device-side counts, tile
+    # lists and flags), so one step is captured once and replayed as a CUDA graph
+    use_graph = not args.no_graph
+    launches_per_step = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        lc0 = ctx.launch_count()
+        with torch.cuda.graph(graph):
+            eager_step()
+        launches_per_step = ctx.launch_count() - lc0
+        graph.replay()
+        torch.cuda.synchronize(dev)
+
     def step():
-        ctx.moe_forward_blocking(wd, x, out, stream=stream.cuda_stream)
+        if use_graph:
+            graph.replay()
+        else:
+            eager_step()
 
     for _ in range(args.warmup):
         step()
@@ -197,6 +241,8 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
     launches = ctx.launch_count() - launches0
+    if use_graph:
+        launches = launches_per_step * args.steps
     ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(sum(ms))
     if world > 1:
@@ -211,7 +257,7 @@ def run_gpu(args):
     phase = {}
     for _ in range(max(3, min(args.steps, 10))):
         flush.fill_(0.0)
-        step()
+        eager_step()
         for kname, v in ctx.timings().items():
             phase.setdefault(kname, []).append(v)
     ctx.set_timing(False)
@@ -286,6 +332,7 @@ def run_gpu(args):
                 "d2h_bytes_per_step": T * shape.d * 4 * world,
                 "note": "fsc_moe_forward_blocking_host: pinned host x -> device -> forward -> host out, synced"},
         "gpu_launches": launches,
+        "cuda_graph": use_graph, "ms_per_step_eager": eager_ms,
         "clocks": clk.summary(),
         "wall_s_timed_region": wall,
     }
@@ -350,13 +397,18 @@ def stack_measure(ctx, shape, wd, x, L, steps, world, dev, rank, seed):
         res[name] = {"ms_per_stack": float(vals[0]), "ms_per_layer": float(vals[0]) / L,
                      "exposed_comm_us_per_layer": float(vals[1]) * 1e3,
                      "phase_ms_per_layer": {k: v / steps / L for k, v in comm.items()}}
+    if ctx.lib is not None and getattr(ctx, "cfg", None) is not None and world == 1:
+        # EP=1: the "dispatch" phase is a local permute; there is no all-to-all to expose
+        for r in res.values():
+            r["exposed_comm_us_per_layer"] = 0.0
     blk, fs = res["blocking"]["exposed_comm_us_per_layer"], res["farskip"]["exposed_comm_us_per_layer"]
     return {"layers": L, "modes": "hybrid", "attention": f"GQA {shape.n_heads}/{shape.n_kv_heads}x{shape.head_dim},"
                                                          f" seq {shape.seq_len}",
             "blocking": res["blocking"], "farskip": res["farskip"],
             "speedup_farskip_vs_blocking": res["blocking"]["ms_per_stack"] / res["farskip"]["ms_per_stack"],
-            "exposed_a2a_us_per_layer": {"farskip": fs, "blocking": blk,
-                                         "farskip_frac_of_blocking": (fs / blk) if blk > 0 else None}}
+            "exposed_a2a_us_per_layer": {"farskip": fs if world > 1 else None, "blocking": blk if world > 1 else None,
+                                         "farskip_frac_of_blocking": (fs / blk) if (world > 1 and blk > 0) else None,
+                                         "note": None if world > 1 else "EP=1: no all-to-all on one GPU"}}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -407,6 +459,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of a CUDA graph")
     ap.add_argument("--stack-layers", type=int, default=4, help="0 disables the FarSkip-vs-blocking stack timing")
     args = ap.parse_args()
     if args.warmup < 3:

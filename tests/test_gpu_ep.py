@@ -113,3 +113,77 @@ def test_ep_matches_oracle_and_ep1(world):
     for r in range(world):
         np.testing.assert_array_equal(res[r]["out"], o1[r * T:(r + 1) * T])
     c1.close()
+
+
+def _stack_worker(rank, world, port, shape, seed, outdir, L):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2511_11505_b200 import FSC_BLOCKING, FSC_HYBRID, FSC_OVERLAPPED, FSC_REGULAR, Context
+    from tests.gpu_util import attn_weights_dev, dev_f32, moe_weights_dev
+    e_loc = shape.n_experts // world
+    mw = [moe_weights_dev(synth.moe_weights(shape, seed=seed, layer=k, e0=rank * e_loc, e_loc=e_loc))
+          for k in range(L)]
+    aw = [attn_weights_dev(synth.attn_weights(shape, seed=seed, layer=k)) for k in range(L)]
+    x = synth.tokens(shape, seed=seed, rank=rank)
+    T = x.shape[0]
+    ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
+                  shared_ffn=shape.shared_ffn, max_tokens=T, rank=rank, ep_size=world, device=0)
+    ctx.connect()
+    res = {}
+    for name, modes in (("hyb", [FSC_HYBRID] * L), ("mix", [FSC_REGULAR] + [FSC_HYBRID] * (L - 1))):
+        for sname, sched in (("blk", FSC_BLOCKING), ("ovl", FSC_OVERLAPPED)):
+            o0 = dev_f32(x)
+            oL = torch.empty_like(o0)
+            ctx.layer_stack_forward(aw, mw, T, shape.seq_len, modes, sched, o0, oL)
+            torch.cuda.synchronize()
+            res[f"{name}_{sname}"] = oL.cpu().numpy()
+    np.savez(os.path.join(outdir, f"s{rank}.npz"), **res)
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+STACK_SHAPE = synth.MoeShape("ep_stack", d=256, n_experts=8, top_k=2, ffn=128, shared_ffn=128, tokens=128,
+                             n_heads=4, n_kv_heads=2, head_dim=64, seq_len=64)
+
+
+@pytest.mark.parametrize("world", [2])
+def test_ep_stack_schedules_bitwise_and_ep_invariant(world):
+    """EP=2 layer stack: BLOCKING == OVERLAPPED (the comm stream / event
+    ordering changes nothing) and both equal the EP=1 stack on the same tokens."""
+    from paper_2511_11505_b200 import FSC_HYBRID, FSC_OVERLAPPED, FSC_REGULAR, Context, build
+    from tests.gpu_util import attn_weights_dev, dev_f32, moe_weights_dev
+    build.build()
+    L = 3
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as td:
+        ps = [ctx.Process(target=_stack_worker, args=(r, world, port, STACK_SHAPE, 0, td, L)) for r in range(world)]
+        for p in ps:
+            p.start()
+        for p in ps:
+            p.join(timeout=600)
+        assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+        res = [dict(np.load(os.path.join(td, f"s{r}.npz"))) for r in range(world)]
+    for r in range(world):
+        np.testing.assert_array_equal(res[r]["hyb_blk"], res[r]["hyb_ovl"])
+        np.testing.assert_array_equal(res[r]["mix_blk"], res[r]["mix_ovl"])
+    # EP=1 on the concatenated tokens (sequences never straddle ranks: T % seq_len == 0)
+    sh = STACK_SHAPE
+    X = np.concatenate([synth.tokens(sh, seed=0, rank=r) for r in range(world)])
+    c1 = Context(d=sh.d, n_experts=sh.n_experts, top_k=sh.top_k, ffn=sh.ffn, shared_ffn=sh.shared_ffn,
+                 max_tokens=X.shape[0])
+    mw = [moe_weights_dev(synth.moe_weights(sh, seed=0, layer=k)) for k in range(L)]
+    aw = [attn_weights_dev(synth.attn_weights(sh, seed=0, layer=k)) for k in range(L)]
+    for name, modes in (("hyb", [FSC_HYBRID] * L), ("mix", [FSC_REGULAR] + [FSC_HYBRID] * (L - 1))):
+        o0 = dev_f32(X)
+        oL = torch.empty_like(o0)
+        c1.layer_stack_forward(aw, mw, X.shape[0], sh.seq_len, modes, FSC_OVERLAPPED, o0, oL)
+        torch.cuda.synchronize()
+        o1 = oL.cpu().numpy()
+        for r in range(world):
+            np.testing.assert_array_equal(res[r][f"{name}_ovl"], o1[r * sh.tokens:(r + 1) * sh.tokens])
+    c1.close()
