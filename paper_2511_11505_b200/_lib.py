@@ -12,7 +12,7 @@ import os
 from typing import Optional, Sequence
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfsc.so")
+LIB_PATH = os.environ.get("FSC_LIB", os.path.join(HERE, "libfsc.so"))
 
 FSC_OK, FSC_ERR_CONFIG, FSC_ERR_SHAPE, FSC_ERR_CUDA, FSC_ERR_COMM, FSC_ERR_NONFINITE, FSC_ERR_STATE = 0, -1, -2, -3, -4, -5, -6
 FSC_REGULAR, FSC_HYBRID = 0, 1

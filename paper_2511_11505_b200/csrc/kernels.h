@@ -66,6 +66,8 @@ struct RouterLaunch {
   int* rf_list;          // workspace [T]: tokens flagged for fp64 refinement
   int* rf_ctrl;          // workspace [2]: {count, done-ticket}, zero between calls
   double* rf_l64;        // workspace [T, E]: fp64 logits of flagged tokens
+  float* w_scaled;       // workspace [E, d]: gamma * W_R
+  float* w_sq;           // workspace [E]: ||gamma * W_R[e]||^2
 };
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s);
 

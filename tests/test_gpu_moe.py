@@ -165,3 +165,50 @@ def test_full_size_sampled_parity(name):
     np.testing.assert_array_equal(dbg["pos"], m.pos)
     print(f"{name}: refined={int(dbg['n_refined'][0])} excluded={int(excl.sum())}")
     ctx.close()
+
+
+def _layer_f32(w, top_k):
+    """EpLayer holding exact fp32 widenings of the bf16 weights (the oracle widens
+    each expert to fp64 when it uses it) - keeps Scout-sized layers in memory."""
+    f = lambda b: None if b is None else synth.bf16_bits_to_f32(b)  # noqa: E731
+    return om.EpLayer(w.gamma.astype(np.float64), w.w_router.astype(np.float64), f(w.w1), f(w.w2), f(w.w3),
+                      f(w.ws1), f(w.ws2), f(w.ws3), top_k)
+
+
+def test_scout_full_size_sampled_parity():
+    """Llama-4-Scout-shaped layer (d=5120, 16 experts top-1, FFN 8192 + shared 8192)
+    at the full 8192 tokens; 16 sampled tokens recomputed by the oracle."""
+    shape = synth.CONFIGS["scout"]
+    T = shape.tokens
+    ctx = make_ctx(shape, T)
+    w = synth.moe_weights(shape, seed=0)
+    x = synth.tokens(shape, seed=0, T=T)
+    out, dbg = run_blocking(ctx, moe_weights_dev(w), x)
+    ctx.close()
+    lay = _layer_f32(w, shape.top_k)
+    del w
+    assert dbg["counts"].sum() == T
+    sample = np.array([0, 1, 777, 4095, 4096, 6000, 8190, 8191] + list(range(100, 108)))
+    r, excl = om.adopt_router(lay, x[sample], dbg["topk_idx"][sample])
+    np.testing.assert_array_equal(dbg["topk_idx"][sample], r.idx)
+    assert np.all(dbg["topk_w"][sample] == 1.0)          # top-1: the renormalised gate is exactly 1
+    sh, ro, _ = om.moe_block(x[sample], lay, router=r)
+    assert rel_l2(out[sample], (x[sample].astype(np.float64) + sh) + ro) < TOL
+    assert rel_l2(dbg["routed_out"][sample], ro) < TOL
+    assert rel_l2(dbg["shared_out"][sample], sh) < TOL
+
+
+@pytest.mark.parametrize("base,T", [("qwen3", 64), ("qwen3", 512), ("scout", 64), ("dsv2lite", 128)])
+def test_decode_regime_parity(base, T):
+    """configs[4]: decode-sized batches (64-512 tokens per step)."""
+    shape = synth.decode_shape(base, T)
+    ctx = make_ctx(shape, T)
+    w = synth.moe_weights(shape, seed=5)
+    x = synth.tokens(shape, seed=5, T=T)
+    out, dbg = run_blocking(ctx, moe_weights_dev(w), x)
+    ctx.close()
+    lay = _layer_f32(w, shape.top_k)
+    r, _ = om.adopt_router(lay, x, dbg["topk_idx"])
+    np.testing.assert_array_equal(dbg["topk_idx"], r.idx)
+    sh, ro, _ = om.moe_block(x, lay, router=r)
+    assert rel_l2(out, (x.astype(np.float64) + sh) + ro) < TOL
