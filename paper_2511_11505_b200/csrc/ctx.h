@@ -42,6 +42,8 @@ struct fsc_ctx {
   int* rf_list = nullptr;      // [T]                router near-tie list
   int* rf_ctrl = nullptr;      // [2]                {count, ticket}
   double* rf_l64 = nullptr;    // [T, E]             fp64 logits of flagged tokens
+  float* rf_lg = nullptr;      // [T, E]             fp32 logits of flagged tokens
+  float* rf_thr = nullptr;     // [T, 3]             band thresholds of flagged tokens
   float* w_scaled = nullptr;   // [E, d]             gamma * W_R
   float* w_sq = nullptr;       // [E]                ||gamma * W_R[e]||^2
   uint16_t* xs = nullptr;      // bf16 [T*k, d]      expert-sorted send buffer

@@ -120,6 +120,8 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(dalloc(&ctx->rf_list, T));
   CK(dalloc(&ctx->rf_ctrl, 2));
   CK(dalloc(&ctx->rf_l64, T * E));
+  CK(dalloc(&ctx->rf_lg, T * E));
+  CK(dalloc(&ctx->rf_thr, T * 3));
   CK(dalloc(&ctx->w_scaled, E * d));
   CK(dalloc(&ctx->w_sq, E));
   CK(cudaMemset(ctx->rf_ctrl, 0, 2 * sizeof(int)));
@@ -154,7 +156,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->rf_lg, ctx->rf_thr, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -249,7 +251,7 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   const fsc_moe_config& c = ctx->cfg;
   const int d = c.d, E = c.n_experts, k = c.top_k;
   RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
-                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->w_scaled, ctx->w_sq};
+                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->rf_lg, ctx->rf_thr, ctx->w_scaled, ctx->w_sq};
   PH_BEGIN(PH_ROUTER);
   CK(launch_router(rl, s));
   PH_END(PH_ROUTER);
@@ -459,7 +461,7 @@ extern "C" int fsc_op_router(fsc_ctx* ctx, const float* x, const float* gamma, c
   REQUIRE(T >= 0 && T <= ctx->cfg.max_tokens && E <= ctx->cfg.n_experts && d <= ctx->cfg.d, FSC_ERR_CONFIG,
           "router shape beyond the context workspace");
   RouterLaunch rl{x, gamma, w_router, T, d, E, k, ctx->cfg.rms_eps, static_cast<uint16_t*>(xn), topk_idx, topk_w,
-                  logits, n_refined, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->w_scaled, ctx->w_sq};
+                  logits, n_refined, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->rf_lg, ctx->rf_thr, ctx->w_scaled, ctx->w_sq};
   CK(launch_router(rl, static_cast<cudaStream_t>(stream)));
   return FSC_OK;
 }

@@ -65,7 +65,9 @@ struct RouterLaunch {
   int* n_refined;        // optional device counter
   int* rf_list;          // workspace [T]: tokens flagged for fp64 refinement
   int* rf_ctrl;          // workspace [2]: {count, done-ticket}, zero between calls
-  double* rf_l64;        // workspace [T, E]: fp64 logits of flagged tokens
+  double* rf_l64;        // workspace [T, E]: fp64 raw dots of band experts of flagged tokens
+  float* rf_lg;          // workspace [T, E]: fp32 logits of flagged tokens
+  float* rf_thr;         // workspace [T, 3]: {2B, l_(k), l_(k+1)} of flagged tokens
   float* w_scaled;       // workspace [E, d]: gamma * W_R
   float* w_sq;           // workspace [E]: ||gamma * W_R[e]||^2
 };
