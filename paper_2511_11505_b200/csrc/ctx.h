@@ -63,7 +63,8 @@ struct fsc_ctx {
   fsc_peer_state* peer = nullptr;
 
   cudaStream_t comm = nullptr;  // high-priority communication stream
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  cudaStream_t aux = nullptr;   // second compute stream (overlaps independent kernels)
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_d = nullptr;
 
   int pending = 0;
   int no_overlap = 0;          // FarSkip call made under the BLOCKING stack schedule

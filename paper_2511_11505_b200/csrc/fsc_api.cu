@@ -135,6 +135,9 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, -5));
   CK(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_c, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_d, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
   rc = fsc_transport_init(ctx);
   if (rc) return rc;
   return FSC_OK;
@@ -162,6 +165,9 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+  if (ctx->ev_c) cudaEventDestroy(ctx->ev_c);
+  if (ctx->ev_d) cudaEventDestroy(ctx->ev_d);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
   for (int i = 0; i < PH_N; ++i)
     for (int j = 0; j < 2; ++j)
       if (ctx->ph_ev[i][j]) cudaEventDestroy(ctx->ph_ev[i][j]);
@@ -242,29 +248,37 @@ static int validate_call(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const fl
   return FSC_OK;
 }
 
+// Forward declarations (shared expert used by the blocking overlap below)
+static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* resid, float* out,
+                      const fsc_moe_debug* dbg, cudaStream_t s);
+
 // Steps 3-4 of P:198 (gate + dispatch start) and 6 (routed experts). On return
 // the routed expert outputs y are complete in this rank's receive layout and,
 // for EP > 1, already pushed back toward their source ranks (combine started).
+// shared_resid != nullptr (blocking schedule, EP = 1): the shared expert
+// (out = shared_resid + shared) runs on the compute stream right after the router
+// while the permutation maps and the permute run beside it on the aux stream.
 static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in,
                                  const fsc_moe_debug* dbg, cudaStream_t s, fsc_overlap_cb cb, void* user,
-                                 bool overlap) {
+                                 bool overlap, const float* shared_resid = nullptr, float* shared_out = nullptr) {
   const fsc_moe_config& c = ctx->cfg;
   const int d = c.d, E = c.n_experts, k = c.top_k;
   RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
-                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->rf_lg, ctx->rf_thr, ctx->w_scaled, ctx->w_sq};
+                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr, ctx->rf_list, ctx->rf_ctrl,
+                  ctx->rf_l64, ctx->rf_lg, ctx->rf_thr, ctx->w_scaled, ctx->w_sq};
   PH_BEGIN(PH_ROUTER);
   CK(launch_router(rl, s));
   PH_END(PH_ROUTER);
-  PermLaunch pl{ctx->topk_idx, T, k, E, ctx->hist, ctx->base, ctx->counts, ctx->offsets, ctx->pos, ctx->src_row};
-  PH_BEGIN(PH_PERM);
-  CK(launch_perm_maps(pl, s));
-  PH_END(PH_PERM);
-  if (dbg) {
-    if (dbg->topk_idx) CK(cudaMemcpyAsync(dbg->topk_idx, ctx->topk_idx, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
-    if (dbg->topk_w) CK(cudaMemcpyAsync(dbg->topk_w, ctx->topk_w, sizeof(float) * T * k, cudaMemcpyDeviceToDevice, s));
-    if (dbg->counts) CK(cudaMemcpyAsync(dbg->counts, ctx->counts, sizeof(int) * E, cudaMemcpyDeviceToDevice, s));
-    if (dbg->pos) CK(cudaMemcpyAsync(dbg->pos, ctx->pos, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
+  const bool early_shared = shared_out && ctx->ep == 1;
+  cudaStream_t ps = early_shared ? ctx->aux : s;   // stream of the permutation work
+  if (early_shared) {
+    CK(cudaEventRecord(ctx->ev_c, s));
+    CK(cudaStreamWaitEvent(ps, ctx->ev_c, 0));
   }
+  PermLaunch pl{ctx->topk_idx, T, k, E, ctx->hist, ctx->base, ctx->counts, ctx->offsets, ctx->pos, ctx->src_row};
+  PH_BEGIN_ON(PH_PERM, ps);
+  CK(launch_perm_maps(pl, ps));
+  PH_END_ON(PH_PERM, ps);
   // Dispatch: permute into the expert-sorted order and, for EP > 1,
   // straight into the owning ranks' receive buffers. In the FarSkip schedule the
   // counts exchange and dispatch run on the comm stream (P:198 step 4) while the
@@ -275,9 +289,15 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   const int* recv_counts = ctx->counts;
   cudaStream_t cs = overlap ? ctx->comm : s;
   if (ctx->ep == 1) {
-    PH_BEGIN(PH_DISPATCH);
-    CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, s));
-    PH_END(PH_DISPATCH);
+    PH_BEGIN_ON(PH_DISPATCH, ps);
+    CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, ps));
+    PH_END_ON(PH_DISPATCH, ps);
+    if (early_shared) {
+      CK(cudaEventRecord(ctx->ev_d, ps));
+      int rc = moe_shared(ctx, w, T, shared_resid, shared_out, dbg, s);   // beside the permutation
+      if (rc) return rc;
+      CK(cudaStreamWaitEvent(s, ctx->ev_d, 0));
+    }
   } else {
     if (overlap) {
       CK(cudaEventRecord(ctx->ev_a, s));
@@ -293,6 +313,12 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     recv = ctx->xr;
     recv_rows = ctx->recv_rows_cap;
     recv_counts = ctx->recv_counts;
+  }
+  if (dbg) {
+    if (dbg->topk_idx) CK(cudaMemcpyAsync(dbg->topk_idx, ctx->topk_idx, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
+    if (dbg->topk_w) CK(cudaMemcpyAsync(dbg->topk_w, ctx->topk_w, sizeof(float) * T * k, cudaMemcpyDeviceToDevice, s));
+    if (dbg->counts) CK(cudaMemcpyAsync(dbg->counts, ctx->counts, sizeof(int) * E, cudaMemcpyDeviceToDevice, s));
+    if (dbg->pos) CK(cudaMemcpyAsync(dbg->pos, ctx->pos, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
   }
   if (cb) cb(user, 0, s);  // P:198 step 5: attention part (b) while dispatch is in flight
   if (ctx->ep > 1 && overlap) {  // step 6: sync Dispatch (the compute stream stalls only if it is late)
@@ -321,6 +347,10 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     int rc = fsc_transport_combine(ctx, T, s);  // P:198 step 7: Combine completes asynchronously
     if (rc) return rc;
     PH_END(PH_COMBINE);
+  }
+  if (shared_out && !early_shared) {
+    int rc = moe_shared(ctx, w, T, shared_resid, shared_out, dbg, s);
+    if (rc) return rc;
   }
   return FSC_OK;
 }
@@ -388,10 +418,9 @@ extern "C" int fsc_moe_forward_blocking(fsc_ctx* ctx, const fsc_moe_weights* w, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (T == 0 && ctx->ep == 1) return FSC_OK;
   memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
-  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false);
-  if (rc) return rc;
-  // Regular order (C-amb-12): tmp = x_in + shared; out = tmp + routed.
-  rc = moe_shared(ctx, w, T, x_in, ctx->tmp, dbg, s);
+  // Regular order (C-amb-12): tmp = x_in + shared; out = tmp + routed. The shared
+  // expert overlaps the permutation (EP = 1) or follows the routed experts (EP > 1).
+  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false, x_in, ctx->tmp);
   if (rc) return rc;
   return moe_finish(ctx, T, ctx->tmp, out, dbg, s);
 }
