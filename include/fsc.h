@@ -171,6 +171,17 @@ FSC_API int fsc_moe_forward_blocking(fsc_ctx* ctx, const fsc_moe_weights* w, int
 FSC_API int fsc_moe_forward_blocking_host(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in_host,
                                   float* out_host, void* stream);
 
+/* Pipelined host-buffer variant for serving loops: enqueues the H2D copy of
+ * x_in_host (pinned) on an internal copy stream, the forward on `stream` and the
+ * D2H copy into out_host (pinned) on a second copy stream, ordered by events on
+ * two internal staging slots, and returns at once. Step i's compute therefore
+ * overlaps step i+1's upload and step i-1's download. Host buffers must stay
+ * untouched until fsc_host_flush returns (or two calls later). */
+FSC_API int fsc_moe_forward_host_async(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in_host,
+                                       float* out_host, void* stream);
+/* Wait until every fsc_moe_forward_host_async output has reached host memory. */
+FSC_API int fsc_host_flush(fsc_ctx* ctx);
+
 /* FarSkip MoE sub-block (schedule P:198 steps 3-8):
  *   x_in          = mlp-in_k = o_{k-1}        fp32 [T,d]
  *   partial_inout = attn-in_{k+1} in progress: on entry (mlp-in_k + attn-out_k),

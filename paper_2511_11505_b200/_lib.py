@@ -73,6 +73,8 @@ _SIGS = {
     "fsc_timing_log": (_I, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_float), _I]),
     "fsc_moe_forward_blocking": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, ctypes.POINTER(MoeDebugC), _P]),
     "fsc_moe_forward_blocking_host": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, _P]),
+    "fsc_moe_forward_host_async": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, _P]),
+    "fsc_host_flush": (_I, [_P]),
     "fsc_moe_forward_farskip": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, OVERLAP_CB, _P,
                                      ctypes.POINTER(_P), ctypes.POINTER(MoeDebugC), _P]),
     "fsc_moe_wait": (_I, [_P, _P, _P, _P, _P]),
@@ -242,6 +244,14 @@ class Context:
         T = x_host.shape[0]
         self._ck(self.lib.fsc_moe_forward_blocking_host(self.h, ctypes.byref(w.c), T, ptr(x_host), ptr(out_host),
                                                         stream if stream is not None else cur_stream()))
+
+    def moe_forward_host_async(self, w: MoeWeights, x_host, out_host, stream=None):
+        T = x_host.shape[0]
+        self._ck(self.lib.fsc_moe_forward_host_async(self.h, ctypes.byref(w.c), T, ptr(x_host), ptr(out_host),
+                                                     stream if stream is not None else cur_stream()))
+
+    def host_flush(self):
+        self._ck(self.lib.fsc_host_flush(self.h))
 
     def moe_forward_farskip(self, w: MoeWeights, x_in, partial_inout, callback=None,
                             dbg: Optional[MoeDebug] = None, stream=None):

@@ -64,6 +64,12 @@ struct fsc_ctx {
 
   cudaStream_t comm = nullptr;  // high-priority communication stream
   cudaStream_t aux = nullptr;   // second compute stream (overlaps independent kernels)
+  // pipelined host entry point (fsc_moe_forward_host_async)
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  float* io_slot_in[2] = {nullptr, nullptr};
+  float* io_slot_out[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[2] = {}, ev_cdone[2] = {}, ev_out[2] = {};
+  int io_slot = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_d = nullptr;
 
   int pending = 0;

@@ -168,6 +168,15 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   if (ctx->ev_c) cudaEventDestroy(ctx->ev_c);
   if (ctx->ev_d) cudaEventDestroy(ctx->ev_d);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+  if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->io_slot_in[i]) cudaFree(ctx->io_slot_in[i]);
+    if (ctx->io_slot_out[i]) cudaFree(ctx->io_slot_out[i]);
+    if (ctx->ev_in[i]) cudaEventDestroy(ctx->ev_in[i]);
+    if (ctx->ev_cdone[i]) cudaEventDestroy(ctx->ev_cdone[i]);
+    if (ctx->ev_out[i]) cudaEventDestroy(ctx->ev_out[i]);
+  }
   for (int i = 0; i < PH_N; ++i)
     for (int j = 0; j < 2; ++j)
       if (ctx->ph_ev[i][j]) cudaEventDestroy(ctx->ph_ev[i][j]);
@@ -438,6 +447,55 @@ extern "C" int fsc_moe_forward_blocking_host(fsc_ctx* ctx, const fsc_moe_weights
   if (rc) return rc;
   CK(cudaMemcpyAsync(out_host, ctx->io_out, bytes, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return FSC_OK;
+}
+
+// Pipelined host entry: step i's H2D copy (copy stream), MoE forward (caller's
+// stream) and D2H copy (second copy stream) are ordered by events on two device
+// staging slots, so consecutive calls overlap step i+1's upload and step i-1's
+// download with step i's compute. Returns without waiting; fsc_host_flush waits.
+extern "C" int fsc_moe_forward_host_async(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in_host,
+                                          float* out_host, void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(T == 0 || (x_in_host && out_host), FSC_ERR_SHAPE, "null host buffer");
+  REQUIRE(T >= 0 && T <= ctx->cfg.max_tokens, FSC_ERR_CONFIG, "T=%d outside [0,max_tokens]", T);
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long n = (long)ctx->cfg.max_tokens * ctx->cfg.d;
+  if (!ctx->h2d) {
+    CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaMalloc(&ctx->io_slot_in[i], sizeof(float) * n));
+      CK(cudaMalloc(&ctx->io_slot_out[i], sizeof(float) * n));
+      CK(cudaEventCreateWithFlags(&ctx->ev_in[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_cdone[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_out[i], cudaEventDisableTiming));
+      CK(cudaEventRecord(ctx->ev_cdone[i], s));
+      CK(cudaEventRecord(ctx->ev_out[i], s));
+    }
+  }
+  const int slot = ctx->io_slot;
+  ctx->io_slot ^= 1;
+  const size_t bytes = sizeof(float) * (size_t)T * ctx->cfg.d;
+  CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_cdone[slot], 0));      // slot's previous compute read its input
+  CK(cudaMemcpyAsync(ctx->io_slot_in[slot], x_in_host, bytes, cudaMemcpyHostToDevice, ctx->h2d));
+  CK(cudaEventRecord(ctx->ev_in[slot], ctx->h2d));
+  CK(cudaStreamWaitEvent(s, ctx->ev_in[slot], 0));
+  CK(cudaStreamWaitEvent(s, ctx->ev_out[slot], 0));               // slot's previous download finished
+  int rc = fsc_moe_forward_blocking(ctx, w, T, ctx->io_slot_in[slot], ctx->io_slot_out[slot], nullptr, stream);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev_cdone[slot], s));
+  CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_cdone[slot], 0));
+  CK(cudaMemcpyAsync(out_host, ctx->io_slot_out[slot], bytes, cudaMemcpyDeviceToHost, ctx->d2h));
+  CK(cudaEventRecord(ctx->ev_out[slot], ctx->d2h));
+  return FSC_OK;
+}
+
+extern "C" int fsc_host_flush(fsc_ctx* ctx) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->d2h) CK(cudaStreamSynchronize(ctx->d2h));
   return FSC_OK;
 }
 
