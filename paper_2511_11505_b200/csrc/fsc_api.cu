@@ -122,7 +122,7 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(dalloc(&ctx->rf_l64, T * E));
   CK(dalloc(&ctx->rf_lg, T * E));
   CK(dalloc(&ctx->rf_thr, T * 3));
-  CK(dalloc(&ctx->w_scaled, E * d));
+  CK(dalloc(&ctx->w_scaled, (E > 128 ? E : 128) * d));  // e-major [E][d] or k-major [d][EP<=128]
   CK(dalloc(&ctx->w_sq, E));
   CK(cudaMemset(ctx->rf_ctrl, 0, 2 * sizeof(int)));
   CK(dalloc(&ctx->xs, (T * k > ctx->max_recv ? T * k : ctx->max_recv) * d));

@@ -70,6 +70,7 @@ struct RouterLaunch {
   float* rf_thr;         // workspace [T, 3]: {2B, l_(k), l_(k+1)} of flagged tokens
   float* w_scaled;       // workspace [E, d]: gamma * W_R
   float* w_sq;           // workspace [E]: ||gamma * W_R[e]||^2
+  int rpb = 32;          // tokens per CTA (set by launch_router)
 };
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s);
 

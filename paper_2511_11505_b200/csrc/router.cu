@@ -12,7 +12,7 @@
 // (k+1)-th largest fp32 logits, an expert with v > t_hi + 2B is certainly selected
 // and one with v < t_lo - 2B certainly not; only the experts in between ("the
 // band", usually 2-3) of tokens with t_hi - t_lo <= 2B are recomputed in fp64
-// (router_refine_*) and the missing slots filled by their fp64 order. The
+// (router_refine_kernel) and the missing slots filled by their fp64 order. The
 // selection therefore equals the fp64 selection of the oracle for every token.
 //
 // Main kernel (E > 32): block = 32 tokens x 64/128 experts, 8 warps; each warp
@@ -72,24 +72,55 @@ template <int N>
 FSC_DEVINL void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 }  // namespace
 
-// W'[e][i] = gamma_i * W_R[e][i] and ||W'_e||^2 (error bound). One warp per expert.
+// W'[e][i] = gamma_i * W_R[e][i] and ||W'_e||^2 (error bound). One CTA per expert.
+// ldt > 0: W' is written k-major (W'T[i][e], row stride ldt, rows padded with
+// zeros for E <= e < ldt by the CTAs with e >= E) for the FFMA2 main kernel.
 __global__ void __launch_bounds__(256) router_prescale_kernel(const float* __restrict__ W,
                                                               const float* __restrict__ gamma, float* __restrict__ Wg,
-                                                              float* __restrict__ wq, int E, int d) {
-  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (e >= E) return;
+                                                              float* __restrict__ wq, int E, int d, int ldt) {
+  __shared__ float red[8];
+  const int e = blockIdx.x, tid = threadIdx.x;
+  if (e >= E) {                                  // zero padding columns of W'T
+    for (int c = tid; c < d; c += 256) Wg[(long)c * ldt + e] = 0.f;
+    return;
+  }
   const float4* w = reinterpret_cast<const float4*>(W + (long)e * d);
   const float4* g = reinterpret_cast<const float4*>(gamma);
-  float4* o = reinterpret_cast<float4*>(Wg + (long)e * d);
   float s = 0.f;
-  for (int c = lane; c < d / 4; c += 32) {
+  for (int c = tid; c < d / 4; c += 256) {
     const float4 a = w[c], b = g[c];
     const float4 v = make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w);
-    o[c] = v;
+    if (ldt > 0) {
+      float* o = Wg + (long)(4 * c) * ldt + e;
+      o[0] = v.x;
+      o[ldt] = v.y;
+      o[2 * ldt] = v.z;
+      o[3 * ldt] = v.w;
+    } else {
+      reinterpret_cast<float4*>(Wg + (long)e * d)[c] = v;
+    }
     s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   s = warp_sum_f32(s);
-  if (lane == 0) wq[e] = s;
+  if ((tid & 31) == 0) red[tid >> 5] = s;
+  __syncthreads();
+  if (tid == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i];
+    wq[e] = t;
+  }
+}
+
+// packed fp32x2 FMA (sm_100 FFMA2) with a scalar operand broadcast to both lanes:
+// acc.{x,y} += a * b.{x,y}
+FSC_DEVINL void ffma2_bcast(float2& acc, float a, float2 b) {
+  unsigned long long B = *reinterpret_cast<unsigned long long*>(&b);
+  unsigned long long C = *reinterpret_cast<unsigned long long*>(&acc);
+  unsigned long long A;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(A) : "f"(a));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
+  acc = *reinterpret_cast<float2*>(&C);
 }
 
 // Phase C for one token (one warp): top-k over the fp32 logits of row `lg`, gates,
@@ -138,7 +169,7 @@ FSC_DEVINL void select_token(const float* lg, long t, float B, const RouterLaunc
   }
   const float thr2 = 2.f * B + 4.f * kU * (fabsf(vk) + fabsf(vk1)) + 1e-7f;
   if (k < E && vk - vk1 <= thr2) {
-    // ambiguous boundary: record the token, its fp32 row and thresholds for router_refine_*
+    // ambiguous boundary: record the token, its fp32 row and thresholds for router_refine_kernel
     int slot = 0;
     if (lane == 0) {
       if (L.n_refined) atomicAdd(L.n_refined, 1);
@@ -172,21 +203,34 @@ FSC_DEVINL void select_token(const float* lg, long t, float B, const RouterLaunc
   }
 }
 
-// xn = bf16(x gamma r) for the block's rows (rows were just streamed: L2 hits)
-FSC_DEVINL void write_xn(const RouterLaunch& L, long t0, const float* s_r, int tid, int nt) {
+// xn = bf16(x gamma r) for the block's rows (rows were just streamed: L2 hits);
+// loads are issued in batches of 8 per thread to keep enough bytes in flight.
+FSC_DEVINL void write_xn(const RouterLaunch& L, long t0, int rows, const float* s_r, int tid, int nt) {
   const int d = L.d;
-  const int rows = (int)min((long)TB, (long)L.T - t0);
   const int dv = d / 4;
+  const int n = rows * dv;
   const float4* g4 = reinterpret_cast<const float4*>(L.gamma);
-#pragma unroll 4
-  for (int i = tid; i < rows * dv; i += nt) {
-    const int tt = i / dv, c = i - tt * dv;
-    const long t = t0 + tt;
-    const float4 v = reinterpret_cast<const float4*>(L.x + t * d)[c];
-    const float4 g = g4[c];
-    const float r = s_r[tt];
-    reinterpret_cast<uint2*>(L.xn + t * d)[c] =
-        make_uint2(pack_bf16x2(v.x * g.x * r, v.y * g.y * r), pack_bf16x2(v.z * g.z * r, v.w * g.w * r));
+  const float4* x4 = reinterpret_cast<const float4*>(L.x + t0 * d);
+  uint2* o2 = reinterpret_cast<uint2*>(L.xn + t0 * d);
+  for (int base = tid; base < n; base += 8 * nt) {
+    float4 v[8], g[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * nt;
+      if (i < n) {
+        v[u] = x4[i];
+        g[u] = g4[i % dv];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * nt;
+      if (i < n) {
+        const float r = s_r[i / dv];
+        o2[i] = make_uint2(pack_bf16x2(v[u].x * g[u].x * r, v[u].y * g[u].y * r),
+                           pack_bf16x2(v[u].z * g[u].z * r, v[u].w * g[u].w * r));
+      }
+    }
   }
 }
 
@@ -201,7 +245,10 @@ FSC_DEVINL void write_xn(const RouterLaunch& L, long t0, const float* s_r, int t
 #define RSTAMP(kk)
 #endif
 
-// E in (32, 128]: 8 warps = KS k-groups x NEH expert halves of 64; 8x8 tile per lane.
+// E in (32, 128]: 8 warps = KS k-groups x NEH expert halves of 64. Each lane owns
+// 8 tokens (lt + 4i) x 4 expert pairs (2 le + 16 j + {0,1}); x is staged token-major,
+// W' k-major, so one LDS.64 yields an expert pair at one k and every product is an
+// FFMA2 with the token value broadcast (full fp32 issue rate on sm_100).
 template <int EW>
 __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
   constexpr int EP = 32 * EW;          // padded experts: 64 or 128
@@ -211,10 +258,11 @@ __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
   constexpr int NT = 256;
   constexpr int XV = TB * DC / 4 / NT; // float4 of the x chunk per thread (2)
   constexpr int WV = EP * DC / 4 / NT; // float4 of the W' chunk per thread (4 / 8)
-  constexpr int BUF = (TB + EP) * LDS;
+  constexpr int XBUF = TB * LDS;       // x chunk, token-major [TB][LDS]
+  constexpr int BUF = XBUF + DC * EP;  // + W' chunk, k-major [DC][EP]
   constexpr int NS = EW >= 4 ? 3 : 4;  // cp.async pipeline depth
   extern __shared__ __align__(16) float sm[];
-  float* stage0 = sm;                  // [NS][TB+EP][LDS]
+  float* stage0 = sm;                  // [NS][BUF]
   float* red = sm;                     // [KS][TB][EP] k-group partials (after the loop)
   float* lg = sm + KS * TB * EP;       // [TB][EP+1] fp32 logits
   float* s_r = sm + NS * BUF;          // [TB]
@@ -222,10 +270,12 @@ __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
   float* s_wsq = s_xn + TB;            // [EP]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int T = L.T, d = L.d, E = L.E;
-  const long t0 = (long)blockIdx.x * TB;
+  const int d = L.d, E = L.E;
+  const long t0 = (long)blockIdx.x * L.rpb;    // rpb <= TB rows per block (balanced grid)
+  const int rows = (int)min((long)L.rpb, (long)L.T - t0);
+  const long T = t0 + rows;                    // rows >= T are padding
   const float* __restrict__ x = L.x;
-  const float* __restrict__ W = L.w_scaled;
+  const float* __restrict__ WT = L.w_scaled;   // [d][EP]
   RSTAMP(0);
   auto issue_chunk = [&](int c0, float* buf) {
 #pragma unroll
@@ -237,9 +287,8 @@ __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
     }
 #pragma unroll
     for (int v = 0; v < WV; ++v) {
-      const int i = tid + v * NT;
-      const int e = i / (DC / 4), cc = (i % (DC / 4)) * 4;
-      cp_async16(buf + (TB + e) * LDS + cc, W + (long)(e < E ? e : 0) * d + c0 + cc, e < E);
+      const int i = tid + v * NT;       // float4 index inside the [DC][EP] chunk
+      cp_async16(buf + XBUF + 4 * i, WT + (long)c0 * EP + 4 * i, true);
     }
     cp_async_commit();
   };
@@ -252,11 +301,11 @@ __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
   for (int e = tid; e < EP; e += NT) s_wsq[e] = e < E ? L.w_sq[e] : 0.f;
 
   const int eh = warp % NEH, ks = warp / NEH, lt = lane >> 3, le = lane & 7;
-  float acc[8][8];
+  float2 acc[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
   double ssp = 0.0;                     // partial sum x^2 of row tid/8 (8 values per chunk)
   const int srow = tid >> 3, scol = (tid & 7) * 8;
 
@@ -273,20 +322,23 @@ __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
              ((double)q.x * q.x + (double)q.y * q.y) + ((double)q.z * q.z + (double)q.w * q.w);
     }
     const float* xa = buf + lt * LDS + ks * KW;
-    const float* wb = buf + (TB + eh * 64 + le) * LDS + ks * KW;
+    const float* wb = buf + XBUF + (ks * KW) * EP + eh * 64 + 2 * le;
 #pragma unroll
     for (int kk = 0; kk < KW; kk += 2) {
-      float2 a[8], b[8];
+      float2 a[8], b0[4], b1[4];
 #pragma unroll
       for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float2*>(xa + 4 * i * LDS + kk);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) b[j] = *reinterpret_cast<const float2*>(wb + 8 * j * LDS + kk);
+      for (int j = 0; j < 4; ++j) {
+        b0[j] = *reinterpret_cast<const float2*>(wb + kk * EP + 16 * j);
+        b1[j] = *reinterpret_cast<const float2*>(wb + (kk + 1) * EP + 16 * j);
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          acc[i][j] = fmaf(a[i].x, b[j].x, acc[i][j]);
-          acc[i][j] = fmaf(a[i].y, b[j].y, acc[i][j]);
+        for (int j = 0; j < 4; ++j) {
+          ffma2_bcast(acc[i][j], a[i].x, b0[j]);
+          ffma2_bcast(acc[i][j], a[i].y, b1[j]);
         }
     }
   }
@@ -295,7 +347,8 @@ __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) red[(ks * TB + lt + 4 * i) * EP + eh * 64 + le + 8 * j] = acc[i][j];
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<float2*>(&red[(ks * TB + lt + 4 * i) * EP + eh * 64 + 2 * le + 16 * j]) = acc[i][j];
   // per-row sum x^2: the 8 threads of a row are consecutive lanes
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) ssp += __shfl_xor_sync(0xffffffff, ssp, o);
@@ -317,13 +370,13 @@ __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
   for (int e = lane; e < E; e += 32) wm = fmaxf(wm, s_wsq[e]);
   const float wmax = sqrtf(warp_max_f32(wm)) * 1.01f;
   const float chain = (float)(d / KS + KS + 6);
-  for (int tt = warp; tt < TB; tt += 8) {
-    const long t = t0 + tt;
-    if (t >= T) break;
-    select_token<EW>(lg + tt * (EP + 1), t, s_r[tt] * chain * kU * s_xn[tt] * wmax, L, lane);
+  if (warp < 4) {            // warps 0-3 select while warps 4-7 write xn
+    for (int tt = warp; tt < rows; tt += 4)
+      select_token<EW>(lg + tt * (EP + 1), t0 + tt, s_r[tt] * chain * kU * s_xn[tt] * wmax, L, lane);
+  } else {
+    write_xn(L, t0, rows, s_r, tid - 128, 128);
   }
   RSTAMP(3);
-  write_xn(L, t0, s_r, tid, NT);
   __syncthreads();
   RSTAMP(4);
 }
@@ -437,115 +490,127 @@ __global__ void __launch_bounds__(128) router_kernel_small(RouterLaunch L) {
     if (t >= T) break;
     select_token<1>(lg + tt * (EP + 1), t, s_r[tt] * chain * kU * s_xn[tt] * wmax, L, lane);
   }
-  write_xn(L, t0, s_r, tid, NT);
+  write_xn(L, t0, (int)min((long)TB, (long)T - t0), s_r, tid, NT);
 }
 
-// Band refinement, step 1: fp64 raw dot sum_i x_i gamma_i W_ei for every expert e in
-// the ambiguous band of a flagged token (one CTA per (token, expert) item, d split
-// over 256 threads; items outside the band are skipped at once). The positive
-// factor r_t does not change the order.
-__global__ void __launch_bounds__(256) router_refine_logits_kernel(RouterLaunch L) {
-  __shared__ double red[8];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int d = L.d, E = L.E;
-  const int n = *reinterpret_cast<volatile int*>(&L.rf_ctrl[0]);
-  for (int item = blockIdx.x; item < n * E; item += gridDim.x) {   // one CTA per band item
-    const int slot = item / E, e = item % E;
-    const float v = L.rf_lg[(long)slot * E + e];
-    const float thr2 = L.rf_thr[3 * slot], hi = L.rf_thr[3 * slot + 1], lo = L.rf_thr[3 * slot + 2];
-    if (v > hi + thr2 || v < lo - thr2) continue;        // certainly in / certainly out
-    const long t = L.rf_list[slot];
-    const float* xr = L.x + t * d;
-    const float* wr = L.w_router + (long)e * d;
-    double s = 0.0;
-    for (int c = tid; c < d; c += 256) s = fma((double)xr[c] * (double)L.gamma[c], (double)wr[c], s);
-    s = warp_sum_f64(s);
-    if (lane == 0) red[warp] = s;
-    __syncthreads();
-    if (tid == 0) {
-      double tot = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) tot += red[w];
-      L.rf_l64[(long)slot * E + e] = tot;
-    }
-    __syncthreads();
-  }
-}
-
-// Band refinement, step 2 (one warp per flagged token): certain experts + the best
-// band experts by fp64 logit (ties -> lower id) fill the k slots; gates from the
-// fp32 logits. The last CTA resets the flag list for the next call.
+// Band refinement (one CTA per flagged token, grid-stride): warp 0 classifies the
+// experts against the token's fp32 band (certainly in / band / certainly out);
+// the 8 warps compute the fp64 raw dots sum_i x_i gamma_i W_ei of the band experts
+// (the positive factor r_t does not change their order); warp 0 then fills the
+// k - |certain| open slots with the best band experts (fp64 value, ties -> lower
+// id) and writes indices and gates (fp32 logits, as for every other token). The
+// last CTA resets the flag list for the next call.
 template <int QN>
-__global__ void __launch_bounds__(256) router_refine_select_kernel(RouterLaunch L) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int E = L.E, k = L.k;
+__global__ void __launch_bounds__(256) router_refine_kernel(RouterLaunch L) {
+  __shared__ int s_band[128];
+  __shared__ int s_nb;
+  __shared__ double s_l64[128];
+  __shared__ double s_red[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int d = L.d, E = L.E, k = L.k;
   const int n = *reinterpret_cast<volatile int*>(&L.rf_ctrl[0]);
-  for (int i = gw; i < n; i += nw) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const long t = L.rf_list[i];
     const float thr2 = L.rf_thr[3 * i], hi = L.rf_thr[3 * i + 1], lo = L.rf_thr[3 * i + 2];
     float v[QN];
-    double l64[QN];
     uint32_t sel = 0, band = 0;
-#pragma unroll
-    for (int q = 0; q < QN; ++q) {
-      const int e = lane + 32 * q;
-      v[q] = e < E ? L.rf_lg[(long)i * E + e] : -FLT_MAX;
-      const bool in = e < E && v[q] > hi + thr2;
-      const bool bnd = e < E && !in && !(v[q] < lo - thr2);
-      if (in) sel |= 1u << q;
-      if (bnd) band |= 1u << q;
-      l64[q] = bnd ? L.rf_l64[(long)i * E + e] : -DBL_MAX;
-    }
-    int nsel = 0;
-#pragma unroll
-    for (int q = 0; q < QN; ++q) nsel += __popc(__ballot_sync(0xffffffff, (sel >> q) & 1u));
-    for (int rd = nsel; rd < k; ++rd) {
-      double bv = -DBL_MAX;
-      int bi = 0x7fffffff;
+    if (warp == 0) {
+      int nb = 0;
 #pragma unroll
       for (int q = 0; q < QN; ++q) {
         const int e = lane + 32 * q;
-        if (((band >> q) & 1u) && !((sel >> q) & 1u) && (l64[q] > bv || (l64[q] == bv && e < bi))) {
-          bv = l64[q];
-          bi = e;
+        v[q] = e < E ? L.rf_lg[(long)i * E + e] : -FLT_MAX;
+        const bool in = e < E && v[q] > hi + thr2;
+        const bool bnd = e < E && !in && !(v[q] < lo - thr2);
+        if (in) sel |= 1u << q;
+        if (bnd) band |= 1u << q;
+        const uint32_t m = __ballot_sync(0xffffffff, bnd);
+        if (bnd) s_band[nb + __popc(m & ((1u << lane) - 1u))] = e;
+        nb += __popc(m);
+      }
+      if (lane == 0) s_nb = nb;
+    }
+    __syncthreads();
+    const int nb = s_nb;
+    const float* xr = L.x + t * d;
+    for (int b = 0; b < nb; ++b) {            // all 256 threads on one band expert at a time
+      const int e = s_band[b];
+      const float* wr = L.w_router + (long)e * d;
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+      for (int c0 = 0; c0 < d; c0 += 2048) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + tid + 256 * u;
+          if (c < d) acc[u] = fma((double)xr[c] * (double)L.gamma[c], (double)wr[c], acc[u]);
         }
       }
+      double sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      sum = warp_sum_f64(sum);
+      if (lane == 0) s_red[warp] = sum;
+      __syncthreads();
+      if (tid == 0) {
+        double tot = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffff, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffff, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        for (int w = 0; w < 8; ++w) tot += s_red[w];
+        s_l64[e] = tot;
       }
-      if (bi != 0x7fffffff && (bi & 31) == lane) sel |= 1u << (bi >> 5);
+      __syncthreads();
     }
-    float vtop = -FLT_MAX;
+    if (warp == 0) {
+      double l64[QN];
 #pragma unroll
-    for (int q = 0; q < QN; ++q)
-      if ((sel >> q) & 1u) vtop = fmaxf(vtop, v[q]);
-    vtop = warp_max_f32(vtop);
-    float ex[QN], sum = 0.f;
+      for (int q = 0; q < QN; ++q) l64[q] = ((band >> q) & 1u) ? s_l64[lane + 32 * q] : -DBL_MAX;
+      int nsel = 0;
 #pragma unroll
-    for (int q = 0; q < QN; ++q) {
-      ex[q] = ((sel >> q) & 1u) ? expf(v[q] - vtop) : 0.f;
-      sum += ex[q];
-    }
-    sum = warp_sum_f32(sum);
-    int slot = 0;
+      for (int q = 0; q < QN; ++q) nsel += __popc(__ballot_sync(0xffffffff, (sel >> q) & 1u));
+      for (int rd = nsel; rd < k; ++rd) {
+        double bv = -DBL_MAX;
+        int bi = 0x7fffffff;
 #pragma unroll
-    for (int q = 0; q < QN; ++q) {
-      const uint32_t m = __ballot_sync(0xffffffff, (sel >> q) & 1u);
-      if ((sel >> q) & 1u) {
-        const int s = slot + __popc(m & ((1u << lane) - 1u));
-        L.topk_idx[t * k + s] = lane + 32 * q;
-        L.topk_w[t * k + s] = ex[q] / sum;
+        for (int q = 0; q < QN; ++q) {
+          const int e = lane + 32 * q;
+          if (((band >> q) & 1u) && !((sel >> q) & 1u) && (l64[q] > bv || (l64[q] == bv && e < bi))) {
+            bv = l64[q];
+            bi = e;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffff, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffff, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        if (bi != 0x7fffffff && (bi & 31) == lane) sel |= 1u << (bi >> 5);
       }
-      slot += __popc(m);
+      float vtop = -FLT_MAX;
+#pragma unroll
+      for (int q = 0; q < QN; ++q)
+        if ((sel >> q) & 1u) vtop = fmaxf(vtop, v[q]);
+      vtop = warp_max_f32(vtop);
+      float ex[QN], sum = 0.f;
+#pragma unroll
+      for (int q = 0; q < QN; ++q) {
+        ex[q] = ((sel >> q) & 1u) ? expf(v[q] - vtop) : 0.f;
+        sum += ex[q];
+      }
+      sum = warp_sum_f32(sum);
+      int slot = 0;
+#pragma unroll
+      for (int q = 0; q < QN; ++q) {
+        const uint32_t m = __ballot_sync(0xffffffff, (sel >> q) & 1u);
+        if ((sel >> q) & 1u) {
+          const int s = slot + __popc(m & ((1u << lane) - 1u));
+          L.topk_idx[t * k + s] = lane + 32 * q;
+          L.topk_w[t * k + s] = ex[q] / sum;
+        }
+        slot += __popc(m);
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     __threadfence();
     if (atomicAdd(&L.rf_ctrl[1], 1) == (int)gridDim.x - 1) {
       L.rf_ctrl[0] = 0;
@@ -557,9 +622,19 @@ __global__ void __launch_bounds__(256) router_refine_select_kernel(RouterLaunch 
 
 template <int EW>
 static cudaError_t launch_router_t(const RouterLaunch& L, cudaStream_t s) {
-  const int grid = (L.T + TB - 1) / TB;
-  g_launches += 4;
-  router_prescale_kernel<<<(L.E * 32 + 255) / 256, 256, 0, s>>>(L.w_router, L.gamma, L.w_scaled, L.w_sq, L.E, L.d);
+  RouterLaunch LL = L;
+  LL.rpb = TB;
+  if constexpr (EW > 1) {   // balance the grid: exactly 2 CTAs per SM when T is large
+    const int want = 2 * kNumSMs;
+    LL.rpb = (L.T + want - 1) / want;
+    if (LL.rpb > TB) LL.rpb = TB;
+    if (LL.rpb < 1) LL.rpb = 1;
+  }
+  const int grid = (L.T + LL.rpb - 1) / LL.rpb;
+  g_launches += 3;
+  constexpr int EPAD = 32 * EW;
+  router_prescale_kernel<<<EW == 1 ? L.E : EPAD, 256, 0, s>>>(L.w_router, L.gamma, L.w_scaled, L.w_sq, L.E, L.d,
+                                                              EW == 1 ? 0 : EPAD);
   if constexpr (EW == 1) {
     constexpr int NS = 4, EP = 32;
     const size_t smem = (size_t)(NS * (TB + EP) * LDS + 2 * TB + EP) * 4 + 16;
@@ -569,20 +644,19 @@ static cudaError_t launch_router_t(const RouterLaunch& L, cudaStream_t s) {
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    router_kernel_small<<<grid, 128, smem, s>>>(L);
+    router_kernel_small<<<grid, 128, smem, s>>>(LL);
   } else {
     constexpr int EP = 32 * EW, NS = EW >= 4 ? 3 : 4;
-    const size_t smem = (size_t)(NS * (TB + EP) * LDS + 2 * TB + EP) * 4 + 16;
+    const size_t smem = (size_t)(NS * (TB * LDS + DC * EP) + 2 * TB + EP) * 4 + 16;
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(router_kernel<EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    router_kernel<EW><<<grid, 256, smem, s>>>(L);
+    router_kernel<EW><<<grid, 256, smem, s>>>(LL);
   }
-  router_refine_logits_kernel<<<4 * kNumSMs, 256, 0, s>>>(L);
-  router_refine_select_kernel<EW><<<16, 256, 0, s>>>(L);
+  router_refine_kernel<EW><<<kNumSMs, 256, 0, s>>>(L);
   return cudaGetLastError();
 }
 

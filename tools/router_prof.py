@@ -7,7 +7,7 @@ import synth
 from paper_2511_11505_b200 import Context
 from tests.gpu_util import dev_f32
 torch.cuda.set_device(0)
-shape = synth.CONFIGS["dsv2lite"]
+shape = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "dsv2lite"]
 T = shape.tokens
 w = synth.moe_weights(__import__("dataclasses").replace(shape, ffn=64, shared_ffn=0), seed=0)
 x = dev_f32(synth.tokens(shape, T=T))
@@ -22,9 +22,9 @@ for _ in range(3):
 torch.cuda.synchronize()
 s = stamps.view(nb, 8).cpu().numpy().astype(np.float64)
 t0 = s[:, 0].min()
-for k, name in enumerate(["start", "phaseA done", "phaseB done", "norms/lg done", "phaseC done"]):
+for k, name in enumerate(["start", "loop done", "lg done", "select done", "xn done"]):
     v = (s[:, k] - t0) / 1e3
     print(f"{name:14s} min {v.min():8.1f} us  median {np.median(v):8.1f}  max {v.max():8.1f}")
 d = (s[:, 1:5] - s[:, 0:4]) / 1e3
-for k, name in enumerate(["A", "B", "norm", "C"]):
+for k, name in enumerate(["loop", "reduce", "select", "xn"]):
     print(f"per-block {name:5s}: median {np.median(d[:, k]):7.1f} us  max {d[:, k].max():7.1f}")
