@@ -143,6 +143,18 @@ def oracle_tokens_per_s(shape, budget_s=12.0, seed=0, max_tokens=None):
     return done / t_used, done, t_used, cores
 
 
+def allreduce_max(vals, dev):
+    """MAX over ranks of a list of floats (device tensor on NCCL, host tensor on gloo)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(vals)
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor(list(vals), dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.cpu()]
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import torch
@@ -152,6 +164,11 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FSC_BENCH_ONE_GPU=1: every rank on cuda:0 over gloo - exercises the N>1 code
+    # path (EP transport, timing reductions) on a single-GPU box; timings meaningless.
+    one_gpu = os.environ.get("FSC_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if rank == 0:
@@ -159,7 +176,10 @@ def run_gpu(args):
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist.barrier()
         fbuild.build()
     else:
@@ -245,10 +265,7 @@ def run_gpu(args):
         launches = launches_per_step * args.steps
     ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(sum(ms))
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = allreduce_max([total_ms], dev)[0]
     ms_per_step = total_ms / args.steps
     value = T * world * args.steps / (total_ms / 1e3)
 
@@ -279,10 +296,7 @@ def run_gpu(args):
         ctx.moe_forward_host_async(wd, xh[i % 2], oh[i % 2], stream=stream.cuda_stream)
     ctx.host_flush()
     e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = allreduce_max([e2e_s], dev)[0]
     e2e_value = T * world * e2e_steps / e2e_s
     # synchronous variant (one call = H2D + forward + D2H + stream sync), for reference
     t0 = time.perf_counter()
@@ -402,9 +416,7 @@ def stack_measure(ctx, shape, wd, x, L, steps, world, dev, rank, seed):
             if ph in comm:
                 comm[ph] += ms
         exposed = (comm["dispatch"] if name == "blocking" else comm["dispatch_stall"]) + comm["combine_wait"]
-        vals = torch.tensor([t, exposed / steps / L], device=dev)
-        if world > 1:
-            dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        vals = allreduce_max([t, exposed / steps / L], dev)
         res[name] = {"ms_per_stack": float(vals[0]), "ms_per_layer": float(vals[0]) / L,
                      "exposed_comm_us_per_layer": float(vals[1]) * 1e3,
                      "phase_ms_per_layer": {k: v / steps / L for k, v in comm.items()}}

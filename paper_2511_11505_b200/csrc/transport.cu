@@ -17,7 +17,9 @@
 //                 EPI_BF16 with a scatter map): each output row is stored into its
 //                 source rank's ys buffer at the row it was sent from; a signal
 //                 kernel then raises flag_comb at every source.
-// Flags carry a per-call epoch, so nothing is ever reset. The same code serves
+// Flags carry a per-call epoch, so nothing is ever reset. The epoch lives in device
+// memory (bumped by the counts kernel, read by the others), so a captured CUDA graph
+// of a whole layer replays correctly. The same code serves
 // P processes on one GPU (tests) and one process per GPU over NVLink/NVSwitch.
 #include <string.h>
 
@@ -41,7 +43,7 @@ Layout layout_for(const fsc_ctx* c) {
   const size_t P = c->ep, E = c->cfg.n_experts, d = c->cfg.d;
   const size_t Tk = (size_t)c->cfg.max_tokens * c->cfg.top_k;
   L.flags = 0;                                       // int [3][kMaxP]
-  L.cnt = align_up(L.flags + 3 * kMaxP * sizeof(int));
+  L.cnt = align_up(L.flags + (3 * kMaxP + 1) * sizeof(int));   // 3 flag rows + epoch
   L.ret = align_up(L.cnt + P * E * sizeof(int));     // int [max_recv]
   L.xr = align_up(L.ret + (size_t)c->max_recv * sizeof(int));
   L.ys = align_up(L.xr + (size_t)c->max_recv * d * 2);
@@ -54,6 +56,9 @@ struct Peers {
 };
 
 enum { FLAG_CNT = 0, FLAG_DISP = 1, FLAG_COMB = 2 };
+constexpr int kEpochSlot = 3 * kMaxP;   // int index of the epoch counter in the flags area
+
+FSC_DEVINL int read_epoch(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
 FSC_DEVINL int* flag_ptr(char* base, int slot, int src) {
   return reinterpret_cast<int*>(base) + slot * kMaxP + src;
@@ -82,17 +87,23 @@ struct fsc_peer_state {
   bool opened[kMaxP] = {};
   int* send_base = nullptr;       // [E]   first row of my expert-e rows in the owner's xr
   int* ticket = nullptr;          // [1]   dispatch-kernel completion ticket
-  int epoch = 0;
 };
 
 // ----------------------------------------------------------------------------- kernels
 
 // a5: counts all-gather through peer stores + receive-side bookkeeping.
-__global__ void __launch_bounds__(256) ep_counts_kernel(Peers peers, int rank, int P, int E, int e_loc, int epoch,
+__global__ void __launch_bounds__(256) ep_counts_kernel(Peers peers, int rank, int P, int E, int e_loc, int* epoch_ptr,
                                                         size_t off_cnt, const int* __restrict__ counts,
                                                         int* __restrict__ send_base, int* __restrict__ recv_counts) {
   __shared__ int cnt[kMaxP * 128];
+  __shared__ int s_epoch;
   const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_epoch = read_epoch(epoch_ptr) + 1;   // this call's epoch
+    *epoch_ptr = s_epoch;
+  }
+  __syncthreads();
+  const int epoch = s_epoch;
   for (int i = tid; i < P * E; i += blockDim.x) {
     const int p = i / E, e = i % E;
     reinterpret_cast<int*>(peers.base[p] + off_cnt)[rank * E + e] = counts[e];
@@ -125,7 +136,8 @@ __global__ void __launch_bounds__(256) ep_counts_kernel(Peers peers, int rank, i
 
 // a4 + a6: permute-and-dispatch. One warp per send row q (expert-sorted order).
 __global__ void __launch_bounds__(256) ep_dispatch_kernel(Peers peers, int rank, int P, int R, int d, int E,
-                                                          int e_loc, int epoch, size_t off_xr, size_t off_ret,
+                                                          int e_loc, const int* epoch_ptr, size_t off_xr,
+                                                          size_t off_ret,
                                                           const uint4* __restrict__ xn, const int* __restrict__ src_row,
                                                           const int* __restrict__ offsets,
                                                           const int* __restrict__ send_base, int* ticket) {
@@ -148,6 +160,7 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(Peers peers, int rank,
     if (lane == 0) reinterpret_cast<int*>(peers.base[p] + off_ret)[dst] = (rank << 24) | (int)q;
   }
   // last CTA out raises the dispatch flag at every destination
+  const int epoch = read_epoch(epoch_ptr);
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -159,13 +172,14 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(Peers peers, int rank,
   }
 }
 
-__global__ void ep_signal_kernel(Peers peers, int rank, int P, int slot, int epoch) {
+__global__ void ep_signal_kernel(Peers peers, int rank, int P, int slot, const int* epoch_ptr) {
+  const int epoch = read_epoch(epoch_ptr);
   __threadfence_system();
   if (threadIdx.x < P) st_release_sys(flag_ptr(peers.base[threadIdx.x], slot, rank), epoch);
 }
 
-__global__ void ep_wait_kernel(char* mybase, int slot, int P, int epoch) {
-  if (threadIdx.x == 0) wait_flags(mybase, slot, P, epoch);
+__global__ void ep_wait_kernel(char* mybase, int slot, int P, const int* epoch_ptr) {
+  if (threadIdx.x == 0) wait_flags(mybase, slot, P, read_epoch(epoch_ptr));
   __syncthreads();
 }
 
@@ -193,7 +207,7 @@ int fsc_transport_init(fsc_ctx* ctx) {
   ctx->peer = st;
   st->lay = layout_for(ctx);
   TCK(cudaMalloc(&st->local, st->lay.total));
-  TCK(cudaMemset(st->local, 0, st->lay.flags + 3 * kMaxP * sizeof(int)));
+  TCK(cudaMemset(st->local, 0, st->lay.flags + (3 * kMaxP + 1) * sizeof(int)));
   TCK(cudaIpcGetMemHandle(&st->my_handle, st->local));
   TCK(cudaMalloc(&st->send_base, sizeof(int) * ctx->cfg.n_experts));
   TCK(cudaMalloc(&st->ticket, sizeof(int)));
@@ -242,6 +256,10 @@ void fsc_transport_finalize(fsc_ctx* ctx) {
   ctx->peer = nullptr;
 }
 
+static int* epoch_ptr(fsc_ctx* ctx) {
+  return reinterpret_cast<int*>(ctx->peer->local + ctx->peer->lay.flags) + kEpochSlot;
+}
+
 static bool connected(fsc_ctx* ctx) {
   for (int p = 0; p < ctx->ep; ++p)
     if (!ctx->peer->peers.base[p]) return false;
@@ -256,10 +274,9 @@ int fsc_transport_dispatch(fsc_ctx* ctx, int T, cudaStream_t s) {
     return FSC_ERR_STATE;
   }
   const fsc_moe_config& c = ctx->cfg;
-  st->epoch += 1;
   const int E = c.n_experts, P = ctx->ep;
   ++g_launches;
-  ep_counts_kernel<<<1, 256, 0, s>>>(st->peers, ctx->rank, P, E, ctx->e_loc, st->epoch, st->lay.cnt, ctx->counts,
+  ep_counts_kernel<<<1, 256, 0, s>>>(st->peers, ctx->rank, P, E, ctx->e_loc, epoch_ptr(ctx), st->lay.cnt, ctx->counts,
                                      st->send_base, ctx->recv_counts);
   TCK(cudaGetLastError());
   const int R = T * c.top_k;
@@ -267,7 +284,7 @@ int fsc_transport_dispatch(fsc_ctx* ctx, int T, cudaStream_t s) {
   if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
   if (blocks < 1) blocks = 1;
   ++g_launches;
-  ep_dispatch_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, P, R, c.d, E, ctx->e_loc, st->epoch, st->lay.xr,
+  ep_dispatch_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, P, R, c.d, E, ctx->e_loc, epoch_ptr(ctx), st->lay.xr,
                                             st->lay.ret, reinterpret_cast<const uint4*>(ctx->xn), ctx->src_row,
                                             ctx->offsets, st->send_base, st->ticket);
   TCK(cudaGetLastError());
@@ -276,7 +293,7 @@ int fsc_transport_dispatch(fsc_ctx* ctx, int T, cudaStream_t s) {
 
 int fsc_transport_dispatch_wait(fsc_ctx* ctx, cudaStream_t s) {
   ++g_launches;
-  ep_wait_kernel<<<1, 32, 0, s>>>(ctx->peer->local, FLAG_DISP, ctx->ep, ctx->peer->epoch);
+  ep_wait_kernel<<<1, 32, 0, s>>>(ctx->peer->local, FLAG_DISP, ctx->ep, epoch_ptr(ctx));
   TCK(cudaGetLastError());
   return FSC_OK;
 }
@@ -285,14 +302,14 @@ int fsc_transport_dispatch_wait(fsc_ctx* ctx, cudaStream_t s) {
 // this raises the per-source completion flags once that GEMM is done.
 int fsc_transport_combine(fsc_ctx* ctx, int, cudaStream_t s) {
   ++g_launches;
-  ep_signal_kernel<<<1, 32, 0, s>>>(ctx->peer->peers, ctx->rank, ctx->ep, FLAG_COMB, ctx->peer->epoch);
+  ep_signal_kernel<<<1, 32, 0, s>>>(ctx->peer->peers, ctx->rank, ctx->ep, FLAG_COMB, epoch_ptr(ctx));
   TCK(cudaGetLastError());
   return FSC_OK;
 }
 
 int fsc_transport_combine_wait(fsc_ctx* ctx, cudaStream_t s) {
   ++g_launches;
-  ep_wait_kernel<<<1, 32, 0, s>>>(ctx->peer->local, FLAG_COMB, ctx->ep, ctx->peer->epoch);
+  ep_wait_kernel<<<1, 32, 0, s>>>(ctx->peer->local, FLAG_COMB, ctx->ep, epoch_ptr(ctx));
   TCK(cudaGetLastError());
   return FSC_OK;
 }
