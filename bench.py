@@ -47,13 +47,24 @@ def load_peaks():
 
 
 def workload_config(shape, ep, n_gpus, schedule):
-    return {"workload": f"{shape.name}_moe_layer_prefill", "d": shape.d, "n_experts": shape.n_experts,
+    regime = "decode" if "_decode" in shape.name else "prefill"
+    return {"workload": f"{shape.name}_moe_layer" + ("" if regime == "decode" else "_prefill"), "regime": regime, "d": shape.d, "n_experts": shape.n_experts,
             "top_k": shape.top_k, "ffn": shape.ffn, "shared_ffn": shape.shared_ffn,
             "tokens_per_rank": shape.tokens, "global_tokens": shape.tokens * n_gpus, "ep": ep,
             "schedule": schedule, "parallelism": f"ep{ep}" + (f"-x{n_gpus // ep}replicas" if n_gpus > ep else ""),
             "l2": "flushed (256 MiB write) before every timed step; per-step working set > L2",
             "launch": "one CUDA-graph replay per step (captured fsc_moe_forward_blocking)",
             "data": "synthetic seeded N(0,1) tokens, random-init weights (SURVEY §8(d) recipe)"}
+
+
+def get_shape(name):
+    """BASELINE configs by name; '<base>_decode<T>' is configs[4] (decode regime)."""
+    if name in synth.CONFIGS:
+        return synth.CONFIGS[name]
+    if "_decode" in name:
+        base, t = name.split("_decode")
+        return synth.decode_shape(base, int(t))
+    raise SystemExit(f"unknown config {name}")
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -187,7 +198,7 @@ def run_gpu(args):
     from paper_2511_11505_b200 import Context
     from tests.gpu_util import moe_weights_dev
 
-    shape = synth.CONFIGS[args.config]
+    shape = get_shape(args.config)
     T = shape.tokens
     # EP = N when the experts shard evenly (C-amb-9), else independent EP=1 replicas
     ep = world if (world > 1 and shape.n_experts % world == 0) else 1
@@ -224,23 +235,32 @@ def run_gpu(args):
     # lists and flags), so one step is captured once and replayed as a CUDA graph
     use_graph = not args.no_graph
     launches_per_step = None
+    n_graphs = min(args.steps, 64)
     if use_graph:
-        graph = torch.cuda.CUDAGraph()
+        # one graph per timed step (cycled when K > 64), captured with the library's
+        # phase timing on: each graph carries its own event-record nodes, so every
+        # replay inside the timed region times its own kernels (roofline below)
+        graphs = []
+        ctx.set_timing_mask([] if args.no_live_timing else ["gemm1"])   # only the dominant kernel is bracketed
         lc0 = ctx.launch_count()
-        with torch.cuda.graph(graph):
-            eager_step()
-        launches_per_step = ctx.launch_count() - lc0
-        graph.replay()
+        for _ in range(n_graphs):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                eager_step()
+            graphs.append(g)
+        launches_per_step = (ctx.launch_count() - lc0) // n_graphs
+        for g in graphs:
+            g.replay()
         torch.cuda.synchronize(dev)
 
-    def step():
+    def step(i=0):
         if use_graph:
-            graph.replay()
+            graphs[i % n_graphs].replay()
         else:
             eager_step()
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(i)
     torch.cuda.synchronize(dev)
 
     # ---------------- timed region: K steps, per-step CUDA events on the launching stream
@@ -254,7 +274,7 @@ def run_gpu(args):
         for i in range(args.steps):
             flush.fill_(float(i))
             ev[i][0].record(stream)
-            step()
+            step(i)
             ev[i][1].record(stream)
         torch.cuda.synchronize(dev)
         wall = time.perf_counter() - wall0
@@ -269,15 +289,32 @@ def run_gpu(args):
     ms_per_step = total_ms / args.steps
     value = T * world * args.steps / (total_ms / 1e3)
 
-    # ---------------- per-phase breakdown (separate, untimed-for-value passes)
-    ctx.set_timing(True)
+    # ---------------- per-phase (per-kernel) times
     phase = {}
-    for _ in range(max(3, min(args.steps, 10))):
-        flush.fill_(0.0)
-        eager_step()
-        for kname, v in ctx.timings().items():
-            phase.setdefault(kname, []).append(v)
+    timed_log = ctx.timing_log(4096) if use_graph else []
     ctx.set_timing(False)
+    # breakdown of every phase: an instrumented graph (or eager step) replayed after the region
+    ctx.set_timing(True)
+    if use_graph:
+        g_all = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_all):
+            eager_step()
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.fill_(0.0)
+            g_all.replay()
+            torch.cuda.synchronize(dev)
+            for kname, v in ctx.timings().items():
+                phase.setdefault(kname, []).append(v)
+        del g_all
+    else:
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.fill_(0.0)
+            eager_step()
+            for kname, v in ctx.timings().items():
+                phase.setdefault(kname, []).append(v)
+    ctx.set_timing(False)
+    phase_src = "CUDA events, instrumented replays of the same step after the timed region"
+    gemm1_live = [v for kname, v in timed_log if kname == "gemm1"]
     phase_ms = {kname: statistics.median(v) for kname, v in phase.items()}
 
     # ---------------- e2e: host buffers through the C ABI, copies inside the region.
@@ -305,7 +342,7 @@ def run_gpu(args):
     e2e_sync_value = T * 3 / (time.perf_counter() - t0)
 
     stack = None
-    if args.stack_layers > 0:
+    if args.stack_layers > 0 and shape.tokens % shape.seq_len == 0:
         stack = stack_measure(ctx, shape, wd, x, args.stack_layers, max(3, min(args.steps, 8)), world, dev,
                               rank, args.seed)
 
@@ -316,38 +353,67 @@ def run_gpu(args):
         return
 
     peaks, src = load_peaks()
+    clocks = clk.summary()
+    # Denominator: the measured BURST bf16 peak (the conservative choice: the step is
+    # short and the clocks stay near max); the sustained-peak fraction is reported beside it.
+    throttled = bool(set(clocks.get("reasons") or []) & {"sw_power_cap", "hw_slowdown", "hw_thermal_slowdown",
+                                                           "sw_thermal_slowdown", "hw_power_brake"})
+    peak_key = "bf16_tflops"
+    peak = peaks["bf16_tflops"]
     # dominant kernel: routed-expert GEMM1 with the fused SwiGLU epilogue (row a7)
-    R = T * shape.top_k
-    g1_flop = 2.0 * R * shape.d * 2 * shape.ffn  # balanced routing: rows received per rank = T*k
-    g1_ms = phase_ms.get("gemm1")
-    achieved = g1_flop / (g1_ms * 1e-3) / 1e12 if g1_ms else None
-    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    R = T * shape.top_k                                        # balanced routing: rows received per rank = T*k
+    g1_flop = 2.0 * R * shape.d * 2 * shape.ffn
+    g1_bytes = 2.0 * e_loc * 2 * shape.ffn * shape.d + 2.0 * R * shape.d + 2.0 * R * shape.ffn  # W1|W2, xs, h
+    if gemm1_live:    # event-record nodes around GEMM1 in every replayed graph of the timed region
+        g1_ms = statistics.mean(gemm1_live)
+        g1_src = f"CUDA events around the kernel in each of the {len(gemm1_live)} graph replays of the timed region"
+    else:
+        g1_ms = statistics.median(phase["gemm1"]) if phase.get("gemm1") else None
+        g1_src = phase_src
+    t_tensor = g1_flop / (peak * 1e12)
+    t_hbm = g1_bytes / (peaks["hbm_gbs"] * 1e9)
+    bound = "tensor" if t_tensor >= t_hbm else "hbm"       # decode batches stream the expert weights
+    if bound == "tensor":
+        achieved = g1_flop / (g1_ms * 1e-3) / 1e12 if g1_ms else None
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "peak_source": f"{src} {peak_key} (burst; clocks in the timed region: "
+                               f"{clocks.get('sm_mhz')} MHz median" + (", throttle reasons seen)" if throttled else ")"),
+                "algorithmic_flop_per_launch": g1_flop}
+    else:
+        achieved = g1_bytes / (g1_ms * 1e-3) / 1e9 if g1_ms else None
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "peak_source": f"{src} hbm_gbs", "algorithmic_bytes_per_launch": g1_bytes}
+    roof["frac"] = (achieved / roof["peak"]) if achieved else None
+    roof["kernel"] = "grouped_gemm_kernel<256,SWIGLU,2> (routed GEMM1, row a7)"
+    roof["launch_ms"] = g1_ms
+    roof["timing"] = g1_src
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_gemm1_dsv2lite.json")
+    prof = os.path.join(ROOT, "profiles", f"ncu_gemm1_{shape.name}.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    roof["traffic"] = traffic
+    if bound == "tensor" and achieved:
+        roof["frac_of_sustained_peak"] = achieved / peaks.get("bf16_tflops_sustained", peak)
     exp_flop = 2.0 * R * shape.d * 3 * shape.ffn + 2.0 * T * shape.d * 3 * shape.shared_ffn
     a2a_bytes = 2.0 * 2 * R * shape.d * (ep - 1) / ep          # dispatch + combine bytes leaving a rank
-    layer_roof_ms = max(exp_flop / (peaks["bf16_tflops"] * 1e12), a2a_bytes / 770e9) * 1e3
+    w_bytes = 2.0 * 3 * shape.d * (e_loc * shape.ffn + shape.shared_ffn)
+    layer_roof_ms = max(exp_flop / (peaks["bf16_tflops"] * 1e12), a2a_bytes / 770e9,
+                        w_bytes / (peaks["hbm_gbs"] * 1e9)) * 1e3
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": workload_config(shape, ep, world, "blocking"),
-        "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel<256,SWIGLU> (routed GEMM1)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",
-                     "algorithmic_flop_per_launch": g1_flop,
-                     "frac_of_burst_peak": (achieved / peaks["bf16_tflops"]) if achieved else None},
+        "roofline": roof,
         "layer_roofline": {"expert_flop": exp_flop, "t_roof_ms": layer_roof_ms,
                            "a2a_bytes": a2a_bytes, "frac": layer_roof_ms / ms_per_step,
+                           "weight_bytes": w_bytes,
                            "note": "max(expert FLOPs / bf16 burst peak, a2a bytes / 770 GB/s measured NVLink "
-                                   "peer bandwidth); a2a = 0 at EP=1"},
-        "phase_ms": phase_ms,
+                                   "peer bandwidth, expert weight bytes / HBM); a2a = 0 at EP=1"},
+        "phase_ms": phase_ms, "phase_timing": phase_src,
         "exposed_a2a_us_per_layer": (stack or {}).get("exposed_a2a_us_per_layer",
                                                        {"farskip": None, "blocking": None}),
         "stack": stack,
@@ -358,7 +424,7 @@ def run_gpu(args):
                 "value_synchronous": e2e_sync_value},
         "gpu_launches": launches,
         "cuda_graph": use_graph, "ms_per_step_eager": eager_ms,
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "wall_s_timed_region": wall,
     }
     if not args.no_cpu_baseline:
@@ -440,7 +506,7 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    shape = synth.CONFIGS[args.config]
+    shape = get_shape(args.config)
     from threadpoolctl import threadpool_info
 
     from oracle import moe as om
@@ -476,13 +542,15 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="dsv2lite", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--config", default="dsv2lite",
+                    help=f"one of {sorted(synth.CONFIGS)} or <qwen3|scout>_decode<T> (configs[4])")
     ap.add_argument("--impl", default="fsc", choices=["fsc", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of a CUDA graph")
+    ap.add_argument("--no-live-timing", action="store_true", help="no CUDA events inside the timed graphs")
     ap.add_argument("--stack-layers", type=int, default=4, help="0 disables the FarSkip-vs-blocking stack timing")
     args = ap.parse_args()
     if args.warmup < 3:

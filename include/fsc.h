@@ -150,6 +150,10 @@ FSC_API int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg);
  * gemm2 (down), combine, shared1, shared2, unpermute, dispatch_stall, combine_wait.
  * Returns the phase count. */
 FSC_API int fsc_set_timing(fsc_ctx* ctx, int enable);
+/* As fsc_set_timing, timing only the phases whose bit (1u << phase id) is set in
+ * `mask` (0 disables timing). Used by the bench to time one kernel inside the
+ * timed region without instrumenting the rest of the step. */
+FSC_API int fsc_set_timing_mask(fsc_ctx* ctx, unsigned mask);
 FSC_API int fsc_get_timings(fsc_ctx* ctx, float* ms, int n);
 /* Every timed phase instance since fsc_set_timing (phase ids as above, then
  * 9 = dispatch stall of the compute stream, 10 = combine wait); waits for the

@@ -68,6 +68,7 @@ _SIGS = {
     "fsc_set_gemm_ctas": (_I, [_P, _I]),
     "fsc_set_gemm_cta_group": (_I, [_P, _I]),
     "fsc_set_timing": (_I, [_P, _I]),
+    "fsc_set_timing_mask": (_I, [_P, ctypes.c_uint]),
     "fsc_get_timings": (_I, [_P, ctypes.POINTER(ctypes.c_float), _I]),
     "fsc_launch_count": (ctypes.c_long, []),
     "fsc_timing_log": (_I, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_float), _I]),
@@ -206,6 +207,13 @@ class Context:
 
     def set_timing(self, enable: bool):
         self._ck(self.lib.fsc_set_timing(self.h, int(enable)))
+
+    def set_timing_mask(self, phases):
+        """Time only the named phases (see PHASES); [] disables timing."""
+        mask = 0
+        for n in phases:
+            mask |= 1 << self.PHASES.index(n)
+        self._ck(self.lib.fsc_set_timing_mask(self.h, mask))
 
     def timings(self) -> dict:
         """Per-phase ms of the last MoE call (phases not run are omitted)."""

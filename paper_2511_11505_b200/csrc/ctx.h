@@ -39,11 +39,8 @@ struct fsc_ctx {
   int* base = nullptr;         // [chunks, E]
   int* counts = nullptr;       // [E]                copies per global expert (this rank)
   int* offsets = nullptr;      // [E+1]
-  int* rf_list = nullptr;      // [T]                router near-tie list
-  int* rf_ctrl = nullptr;      // [2]                {count, ticket}
-  double* rf_l64 = nullptr;    // [T, E]             fp64 logits of flagged tokens
-  float* rf_lg = nullptr;      // [T, E]             fp32 logits of flagged tokens
-  float* rf_thr = nullptr;     // [T, 3]             band thresholds of flagged tokens
+  float* r_part = nullptr;     // [kRouterSplitRows, 128] split-d partial logits (small T)
+  double* r_part_sq = nullptr; // [kRouterSplitRows]      split-d partial sums of x^2
   float* w_scaled = nullptr;   // [E, d]             gamma * W_R
   float* w_sq = nullptr;       // [E]                ||gamma * W_R[e]||^2
   uint16_t* xs = nullptr;      // bf16 [T*k, d]      expert-sorted send buffer
@@ -82,6 +79,7 @@ struct fsc_ctx {
   float* rbuf[3] = {nullptr, nullptr, nullptr};  // fp32 [T, d] rotating residual buffers
   long stack_cap_qkv = 0, stack_cap_ao = 0;
   int timing = 0;
+  unsigned timing_mask = ~0u;   // bit i: time phase i
   cudaEvent_t ph_ev[PH_N][2] = {};
   int ph_used[PH_N] = {};
   // timing log: every phase instance since the last reset (bench: per-layer exposure)

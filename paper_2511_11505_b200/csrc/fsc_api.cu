@@ -45,17 +45,28 @@ namespace fsc {
 long g_launches = 0;
 }
 
+// Phase events are recorded with cudaEventRecordExternal so that, under stream
+// capture, they become event-record nodes of the graph: a replayed graph then
+// times its own phases (bench: per-kernel times inside the timed region).
+static cudaError_t ph_record(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(st, &cs);
+  if (e != cudaSuccess) return e;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
+                                             : cudaEventRecord(ev, st);
+}
+#define PH_REC(ev, st) CK(ph_record(ev, st))
 #define PH_BEGIN_ON(i, st)                                                         \
-  if (ctx->timing) {                                                               \
-    CK(cudaEventRecord(ctx->ph_ev[i][0], st));                                     \
-    if (ctx->log_n < kLogEvents / 2) CK(cudaEventRecord(ctx->log_ev[2 * ctx->log_n], st)); \
+  if (ctx->timing && ((ctx->timing_mask >> (i)) & 1u)) {                                                               \
+    PH_REC(ctx->ph_ev[i][0], st);                                                  \
+    if (ctx->log_n < kLogEvents / 2) PH_REC(ctx->log_ev[2 * ctx->log_n], st);      \
   }
 #define PH_END_ON(i, st)                                                           \
-  if (ctx->timing) {                                                               \
-    CK(cudaEventRecord(ctx->ph_ev[i][1], st));                                     \
+  if (ctx->timing && ((ctx->timing_mask >> (i)) & 1u)) {                                                               \
+    PH_REC(ctx->ph_ev[i][1], st);                                                  \
     ctx->ph_used[i] = 1;                                                           \
     if (ctx->log_n < kLogEvents / 2) {                                             \
-      CK(cudaEventRecord(ctx->log_ev[2 * ctx->log_n + 1], st));                    \
+      PH_REC(ctx->log_ev[2 * ctx->log_n + 1], st);                                 \
       ctx->log_phase[ctx->log_n++] = i;                                            \
     }                                                                              \
   }
@@ -117,14 +128,10 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(dalloc(&ctx->base, nch * E));
   CK(dalloc(&ctx->counts, E));
   CK(dalloc(&ctx->offsets, E + 1));
-  CK(dalloc(&ctx->rf_list, T));
-  CK(dalloc(&ctx->rf_ctrl, 2));
-  CK(dalloc(&ctx->rf_l64, T * E));
-  CK(dalloc(&ctx->rf_lg, T * E));
-  CK(dalloc(&ctx->rf_thr, T * 3));
+  CK(dalloc(&ctx->r_part, (long)kRouterSplitRows * 128));
+  CK(dalloc(&ctx->r_part_sq, (long)kRouterSplitRows));
   CK(dalloc(&ctx->w_scaled, (E > 128 ? E : 128) * d));  // e-major [E][d] or k-major [d][EP<=128]
   CK(dalloc(&ctx->w_sq, E));
-  CK(cudaMemset(ctx->rf_ctrl, 0, 2 * sizeof(int)));
   CK(dalloc(&ctx->xs, (T * k > ctx->max_recv ? T * k : ctx->max_recv) * d));
   CK(dalloc(&ctx->h, ctx->max_recv * (long)c.ffn));
   CK(dalloc(&ctx->y, (T * k > ctx->max_recv ? T * k : ctx->max_recv) * d));
@@ -159,7 +166,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->rf_lg, ctx->rf_thr, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -197,8 +204,16 @@ extern "C" int fsc_set_timing(fsc_ctx* ctx, int enable) {
     for (int i = 0; i < kLogEvents; ++i) CK(cudaEventCreate(&ctx->log_ev[i]));
   }
   ctx->timing = enable ? 1 : 0;
+  ctx->timing_mask = ~0u;
   ctx->log_n = 0;
   return FSC_OK;
+}
+
+extern "C" int fsc_set_timing_mask(fsc_ctx* ctx, unsigned mask) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  int rc = fsc_set_timing(ctx, mask != 0);
+  ctx->timing_mask = mask;
+  return rc;
 }
 
 extern "C" int fsc_get_timings(fsc_ctx* ctx, float* ms, int n) {
@@ -273,8 +288,8 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   const fsc_moe_config& c = ctx->cfg;
   const int d = c.d, E = c.n_experts, k = c.top_k;
   RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
-                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr, ctx->rf_list, ctx->rf_ctrl,
-                  ctx->rf_l64, ctx->rf_lg, ctx->rf_thr, ctx->w_scaled, ctx->w_sq};
+                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr,
+                  ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq};
   PH_BEGIN(PH_ROUTER);
   CK(launch_router(rl, s));
   PH_END(PH_ROUTER);
@@ -371,9 +386,11 @@ static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float
   const int d = c.d;
   if (c.shared_ffn == 0) {
     if (dbg && dbg->shared_out) CK(cudaMemsetAsync(dbg->shared_out, 0, sizeof(float) * T * (long)d, s));
-    PH_BEGIN(PH_SHARED2);
-    CK(launch_copy_f32(resid, out, (long)T * d, s));
-    PH_END(PH_SHARED2);
+    if (resid != out) {   // (never on the blocking / FarSkip paths: they pass resid == out or skip the call)
+      PH_BEGIN(PH_SHARED2);
+      CK(launch_copy_f32(resid, out, (long)T * d, s));
+      PH_END(PH_SHARED2);
+    }
     return FSC_OK;
   }
   GemmLaunch g1{};
@@ -429,6 +446,13 @@ extern "C" int fsc_moe_forward_blocking(fsc_ctx* ctx, const fsc_moe_weights* w, 
   memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
   // Regular order (C-amb-12): tmp = x_in + shared; out = tmp + routed. The shared
   // expert overlaps the permutation (EP = 1) or follows the routed experts (EP > 1).
+  if (ctx->cfg.shared_ffn == 0) {   // no shared expert: out = x_in + routed, straight from x_in
+    rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false);
+    if (rc) return rc;
+    rc = moe_shared(ctx, w, T, x_in, const_cast<float*>(x_in), dbg, s);   // debug shared_out = 0 only
+    if (rc) return rc;
+    return moe_finish(ctx, T, x_in, out, dbg, s);
+  }
   rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false, x_in, ctx->tmp);
   if (rc) return rc;
   return moe_finish(ctx, T, ctx->tmp, out, dbg, s);
@@ -548,7 +572,7 @@ extern "C" int fsc_op_router(fsc_ctx* ctx, const float* x, const float* gamma, c
   REQUIRE(T >= 0 && T <= ctx->cfg.max_tokens && E <= ctx->cfg.n_experts && d <= ctx->cfg.d, FSC_ERR_CONFIG,
           "router shape beyond the context workspace");
   RouterLaunch rl{x, gamma, w_router, T, d, E, k, ctx->cfg.rms_eps, static_cast<uint16_t*>(xn), topk_idx, topk_w,
-                  logits, n_refined, ctx->rf_list, ctx->rf_ctrl, ctx->rf_l64, ctx->rf_lg, ctx->rf_thr, ctx->w_scaled, ctx->w_sq};
+                  logits, n_refined, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq};
   CK(launch_router(rl, static_cast<cudaStream_t>(stream)));
   return FSC_OK;
 }

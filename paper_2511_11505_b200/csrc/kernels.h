@@ -62,16 +62,15 @@ struct RouterLaunch {
   int* topk_idx;         // [T, k]
   float* topk_w;         // [T, k]
   float* logits;         // optional [T, E]
-  int* n_refined;        // optional device counter
-  int* rf_list;          // workspace [T]: tokens flagged for fp64 refinement
-  int* rf_ctrl;          // workspace [2]: {count, done-ticket}, zero between calls
-  double* rf_l64;        // workspace [T, E]: fp64 raw dots of band experts of flagged tokens
-  float* rf_lg;          // workspace [T, E]: fp32 logits of flagged tokens
-  float* rf_thr;         // workspace [T, 3]: {2B, l_(k), l_(k+1)} of flagged tokens
+  int* n_refined;        // optional device counter of tokens refined in fp64
+  float* part;           // workspace [kRouterSplitRows, 128]: split-d raw partial logits (small T)
+  double* part_sq;       // workspace [kRouterSplitRows]: split-d partial sums of x^2
   float* w_scaled;       // workspace [E, d]: gamma * W_R
   float* w_sq;           // workspace [E]: ||gamma * W_R[e]||^2
   int rpb = 32;          // tokens per CTA (set by launch_router)
 };
+// split-d partials: (token blocks) x (d splits) <= 2 x 148 CTAs of <= 32 rows
+constexpr int kRouterSplitRows = 2 * 148 * 32;
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s);
 
 // K2: deterministic histogram / scan / positions

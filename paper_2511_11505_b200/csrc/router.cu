@@ -11,16 +11,18 @@
 // rounding of the accumulation chain, Cauchy-Schwarz). With t_hi / t_lo the k-th /
 // (k+1)-th largest fp32 logits, an expert with v > t_hi + 2B is certainly selected
 // and one with v < t_lo - 2B certainly not; only the experts in between ("the
-// band", usually 2-3) of tokens with t_hi - t_lo <= 2B are recomputed in fp64
-// (router_refine_kernel) and the missing slots filled by their fp64 order. The
+// band", usually 2-3) of tokens with t_hi - t_lo <= 2B are recomputed in fp64 by
+// the same CTA (refine_block) and the missing slots filled by their fp64 order. The
 // selection therefore equals the fp64 selection of the oracle for every token.
 //
-// Main kernel (E > 32): block = 32 tokens x 64/128 experts, 8 warps; each warp
+// Main kernel: block = 32 tokens x 32/64/128 (padded) experts, 8 warps; each warp
 // owns one k-slice of every 64-wide chunk (k-split, summed in a fixed order at the
-// end) and an 8 tokens x 8 experts register tile per lane; operands are staged by a
-// 3-4 deep cp.async pipeline, read with conflict-free LDS.64 (128 FMA per shared
-// memory wavefront, the binding resource of an fp32 SIMT contraction on sm_100).
-// sum x^2 is accumulated from the staged chunks (no extra pass over x).
+// end) and an 8 tokens x 8 (or 4) experts register tile per lane; operands are
+// staged by a 2-4 deep cp.async pipeline, read with conflict-free LDS.64 (128 FMA
+// per shared-memory wavefront, the binding resource of an fp32 SIMT contraction on
+// sm_100). sum x^2 is accumulated from the staged chunks (no extra pass over x).
+// Small T (decode): the grid also splits d (gridDim.y), raw partials go to a
+// workspace and router_finish_kernel sums them in a fixed order and selects.
 #include <float.h>
 
 #include "common.cuh"
@@ -34,6 +36,9 @@ constexpr int DC = 64;      // k per staged chunk
 constexpr int LDS = DC + 4; // padded smem row (floats): rows r, r+1 start 4 banks apart
 constexpr float kU = 5.9604645e-08f;  // 2^-24
 constexpr int kMaxD = 8192;
+constexpr int kThreadSelK1 = 9;
+constexpr int kMaxSplit = 8;
+constexpr int kFinishRows = 8;  // thread-per-token selection for k <= 8
 
 FSC_DEVINL uint32_t ordered_f32(float v) {
   uint32_t u = __float_as_uint(v);
@@ -70,6 +75,14 @@ FSC_DEVINL void cp_async16(void* smem, const void* gmem, bool valid) {
 FSC_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 FSC_DEVINL void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// Per-CTA state of the in-block band refinement (see refine_block).
+struct RefineSmem {
+  int flag[TB];          // token of the block has an ambiguous top-k boundary
+  float thr[TB][3];      // {2B + 4u(|l_(k)| + |l_(k+1)|), l_(k), l_(k+1)} of flagged tokens
+  int band[128];
+  int nb;
+  double l64[128];
+};
 }  // namespace
 
 // W'[e][i] = gamma_i * W_R[e][i] and ||W'_e||^2 (error bound). One CTA per expert.
@@ -126,7 +139,8 @@ FSC_DEVINL void ffma2_bcast(float2& acc, float a, float2 b) {
 // Phase C for one token (one warp): top-k over the fp32 logits of row `lg`, gates,
 // or hand-off of the token to the band refinement when its boundary is ambiguous.
 template <int QN>
-FSC_DEVINL void select_token(const float* lg, long t, float B, const RouterLaunch& L, int lane) {
+FSC_DEVINL void select_token(const float* lg, long t, int tt, float B, const RouterLaunch& L, RefineSmem& rs,
+                             int lane) {
   const int E = L.E, k = L.k;
   float v[QN];
 #pragma unroll
@@ -168,19 +182,14 @@ FSC_DEVINL void select_token(const float* lg, long t, float B, const RouterLaunc
     }
   }
   const float thr2 = 2.f * B + 4.f * kU * (fabsf(vk) + fabsf(vk1)) + 1e-7f;
-  if (k < E && vk - vk1 <= thr2) {
-    // ambiguous boundary: record the token, its fp32 row and thresholds for router_refine_kernel
-    int slot = 0;
+  if (k < E && vk - vk1 <= thr2) {   // ambiguous boundary: refined by the block (refine_block)
     if (lane == 0) {
       if (L.n_refined) atomicAdd(L.n_refined, 1);
-      slot = atomicAdd(&L.rf_ctrl[0], 1);
-      L.rf_list[slot] = (int)t;
-      L.rf_thr[3 * slot] = thr2;
-      L.rf_thr[3 * slot + 1] = vk;
-      L.rf_thr[3 * slot + 2] = vk1;
+      rs.flag[tt] = 1;
+      rs.thr[tt][0] = thr2;
+      rs.thr[tt][1] = vk;
+      rs.thr[tt][2] = vk1;
     }
-    slot = __shfl_sync(0xffffffff, slot, 0);
-    for (int e = lane; e < E; e += 32) L.rf_lg[(long)slot * E + e] = lg[e];
     return;
   }
   float ex[QN], sum = 0.f;
@@ -200,6 +209,91 @@ FSC_DEVINL void select_token(const float* lg, long t, float B, const RouterLaunc
       L.topk_w[t * k + s] = ex[q] / sum;
     }
     slot += __popc(m);
+  }
+}
+
+// Phase C, one THREAD per token (k < K1): the top-(k+1) of the row by insertion
+// over the E logits in ascending expert order (strict '>' keeps the lower id on
+// exact ties), then the boundary test, gates and ascending-id slots exactly as in
+// select_token. A warp selects 32 tokens at once with no shuffles (the warp
+// version above is latency-bound on k+1 rounds of 64-bit shuffle argmax).
+template <int K1>   // K1 = k + 1 (compile time: every register array index is static)
+FSC_DEVINL void select_token_thread(const float* lg, long t, int tt, float B, const RouterLaunch& L,
+                                    RefineSmem& rs) {
+  constexpr int k = K1 - 1;
+  const int E = L.E;
+  float val[K1];
+  int idx[K1];
+#pragma unroll
+  for (int j = 0; j < K1; ++j) {
+    val[j] = -FLT_MAX;
+    idx[j] = 0x7fffffff;
+  }
+  // the row (16-byte aligned, E <= padded width, a multiple of 16) is read 16
+  // logits at a time with independent LDS.128: one shared-memory latency per 16
+  // insertions instead of one per logit (the MIO queue is busy with the xn warps)
+  for (int e0 = 0; e0 < E; e0 += 16) {
+    float vv[16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 q = *reinterpret_cast<const float4*>(lg + e0 + 4 * u);
+      vv[4 * u] = q.x;
+      vv[4 * u + 1] = q.y;
+      vv[4 * u + 2] = q.z;
+      vv[4 * u + 3] = q.w;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = e0 + u;
+      const float v = e < E ? vv[u] : -FLT_MAX;
+      if (v > val[K1 - 1]) {
+        bool gt[K1];
+#pragma unroll
+        for (int j = 0; j < K1; ++j) gt[j] = v > val[j];
+#pragma unroll
+        for (int j = K1 - 1; j >= 1; --j) {
+          if (gt[j]) {
+            val[j] = gt[j - 1] ? val[j - 1] : v;
+            idx[j] = gt[j - 1] ? idx[j - 1] : e;
+          }
+        }
+        if (gt[0]) {
+          val[0] = v;
+          idx[0] = e;
+        }
+      }
+    }
+  }
+#ifndef FSC_ROUTER_PROF
+  if (L.logits)
+    for (int e = 0; e < E; ++e) L.logits[t * E + e] = lg[e];
+#endif
+  const float vk = val[k - 1], vk1 = k < E ? val[k] : -FLT_MAX;
+  const float thr2 = 2.f * B + 4.f * kU * (fabsf(vk) + fabsf(vk1)) + 1e-7f;
+  if (k < E && vk - vk1 <= thr2) {   // ambiguous boundary: refined by the block (refine_block)
+    if (L.n_refined) atomicAdd(L.n_refined, 1);
+    rs.flag[tt] = 1;
+    rs.thr[tt][0] = thr2;
+    rs.thr[tt][1] = vk;
+    rs.thr[tt][2] = vk1;
+    return;
+  }
+  const float vtop = val[0];
+  float ex[K1], sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < K1; ++j) {
+    ex[j] = j < k ? expf(val[j] - vtop) : 0.f;
+    sum += ex[j];
+  }
+#pragma unroll
+  for (int j = 0; j < K1; ++j) {
+    if (j < k) {
+      int rank = 0;
+#pragma unroll
+      for (int i = 0; i < K1; ++i) rank += (i < k && idx[i] < idx[j]) ? 1 : 0;
+      L.topk_idx[t * k + rank] = idx[j];
+      L.topk_w[t * k + rank] = ex[j] / sum;
+    }
   }
 }
 
@@ -245,273 +339,23 @@ FSC_DEVINL void write_xn(const RouterLaunch& L, long t0, int rows, const float* 
 #define RSTAMP(kk)
 #endif
 
-// E in (32, 128]: 8 warps = KS k-groups x NEH expert halves of 64. Each lane owns
-// 8 tokens (lt + 4i) x 4 expert pairs (2 le + 16 j + {0,1}); x is staged token-major,
-// W' k-major, so one LDS.64 yields an expert pair at one k and every product is an
-// FFMA2 with the token value broadcast (full fp32 issue rate on sm_100).
-template <int EW>
-__global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
-  constexpr int EP = 32 * EW;          // padded experts: 64 or 128
-  constexpr int NEH = EP / 64;         // 64-expert halves
-  constexpr int KS = 8 / NEH;          // k-groups (warps sharing a chunk)
-  constexpr int KW = DC / KS;          // k per warp per chunk (8 or 16)
-  constexpr int NT = 256;
-  constexpr int XV = TB * DC / 4 / NT; // float4 of the x chunk per thread (2)
-  constexpr int WV = EP * DC / 4 / NT; // float4 of the W' chunk per thread (4 / 8)
-  constexpr int XBUF = TB * LDS;       // x chunk, token-major [TB][LDS]
-  constexpr int BUF = XBUF + DC * EP;  // + W' chunk, k-major [DC][EP]
-  constexpr int NS = EW >= 4 ? 3 : 4;  // cp.async pipeline depth
-  extern __shared__ __align__(16) float sm[];
-  float* stage0 = sm;                  // [NS][BUF]
-  float* red = sm;                     // [KS][TB][EP] k-group partials (after the loop)
-  float* lg = sm + KS * TB * EP;       // [TB][EP+1] fp32 logits
-  float* s_r = sm + NS * BUF;          // [TB]
-  float* s_xn = s_r + TB;              // [TB] ||x_t||
-  float* s_wsq = s_xn + TB;            // [EP]
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int d = L.d, E = L.E;
-  const long t0 = (long)blockIdx.x * L.rpb;    // rpb <= TB rows per block (balanced grid)
-  const int rows = (int)min((long)L.rpb, (long)L.T - t0);
-  const long T = t0 + rows;                    // rows >= T are padding
-  const float* __restrict__ x = L.x;
-  const float* __restrict__ WT = L.w_scaled;   // [d][EP]
-  RSTAMP(0);
-  auto issue_chunk = [&](int c0, float* buf) {
-#pragma unroll
-    for (int v = 0; v < XV; ++v) {
-      const int i = tid + v * NT;
-      const int tt = i / (DC / 4), cc = (i % (DC / 4)) * 4;
-      const long t = t0 + tt;
-      cp_async16(buf + tt * LDS + cc, x + (t < T ? t : 0) * d + c0 + cc, t < T);
-    }
-#pragma unroll
-    for (int v = 0; v < WV; ++v) {
-      const int i = tid + v * NT;       // float4 index inside the [DC][EP] chunk
-      cp_async16(buf + XBUF + 4 * i, WT + (long)c0 * EP + 4 * i, true);
-    }
-    cp_async_commit();
-  };
-  const int nch = d / DC;
-#pragma unroll
-  for (int i = 0; i < NS - 1; ++i) {
-    if (i < nch) issue_chunk(i * DC, stage0 + i * BUF);
-    else cp_async_commit();
-  }
-  for (int e = tid; e < EP; e += NT) s_wsq[e] = e < E ? L.w_sq[e] : 0.f;
-
-  const int eh = warp % NEH, ks = warp / NEH, lt = lane >> 3, le = lane & 7;
-  float2 acc[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
-  double ssp = 0.0;                     // partial sum x^2 of row tid/8 (8 values per chunk)
-  const int srow = tid >> 3, scol = (tid & 7) * 8;
-
-  for (int it = 0; it < nch; ++it) {
-    const float* buf = stage0 + (it % NS) * BUF;
-    cp_async_wait<NS - 2>();
-    __syncthreads();
-    if (it + NS - 1 < nch) issue_chunk((it + NS - 1) * DC, stage0 + ((it + NS - 1) % NS) * BUF);
-    else cp_async_commit();
-    {
-      const float4 p = *reinterpret_cast<const float4*>(buf + srow * LDS + scol);
-      const float4 q = *reinterpret_cast<const float4*>(buf + srow * LDS + scol + 4);
-      ssp += ((double)p.x * p.x + (double)p.y * p.y) + ((double)p.z * p.z + (double)p.w * p.w) +
-             ((double)q.x * q.x + (double)q.y * q.y) + ((double)q.z * q.z + (double)q.w * q.w);
-    }
-    const float* xa = buf + lt * LDS + ks * KW;
-    const float* wb = buf + XBUF + (ks * KW) * EP + eh * 64 + 2 * le;
-#pragma unroll
-    for (int kk = 0; kk < KW; kk += 2) {
-      float2 a[8], b0[4], b1[4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float2*>(xa + 4 * i * LDS + kk);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        b0[j] = *reinterpret_cast<const float2*>(wb + kk * EP + 16 * j);
-        b1[j] = *reinterpret_cast<const float2*>(wb + (kk + 1) * EP + 16 * j);
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          ffma2_bcast(acc[i][j], a[i].x, b0[j]);
-          ffma2_bcast(acc[i][j], a[i].y, b1[j]);
-        }
-    }
-  }
-  __syncthreads();                       // stages free: reuse for the k-group partials
-  RSTAMP(1);
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      *reinterpret_cast<float2*>(&red[(ks * TB + lt + 4 * i) * EP + eh * 64 + 2 * le + 16 * j]) = acc[i][j];
-  // per-row sum x^2: the 8 threads of a row are consecutive lanes
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) ssp += __shfl_xor_sync(0xffffffff, ssp, o);
-  if ((tid & 7) == 0) {
-    s_r[srow] = (float)(1.0 / sqrt(ssp / (double)d + (double)L.eps));
-    s_xn[srow] = (float)sqrt(ssp) * 1.0001f;
-  }
-  __syncthreads();
-  for (int i = tid; i < TB * EP; i += NT) {   // k-groups summed in a fixed order
-    const int tt = i / EP, e = i % EP;
-    float s = red[tt * EP + e];
-#pragma unroll
-    for (int g = 1; g < KS; ++g) s += red[(g * TB + tt) * EP + e];
-    lg[tt * (EP + 1) + e] = s * s_r[tt];
-  }
-  __syncthreads();
-  RSTAMP(2);
-  float wm = 0.f;
-  for (int e = lane; e < E; e += 32) wm = fmaxf(wm, s_wsq[e]);
-  const float wmax = sqrtf(warp_max_f32(wm)) * 1.01f;
-  const float chain = (float)(d / KS + KS + 6);
-  if (warp < 4) {            // warps 0-3 select while warps 4-7 write xn
-    for (int tt = warp; tt < rows; tt += 4)
-      select_token<EW>(lg + tt * (EP + 1), t0 + tt, s_r[tt] * chain * kU * s_xn[tt] * wmax, L, lane);
-  } else {
-    write_xn(L, t0, rows, s_r, tid - 128, 128);
-  }
-  RSTAMP(3);
-  __syncthreads();
-  RSTAMP(4);
-}
-
-// E <= 32: 4 warps, 4x4 tile per lane (tokens lt + 4i + 16 wt, experts le + 8j), k split in halves.
-__global__ void __launch_bounds__(128) router_kernel_small(RouterLaunch L) {
-  constexpr int EP = 32, NT = 128, XV = TB * DC / 4 / NT, WV = EP * DC / 4 / NT;
-  constexpr int BUF = (TB + EP) * LDS, NS = 4;
-  extern __shared__ __align__(16) float sm[];
-  float* stage0 = sm;
-  float* lg = sm;                      // [TB][EP+1]
-  float* red = sm + TB * (EP + 1);     // [TB][EP]
-  float* s_r = sm + NS * BUF;
-  float* s_xn = s_r + TB;
-  float* s_wsq = s_xn + TB;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int T = L.T, d = L.d, E = L.E;
-  const long t0 = (long)blockIdx.x * TB;
-  const float* __restrict__ x = L.x;
-  const float* __restrict__ W = L.w_scaled;
-  auto issue_chunk = [&](int c0, float* buf) {
-#pragma unroll
-    for (int v = 0; v < XV; ++v) {
-      const int i = tid + v * NT;
-      const int tt = i / (DC / 4), cc = (i % (DC / 4)) * 4;
-      const long t = t0 + tt;
-      cp_async16(buf + tt * LDS + cc, x + (t < T ? t : 0) * d + c0 + cc, t < T);
-    }
-#pragma unroll
-    for (int v = 0; v < WV; ++v) {
-      const int i = tid + v * NT;
-      const int e = i / (DC / 4), cc = (i % (DC / 4)) * 4;
-      cp_async16(buf + (TB + e) * LDS + cc, W + (long)(e < E ? e : 0) * d + c0 + cc, e < E);
-    }
-    cp_async_commit();
-  };
-  const int nch = d / DC;
-#pragma unroll
-  for (int i = 0; i < NS - 1; ++i) {
-    if (i < nch) issue_chunk(i * DC, stage0 + i * BUF);
-    else cp_async_commit();
-  }
-  for (int e = tid; e < EP; e += NT) s_wsq[e] = e < E ? L.w_sq[e] : 0.f;
-  const int kg = warp >> 1, wt = warp & 1, lt = lane >> 3, le = lane & 7;
-  float acc[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  double ssp = 0.0;
-  const int srow = tid >> 2, scol = (tid & 3) * 16;
-  for (int it = 0; it < nch; ++it) {
-    const float* buf = stage0 + (it % NS) * BUF;
-    cp_async_wait<NS - 2>();
-    __syncthreads();
-    if (it + NS - 1 < nch) issue_chunk((it + NS - 1) * DC, stage0 + ((it + NS - 1) % NS) * BUF);
-    else cp_async_commit();
-#pragma unroll
-    for (int c = 0; c < 16; c += 4) {
-      const float4 p = *reinterpret_cast<const float4*>(buf + srow * LDS + scol + c);
-      ssp += ((double)p.x * p.x + (double)p.y * p.y) + ((double)p.z * p.z + (double)p.w * p.w);
-    }
-    const float* xa = buf + (16 * wt + lt) * LDS + kg * (DC / 2);
-    const float* wb = buf + (TB + le) * LDS + kg * (DC / 2);
-#pragma unroll
-    for (int kk = 0; kk < DC / 2; kk += 2) {
-      float2 a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float2*>(xa + 4 * i * LDS + kk);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const float2*>(wb + 8 * j * LDS + kk);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc[i][j] = fmaf(a[i].x, b[j].x, acc[i][j]);
-          acc[i][j] = fmaf(a[i].y, b[j].y, acc[i][j]);
-        }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int o = 2; o > 0; o >>= 1) ssp += __shfl_xor_sync(0xffffffff, ssp, o);
-  if ((tid & 3) == 0) {
-    s_r[srow] = (float)(1.0 / sqrt(ssp / (double)d + (double)L.eps));
-    s_xn[srow] = (float)sqrt(ssp) * 1.0001f;
-  }
-  if (kg == 1) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) red[(16 * wt + lt + 4 * i) * EP + le + 8 * j] = acc[i][j];
-  }
-  __syncthreads();
-  if (kg == 0) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int tt = 16 * wt + lt + 4 * i;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        lg[tt * (EP + 1) + le + 8 * j] = (acc[i][j] + red[tt * EP + le + 8 * j]) * s_r[tt];
-    }
-  }
-  __syncthreads();
-  float wm = 0.f;
-  for (int e = lane; e < E; e += 32) wm = fmaxf(wm, s_wsq[e]);
-  const float wmax = sqrtf(warp_max_f32(wm)) * 1.01f;
-  const float chain = (float)(d / 2 + 8);
-  for (int tt = warp; tt < TB; tt += 4) {
-    const long t = t0 + tt;
-    if (t >= T) break;
-    select_token<1>(lg + tt * (EP + 1), t, s_r[tt] * chain * kU * s_xn[tt] * wmax, L, lane);
-  }
-  write_xn(L, t0, (int)min((long)TB, (long)T - t0), s_r, tid, NT);
-}
-
-// Band refinement (one CTA per flagged token, grid-stride): warp 0 classifies the
-// experts against the token's fp32 band (certainly in / band / certainly out);
-// the 8 warps compute the fp64 raw dots sum_i x_i gamma_i W_ei of the band experts
-// (the positive factor r_t does not change their order); warp 0 then fills the
-// k - |certain| open slots with the best band experts (fp64 value, ties -> lower
-// id) and writes indices and gates (fp32 logits, as for every other token). The
-// last CTA resets the flag list for the next call.
+// Band refinement of the block's flagged tokens, by the whole CTA (after the
+// selection, so the fp32 logits rows are in shared memory). For each flagged token:
+// warp 0 classifies the experts against the token's fp32 band (certainly in / band /
+// certainly out); the 8 warps compute the fp64 raw dots sum_i x_i gamma_i W_ei of
+// the band experts, one warp per expert (the positive factor r_t does not change
+// their order; x_i gamma_i is exact in fp64); warp 0 fills the k - |certain| open
+// slots with the best band experts (fp64 value, ties -> lower id) and writes the
+// indices and gates (from the fp32 logits, as for every other token).
 template <int QN>
-__global__ void __launch_bounds__(256) router_refine_kernel(RouterLaunch L) {
-  __shared__ int s_band[128];
-  __shared__ int s_nb;
-  __shared__ double s_l64[128];
-  __shared__ double s_red[8];
+FSC_DEVINL void refine_block(const RouterLaunch& L, const float* lg, int lgs, RefineSmem& rs, long t0, int rows) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int d = L.d, E = L.E, k = L.k;
-  const int n = *reinterpret_cast<volatile int*>(&L.rf_ctrl[0]);
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
-    const long t = L.rf_list[i];
-    const float thr2 = L.rf_thr[3 * i], hi = L.rf_thr[3 * i + 1], lo = L.rf_thr[3 * i + 2];
+  for (int tt = 0; tt < rows; ++tt) {
+    if (!rs.flag[tt]) continue;                  // block-uniform
+    const long t = t0 + tt;
+    const float* row = lg + tt * lgs;
+    const float thr2 = rs.thr[tt][0], hi = rs.thr[tt][1], lo = rs.thr[tt][2];
     float v[QN];
     uint32_t sel = 0, band = 0;
     if (warp == 0) {
@@ -519,49 +363,51 @@ __global__ void __launch_bounds__(256) router_refine_kernel(RouterLaunch L) {
 #pragma unroll
       for (int q = 0; q < QN; ++q) {
         const int e = lane + 32 * q;
-        v[q] = e < E ? L.rf_lg[(long)i * E + e] : -FLT_MAX;
+        v[q] = e < E ? row[e] : -FLT_MAX;
         const bool in = e < E && v[q] > hi + thr2;
         const bool bnd = e < E && !in && !(v[q] < lo - thr2);
         if (in) sel |= 1u << q;
         if (bnd) band |= 1u << q;
         const uint32_t m = __ballot_sync(0xffffffff, bnd);
-        if (bnd) s_band[nb + __popc(m & ((1u << lane) - 1u))] = e;
+        if (bnd) rs.band[nb + __popc(m & ((1u << lane) - 1u))] = e;
         nb += __popc(m);
       }
-      if (lane == 0) s_nb = nb;
+      if (lane == 0) rs.nb = nb;
     }
     __syncthreads();
-    const int nb = s_nb;
-    const float* xr = L.x + t * d;
-    for (int b = 0; b < nb; ++b) {            // all 256 threads on one band expert at a time
-      const int e = s_band[b];
-      const float* wr = L.w_router + (long)e * d;
-      double acc[8];
+    const int nb = rs.nb;
+    const float4* x4 = reinterpret_cast<const float4*>(L.x + t * d);
+    const float4* g4 = reinterpret_cast<const float4*>(L.gamma);
+    for (int b = warp; b < nb; b += 8) {
+      const int e = rs.band[b];
+      const float4* w4 = reinterpret_cast<const float4*>(L.w_router + (long)e * d);
+      double a0 = 0.0, a1 = 0.0;
+      for (int c0 = lane; c0 < d / 4; c0 += 128) {   // 4 float4 of each operand in flight
+        float4 xv[4], gv[4], wv[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-      for (int c0 = 0; c0 < d; c0 += 2048) {
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + 32 * u;
+          const bool ok = c < d / 4;
+          xv[u] = ok ? x4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+          gv[u] = ok ? g4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+          wv[u] = ok ? w4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = c0 + tid + 256 * u;
-          if (c < d) acc[u] = fma((double)xr[c] * (double)L.gamma[c], (double)wr[c], acc[u]);
+        for (int u = 0; u < 4; ++u) {
+          a0 = fma((double)xv[u].x * (double)gv[u].x, (double)wv[u].x, a0);
+          a1 = fma((double)xv[u].y * (double)gv[u].y, (double)wv[u].y, a1);
+          a0 = fma((double)xv[u].z * (double)gv[u].z, (double)wv[u].z, a0);
+          a1 = fma((double)xv[u].w * (double)gv[u].w, (double)wv[u].w, a1);
         }
       }
-      double sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      sum = warp_sum_f64(sum);
-      if (lane == 0) s_red[warp] = sum;
-      __syncthreads();
-      if (tid == 0) {
-        double tot = 0.0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) tot += s_red[w];
-        s_l64[e] = tot;
-      }
-      __syncthreads();
+      const double sum = warp_sum_f64(a0 + a1);
+      if (lane == 0) rs.l64[e] = sum;
     }
+    __syncthreads();
     if (warp == 0) {
       double l64[QN];
 #pragma unroll
-      for (int q = 0; q < QN; ++q) l64[q] = ((band >> q) & 1u) ? s_l64[lane + 32 * q] : -DBL_MAX;
+      for (int q = 0; q < QN; ++q) l64[q] = ((band >> q) & 1u) ? rs.l64[lane + 32 * q] : -DBL_MAX;
       int nsel = 0;
 #pragma unroll
       for (int q = 0; q < QN; ++q) nsel += __popc(__ballot_sync(0xffffffff, (sel >> q) & 1u));
@@ -608,64 +454,289 @@ __global__ void __launch_bounds__(256) router_refine_kernel(RouterLaunch L) {
         slot += __popc(m);
       }
     }
-    __syncthreads();
   }
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(&L.rf_ctrl[1], 1) == (int)gridDim.x - 1) {
-      L.rf_ctrl[0] = 0;
-      L.rf_ctrl[1] = 0;
-      __threadfence();
+}
+
+// Epilogue of one block of <= 32 tokens whose fp32 logits lg[tt][e] (row stride
+// 32*EW + 4) and RMS factors are in shared memory: warp 0 selects (one thread per
+// token) while warps 1-7 write xn; for k > 8 warps 0-3 select (one warp per token)
+// and warps 4-7 write xn. Then the CTA refines the flagged tokens in fp64.
+// `chain` bounds the rounding chain of every logit. rs.flag must be zero on entry.
+template <int EW>
+FSC_DEVINL void router_select_and_xn(const RouterLaunch& L, const float* lg, const float* s_r, const float* s_xn,
+                                     const float* s_wsq, RefineSmem& rs, long t0, int rows, float chain) {
+  constexpr int LGS = 32 * EW + 4, NT = 256;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float wm = 0.f;
+  for (int e = lane; e < L.E; e += 32) wm = fmaxf(wm, s_wsq[e]);
+  const float wmax = sqrtf(warp_max_f32(wm)) * 1.01f;
+  if (L.k < kThreadSelK1) {
+    if (warp == 0) {
+      if (lane < rows) {
+        const float* row = lg + lane * LGS;
+        const float B = s_r[lane] * chain * kU * s_xn[lane] * wmax;
+        const long t = t0 + lane;
+        switch (L.k) {
+          case 1: select_token_thread<2>(row, t, lane, B, L, rs); break;
+          case 2: select_token_thread<3>(row, t, lane, B, L, rs); break;
+          case 3: select_token_thread<4>(row, t, lane, B, L, rs); break;
+          case 4: select_token_thread<5>(row, t, lane, B, L, rs); break;
+          case 5: select_token_thread<6>(row, t, lane, B, L, rs); break;
+          case 6: select_token_thread<7>(row, t, lane, B, L, rs); break;
+          case 7: select_token_thread<8>(row, t, lane, B, L, rs); break;
+          default: select_token_thread<9>(row, t, lane, B, L, rs); break;
+        }
+      }
+    } else {
+      write_xn(L, t0, rows, s_r, tid - 32, NT - 32);
+    }
+  } else if (warp < 4) {
+    for (int tt = warp; tt < rows; tt += 4)
+      select_token<EW>(lg + tt * LGS, t0 + tt, tt, s_r[tt] * chain * kU * s_xn[tt] * wmax, L, rs, lane);
+  } else {
+    write_xn(L, t0, rows, s_r, tid - 128, 128);
+  }
+  __syncthreads();
+  refine_block<EW>(L, lg, LGS, rs, t0, rows);
+}
+
+// Main kernel: 8 warps = KS k-groups x NEH expert halves of 64 (E <= 64 is padded
+// to 64 with zero W' columns, masked in the selection). Each lane owns 8 tokens
+// (lt + 4i) x 4 expert pairs (2 le + 16 j + {0,1}); x is staged token-major, W'
+// k-major, so one LDS.64 yields an expert pair at one k and every product is an
+// FFMA2 with the token value broadcast (full fp32 issue rate on sm_100).
+// gridDim.y = nsplit > 1 (small T, decode): block (x, y) covers the y-th 1/nsplit of
+// d and writes raw partial dots + partial sum x^2 to L.part / L.part_sq;
+// router_finish_kernel sums the splits in a fixed order and selects.
+template <int EW>
+__global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
+  constexpr int EP = 32 * EW;          // padded experts: 32, 64 or 128
+  constexpr int NEH = EP >= 64 ? EP / 64 : 1;   // 64-expert halves
+  constexpr int NJ = EP >= 64 ? 4 : EP / 16;    // expert pairs per lane (2 le + 16 j)
+  constexpr int KS = 8 / NEH;          // k-groups (warps sharing a chunk)
+  constexpr int KW = DC / KS;          // k per warp per chunk (8 or 16)
+  constexpr int NT = 256;
+  constexpr int XV = TB * DC / 4 / NT; // float4 of the x chunk per thread (2)
+  constexpr int WV = EP * DC / 4 / NT; // float4 of the W' chunk per thread (2 / 4 / 8)
+  constexpr int XBUF = TB * LDS;       // x chunk, token-major [TB][LDS]
+  constexpr int BUF = XBUF + DC * EP;  // + W' chunk, k-major [DC][EP]
+  constexpr int NS = EW >= 4 ? 2 : 4;  // cp.async pipeline depth (E=128: 2 stages -> 2 CTAs/SM)
+  constexpr int LGS = EP + 4;          // logits row stride: float4 rows, conflict-free LDS.128 across rows
+  static_assert(KS * TB * EP + TB * LGS <= NS * BUF, "partials + logits must fit in the stages");
+  extern __shared__ __align__(16) float sm[];
+  float* stage0 = sm;                  // [NS][BUF]
+  float* red = sm;                     // [KS][TB][EP] k-group partials (after the loop)
+  float* lg = sm + KS * TB * EP;       // [TB][LGS] fp32 logits (16-byte rows)
+  float* s_r = sm + NS * BUF;          // [TB]
+  float* s_xn = s_r + TB;              // [TB] ||x_t||
+  float* s_wsq = s_xn + TB;            // [EP]
+  __shared__ RefineSmem rs;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int d = L.d;
+  if (tid < TB) rs.flag[tid] = 0;
+  const long t0 = (long)blockIdx.x * L.rpb;    // rpb <= TB rows per block (balanced grid)
+  const int rows = (int)min((long)L.rpb, (long)L.T - t0);
+  const long T = t0 + rows;                    // rows >= T are padding
+  const int nsplit = gridDim.y, split = blockIdx.y;
+  const int nch_all = d / DC;
+  const int ch0 = split * nch_all / nsplit, nch = (split + 1) * nch_all / nsplit - ch0;
+  const float* __restrict__ x = L.x;
+  const float* __restrict__ WT = L.w_scaled;   // [d][EP]
+  RSTAMP(0);
+  auto issue_chunk = [&](int c0, float* buf) {
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+      const int i = tid + v * NT;
+      const int tt = i / (DC / 4), cc = (i % (DC / 4)) * 4;
+      const long t = t0 + tt;
+      cp_async16(buf + tt * LDS + cc, x + (t < T ? t : 0) * d + c0 + cc, t < T);
+    }
+#pragma unroll
+    for (int v = 0; v < WV; ++v) {
+      const int i = tid + v * NT;       // float4 index inside the [DC][EP] chunk
+      cp_async16(buf + XBUF + 4 * i, WT + (long)c0 * EP + 4 * i, true);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int i = 0; i < NS - 1; ++i) {
+    if (i < nch) issue_chunk((ch0 + i) * DC, stage0 + i * BUF);
+    else cp_async_commit();
+  }
+  if (nsplit == 1)
+    for (int e = tid; e < EP; e += NT) s_wsq[e] = e < L.E ? L.w_sq[e] : 0.f;
+
+  const int eh = warp % NEH, ks = warp / NEH, lt = lane >> 3, le = lane & 7;
+  float2 acc[8][NJ];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  double ssp = 0.0;                     // partial sum x^2 of row tid/8 (8 values per chunk)
+  const int srow = tid >> 3, scol = (tid & 7) * 8;
+
+  for (int it = 0; it < nch; ++it) {
+    const float* buf = stage0 + (it % NS) * BUF;
+    cp_async_wait<NS - 2>();
+    __syncthreads();
+    if (it + NS - 1 < nch) issue_chunk((ch0 + it + NS - 1) * DC, stage0 + ((it + NS - 1) % NS) * BUF);
+    else cp_async_commit();
+    {
+      const float4 p = *reinterpret_cast<const float4*>(buf + srow * LDS + scol);
+      const float4 q = *reinterpret_cast<const float4*>(buf + srow * LDS + scol + 4);
+      ssp += ((double)p.x * p.x + (double)p.y * p.y) + ((double)p.z * p.z + (double)p.w * p.w) +
+             ((double)q.x * q.x + (double)q.y * q.y) + ((double)q.z * q.z + (double)q.w * q.w);
+    }
+    const float* xa = buf + lt * LDS + ks * KW;
+    const float* wb = buf + XBUF + (ks * KW) * EP + eh * 64 + 2 * le;
+#pragma unroll
+    for (int kk = 0; kk < KW; kk += 2) {
+      float2 a[8], b0[NJ], b1[NJ];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float2*>(xa + 4 * i * LDS + kk);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        b0[j] = *reinterpret_cast<const float2*>(wb + kk * EP + 16 * j);
+        b1[j] = *reinterpret_cast<const float2*>(wb + (kk + 1) * EP + 16 * j);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          ffma2_bcast(acc[i][j], a[i].x, b0[j]);
+          ffma2_bcast(acc[i][j], a[i].y, b1[j]);
+        }
     }
   }
+  __syncthreads();                       // stages free: reuse for the k-group partials
+  RSTAMP(1);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+      *reinterpret_cast<float2*>(&red[(ks * TB + lt + 4 * i) * EP + eh * 64 + 2 * le + 16 * j]) = acc[i][j];
+  // per-row sum x^2: the 8 threads of a row are consecutive lanes
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) ssp += __shfl_xor_sync(0xffffffff, ssp, o);
+  if (nsplit > 1) {                      // raw partials of this d-split (the finish kernel selects)
+    if ((tid & 7) == 0 && srow < rows) L.part_sq[(long)split * L.T + t0 + srow] = ssp;
+    __syncthreads();
+    for (int i = tid; i < rows * EP; i += NT) {
+      const int tt = i / EP, e = i % EP;
+      float s = red[tt * EP + e];
+#pragma unroll
+      for (int g = 1; g < KS; ++g) s += red[(g * TB + tt) * EP + e];
+      L.part[((long)split * L.T + t0 + tt) * EP + e] = s;
+    }
+    return;
+  }
+  if ((tid & 7) == 0) {
+    s_r[srow] = (float)(1.0 / sqrt(ssp / (double)d + (double)L.eps));
+    s_xn[srow] = (float)sqrt(ssp) * 1.0001f;
+  }
+  __syncthreads();
+  for (int i = tid; i < TB * EP; i += NT) {   // k-groups summed in a fixed order
+    const int tt = i / EP, e = i % EP;
+    float s = red[tt * EP + e];
+#pragma unroll
+    for (int g = 1; g < KS; ++g) s += red[(g * TB + tt) * EP + e];
+    lg[tt * LGS + e] = s * s_r[tt];
+  }
+  __syncthreads();
+  RSTAMP(2);
+  router_select_and_xn<EW>(L, lg, s_r, s_xn, s_wsq, rs, t0, rows, (float)(d / KS + KS + 6));
+  RSTAMP(3);
+  __syncthreads();
+  RSTAMP(4);
+}
+
+// Split-d finish: logit = r * (sum over splits, in split order, of the raw partials),
+// r from the split partial sums of x^2 (fp64, split order); then the same selection
+// and xn write as the single-pass kernel. Rounding chain: d/(nsplit KS) + KS + nsplit.
+template <int EW>
+__global__ void __launch_bounds__(256) router_finish_kernel(RouterLaunch L, int nsplit, float chain) {
+  constexpr int EP = 32 * EW, LGS = EP + 4, NT = 256;
+  __shared__ __align__(16) float lg[TB * LGS];
+  __shared__ float s_r[TB], s_xn[TB], s_wsq[EP];
+  __shared__ RefineSmem rs;
+  const int tid = threadIdx.x;
+  if (tid < TB) rs.flag[tid] = 0;
+  const long t0 = (long)blockIdx.x * L.rpb;
+  const int rows = (int)min((long)L.rpb, (long)L.T - t0);
+  for (int e = tid; e < EP; e += NT) s_wsq[e] = e < L.E ? L.w_sq[e] : 0.f;
+  if (tid < rows) {
+    double ssp = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) ssp += L.part_sq[(long)sp * L.T + t0 + tid];
+    s_r[tid] = (float)(1.0 / sqrt(ssp / (double)L.d + (double)L.eps));
+    s_xn[tid] = (float)sqrt(ssp) * 1.0001f;
+  }
+  __syncthreads();
+  for (int i = tid; i < rows * EP; i += NT) {
+    const int tt = i / EP, e = i % EP;
+    const float* pp = L.part + (t0 + tt) * EP + e;
+    float v[kMaxSplit];
+#pragma unroll
+    for (int sp = 0; sp < kMaxSplit; ++sp) v[sp] = sp < nsplit ? pp[(long)sp * L.T * EP] : 0.f;
+    float sacc = v[0];
+#pragma unroll
+    for (int sp = 1; sp < kMaxSplit; ++sp)
+      if (sp < nsplit) sacc += v[sp];
+    lg[tt * LGS + e] = sacc * s_r[tt];
+  }
+  __syncthreads();
+  router_select_and_xn<EW>(L, lg, s_r, s_xn, s_wsq, rs, t0, rows, chain);
 }
 
 template <int EW>
 static cudaError_t launch_router_t(const RouterLaunch& L, cudaStream_t s) {
+  constexpr int EP = 32 * EW, NS = EW >= 4 ? 2 : 4, NEH = EP >= 64 ? EP / 64 : 1, KS = 8 / NEH;
   RouterLaunch LL = L;
-  LL.rpb = TB;
-  if constexpr (EW > 1) {   // balance the grid: exactly 2 CTAs per SM when T is large
-    const int want = 2 * kNumSMs;
-    LL.rpb = (L.T + want - 1) / want;
+  const int slots = 2 * kNumSMs;                     // two CTAs per SM
+  int nsplit = 1;
+  const int nblk32 = (L.T + TB - 1) / TB;
+  if (nblk32 < kNumSMs) {                            // small T (decode): split d across CTAs
+    nsplit = slots / nblk32;
+    if (nsplit > kMaxSplit) nsplit = kMaxSplit;       // finish-kernel traffic: nsplit x T x E partials
+    if (nsplit > L.d / DC) nsplit = L.d / DC;
+    if (nsplit < 1) nsplit = 1;
+  }
+  if (nsplit > 1) {
+    LL.rpb = TB;
+  } else {                                           // balance the grid: whole waves of 2 CTAs per SM
+    const int waves = (L.T + slots * TB - 1) / (slots * TB);
+    LL.rpb = (L.T + slots * waves - 1) / (slots * waves);
     if (LL.rpb > TB) LL.rpb = TB;
     if (LL.rpb < 1) LL.rpb = 1;
   }
   const int grid = (L.T + LL.rpb - 1) / LL.rpb;
-  g_launches += 3;
-  constexpr int EPAD = 32 * EW;
-  router_prescale_kernel<<<EW == 1 ? L.E : EPAD, 256, 0, s>>>(L.w_router, L.gamma, L.w_scaled, L.w_sq, L.E, L.d,
-                                                              EW == 1 ? 0 : EPAD);
-  if constexpr (EW == 1) {
-    constexpr int NS = 4, EP = 32;
-    const size_t smem = (size_t)(NS * (TB + EP) * LDS + 2 * TB + EP) * 4 + 16;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(router_kernel_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    router_kernel_small<<<grid, 128, smem, s>>>(LL);
-  } else {
-    constexpr int EP = 32 * EW, NS = EW >= 4 ? 3 : 4;
-    const size_t smem = (size_t)(NS * (TB * LDS + DC * EP) + 2 * TB + EP) * 4 + 16;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(router_kernel<EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    router_kernel<EW><<<grid, 256, smem, s>>>(LL);
+  if (nsplit > 1 && (long)nsplit * L.T > kRouterSplitRows) return cudaErrorInvalidValue;
+  router_prescale_kernel<<<EP, 256, 0, s>>>(L.w_router, L.gamma, L.w_scaled, L.w_sq, L.E, L.d, EP);
+  const size_t smem = (size_t)(NS * (TB * LDS + DC * EP) + 2 * TB + EP) * 4 + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(router_kernel<EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
   }
-  router_refine_kernel<EW><<<kNumSMs, 256, 0, s>>>(L);
+  router_kernel<EW><<<dim3(grid, nsplit), 256, smem, s>>>(LL);
+  g_launches += 2;
+  if (nsplit > 1) {   // 8 tokens per finish CTA: more CTAs in flight for the latency-bound epilogue
+    const float chain = (float)(L.d / (nsplit * KS) + KS + nsplit + 6);
+    RouterLaunch LF = LL;
+    LF.rpb = kFinishRows;
+    router_finish_kernel<EW><<<(L.T + kFinishRows - 1) / kFinishRows, 256, 0, s>>>(LF, nsplit, chain);
+    ++g_launches;
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s) {
   if (L.T == 0) return cudaSuccess;
   if (L.d % DC || L.d > kMaxD || L.E < 1 || L.E > 128 || L.k < 1 || L.k > L.E) return cudaErrorInvalidValue;
-  if (!L.rf_list || !L.rf_ctrl || !L.rf_l64 || !L.rf_lg || !L.rf_thr || !L.w_scaled || !L.w_sq)
+  if (!L.part || !L.part_sq || !L.w_scaled || !L.w_sq)
     return cudaErrorInvalidValue;
-  if (L.E <= 32) return launch_router_t<1>(L, s);
+  if (L.E <= 32) return launch_router_t<1>(L, s);   // padded to 32 / 64 / 128 (zero W' columns)
   if (L.E <= 64) return launch_router_t<2>(L, s);
   return launch_router_t<4>(L, s);
 }

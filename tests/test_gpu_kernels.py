@@ -16,7 +16,7 @@ def ctx():
     from paper_2511_11505_b200 import build
     build.build()
     from paper_2511_11505_b200 import Context
-    c = Context(d=5120, n_experts=128, top_k=8, ffn=1408, shared_ffn=0, max_tokens=4096)
+    c = Context(d=5120, n_experts=128, top_k=8, ffn=1408, shared_ffn=0, max_tokens=8192)
     yield c
     c.close()
 
@@ -123,7 +123,10 @@ def test_gemm_inplace_resid(ctx, cg):
 
 
 # ----------------------------------------------------------------------------- K1 router
-ROUTER_CASES = [("tiny", 32), ("tiny", 1), ("dsv2lite", 700), ("qwen3", 513), ("scout", 256)]
+# T < 148*32 tokens run the split-d path (partials over d, fixed-order finish kernel);
+# larger T the single-pass kernel with balanced waves (two CTAs per SM)
+ROUTER_CASES = [("tiny", 32), ("tiny", 1), ("dsv2lite", 700), ("qwen3", 513), ("scout", 256), ("dsv2lite", 64),
+                ("qwen3", 2400), ("dsv2lite", 4800), ("qwen3", 6000), ("scout", 5000)]
 
 
 @pytest.mark.parametrize("name,T", ROUTER_CASES)

@@ -53,3 +53,30 @@ for cg in (2, 1):
     bench("square 8192^3 bf16", 0, 8192, 1, 8192, 8192, cg=cg, iters=5)
     bench("qwen3 gemm1 (EP1)", 1, 1024, 128, 768, 2048, cg=cg)
     bench("scout gemm1 (EP8-ish)", 1, 4096, 2, 8192, 5120, cg=cg)
+
+
+def cublas(name, M, N, K, iters=10):
+    """Dense cuBLAS (torch.matmul) bf16 with the same total M, N, K: the library ceiling."""
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = (torch.randn(K, N, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    for _ in range(3):
+        torch.matmul(A, B)
+    ts = []
+    for _ in range(iters):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        torch.matmul(A, B)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    t = sorted(ts)[len(ts) // 2]
+    print(f"cuBLAS {name:27s}      M={M:6d} N={N:5d} K={K:5d}      : {t*1e3:8.1f} us  {2.0*M*N*K/t/1e9:7.1f} TF/s",
+          flush=True)
+
+
+cublas("DS gemm1 (dense equiv)", 49152, 2816, 2048)
+cublas("DS gemm2 (dense equiv)", 49152, 2048, 1408)
+cublas("DS shared1", 8192, 5632, 2048)
+cublas("DS shared2", 8192, 2048, 2816)
+cublas("square 8192^3", 8192, 8192, 8192, iters=5)
