@@ -142,6 +142,15 @@ FSC_API int fsc_set_gemm_ctas(fsc_ctx* ctx, int n);
 /* Grouped-GEMM tile mode: 2 (default) = CTA pairs with tcgen05 cta_group::2,
  * 256-row tiles; 1 = single-CTA 128-row tiles. Results are identical. */
 FSC_API int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg);
+/* EP = 1: on != 0 fuses the permute into GEMM1 (its TMA producer gathers the rows of
+ * xn through src_row with tile::gather4) instead of the explicit permute kernel.
+ * Same results bit for bit; default off (slower on the measured shapes). */
+FSC_API int fsc_set_gemm_gather(fsc_ctx* ctx, int on);
+/* Blocking schedule, EP = 1: on > 0 fuses the gate-weighted unpermute into the down
+ * GEMM's epilogue (the k-th arriving copy of a token finishes it; k <= 8), on == 0
+ * runs the separate unpermute kernel, on < 0 (default) fuses for top-1 routing only.
+ * Bitwise the same result either way. */
+FSC_API int fsc_set_fused_unpermute(fsc_ctx* ctx, int on);
 
 /* Per-phase CUDA-event timing of the MoE calls (bench / profiling). When enabled,
  * events are recorded on the call's stream around every phase; fsc_get_timings
@@ -250,6 +259,13 @@ FSC_API int fsc_op_permute(fsc_ctx* ctx, const void* xn, const int* src_row, voi
  *   epi 2: out fp32 [M, N] = resid + A B0_g^T (resid may be NULL -> 0, may alias out) */
 FSC_API int fsc_op_grouped_gemm(fsc_ctx* ctx, int epi, const void* A, long a_rows, const void* B0, const void* B1, int G,
                         const int* counts, int m_total, int N, int K, void* out, const float* resid, void* stream);
+/* K4 with the A operand gathered (EP = 1 fused permute, "requiring
+ * permutation of A"): row r of the grouped problem is row a_idx[r] of A [a_rows, K]
+ * (int32 a_idx [sum of counts], device), loaded by TMA gather4 inside the GEMM;
+ * otherwise as fsc_op_grouped_gemm. a_idx == NULL is fsc_op_grouped_gemm. */
+FSC_API int fsc_op_grouped_gemm_gather(fsc_ctx* ctx, int epi, const void* A, long a_rows, const int* a_idx,
+                                       const void* B0, const void* B1, int G, const int* counts, int m_total, int N,
+                                       int K, void* out, const float* resid, void* stream);
 /* K5: out fp32 [T,d] = resid + sum_j w[t,j] y[pos[t,j]] (resid may be NULL -> 0). */
 FSC_API int fsc_op_unpermute(fsc_ctx* ctx, const void* y, const int* pos, const float* w, const float* resid, float* out,
                      int T, int k, int d, void* stream);

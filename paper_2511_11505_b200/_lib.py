@@ -67,6 +67,8 @@ _SIGS = {
     "fsc_last_error": (ctypes.c_char_p, [_P]),
     "fsc_set_gemm_ctas": (_I, [_P, _I]),
     "fsc_set_gemm_cta_group": (_I, [_P, _I]),
+    "fsc_set_gemm_gather": (_I, [_P, _I]),
+    "fsc_set_fused_unpermute": (_I, [_P, _I]),
     "fsc_set_timing": (_I, [_P, _I]),
     "fsc_set_timing_mask": (_I, [_P, ctypes.c_uint]),
     "fsc_get_timings": (_I, [_P, ctypes.POINTER(ctypes.c_float), _I]),
@@ -85,6 +87,7 @@ _SIGS = {
     "fsc_op_perm_maps": (_I, [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P]),
     "fsc_op_permute": (_I, [_P, _P, _P, _P, _I, _I, _P]),
     "fsc_op_grouped_gemm": (_I, [_P, _I, _P, _L, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
+    "fsc_op_grouped_gemm_gather": (_I, [_P, _I, _P, _L, _P, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "fsc_op_unpermute": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),
 }
 
@@ -238,6 +241,15 @@ class Context:
     def set_gemm_cta_group(self, cg: int):
         self._ck(self.lib.fsc_set_gemm_cta_group(self.h, cg))
 
+    def set_gemm_gather(self, on: bool):
+        """EP = 1: fuse the permute into GEMM1 (TMA gather4 of the xn rows)."""
+        self._ck(self.lib.fsc_set_gemm_gather(self.h, int(on)))
+
+    def set_fused_unpermute(self, on):
+        """Blocking EP = 1: gate-weighted unpermute fused into the down GEMM epilogue
+        (True / False; None = auto: top-1 routing only)."""
+        self._ck(self.lib.fsc_set_fused_unpermute(self.h, -1 if on is None else int(on)))
+
     def set_gemm_ctas(self, n: int):
         self._ck(self.lib.fsc_set_gemm_ctas(self.h, n))
 
@@ -313,6 +325,12 @@ class Context:
         self._ck(self.lib.fsc_op_grouped_gemm(self.h, epi, ptr(A), A.shape[0], ptr(B0), ptr(B1), G, ptr(counts),
                                               m_total, N, K, ptr(out), ptr(resid),
                                               stream if stream is not None else cur_stream()))
+
+    def op_grouped_gemm_gather(self, epi, A, a_idx, B0, B1, G, counts, m_total, N, K, out, resid=None, stream=None):
+        """Row r of the grouped problem reads A[a_idx[r]] (TMA gather4 in the GEMM producer)."""
+        self._ck(self.lib.fsc_op_grouped_gemm_gather(self.h, epi, ptr(A), A.shape[0], ptr(a_idx), ptr(B0), ptr(B1), G,
+                                                     ptr(counts), m_total, N, K, ptr(out), ptr(resid),
+                                                     stream if stream is not None else cur_stream()))
 
     def op_unpermute(self, y, pos, w, resid, out, stream=None):
         T, k = pos.shape

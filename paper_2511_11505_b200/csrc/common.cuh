@@ -177,6 +177,28 @@ FSC_DEVINL void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* m, uint64_t* 
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "l"(cache_hint)
       : "memory");
 }
+// TMA gather4: rows r0..r3 (each one box of 64 bf16 columns from column c0) of a
+// 2-D map with a {64, 1} box land as 4 consecutive 128-byte rows at smem_dst (the
+// 128B swizzle follows the smem address, as for a 4-row tile box). CG = 2: bytes
+// accounted on the leader CTA's barrier like tma_load_2d_2sm.
+template <int CG>
+FSC_DEVINL void tma_gather4(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c0, int r0, int r1, int r2,
+                            int r3, uint64_t cache_hint) {
+  if (CG == 2)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(r0), "r"(r1), "r"(r2),
+        "r"(r3), "l"(cache_hint)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "l"(cache_hint)
+        : "memory");
+}
 FSC_DEVINL void umma_bf16_ss_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                  uint32_t accumulate) {
   asm volatile(

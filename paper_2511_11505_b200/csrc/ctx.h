@@ -26,6 +26,8 @@ struct fsc_ctx {
   long max_recv = 0;
   int gemm_ctas = 148;
   int gemm_cg = 2;
+  int fuse_unpermute = -1;     // blocking EP = 1: unpermute fused into GEMM2 (-1 auto: top-1)
+  int gather_a = 0;            // EP = 1: GEMM1 gathers A through src_row (fused permute)
   int sticky = 0;
   char err[512] = {0};
 
@@ -39,6 +41,7 @@ struct fsc_ctx {
   int* base = nullptr;         // [chunks, E]
   int* counts = nullptr;       // [E]                copies per global expert (this rank)
   int* offsets = nullptr;      // [E+1]
+  int* comb_cnt = nullptr;     // [T, d/32]         fused-unpermute arrival counters
   float* r_part = nullptr;     // [kRouterSplitRows, 128] split-d partial logits (small T)
   double* r_part_sq = nullptr; // [kRouterSplitRows]      split-d partial sums of x^2
   float* w_scaled = nullptr;   // [E, d]             gamma * W_R

@@ -128,6 +128,8 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(dalloc(&ctx->base, nch * E));
   CK(dalloc(&ctx->counts, E));
   CK(dalloc(&ctx->offsets, E + 1));
+  CK(dalloc(&ctx->comb_cnt, T * (d / 32)));   // [T, d / (BN/2)] fused-unpermute counters, BN/2 >= 32
+  CK(cudaMemset(ctx->comb_cnt, 0, sizeof(int) * T * (d / 32)));
   CK(dalloc(&ctx->r_part, (long)kRouterSplitRows * 128));
   CK(dalloc(&ctx->r_part_sq, (long)kRouterSplitRows));
   CK(dalloc(&ctx->w_scaled, (E > 128 ? E : 128) * d));  // e-major [E][d] or k-major [d][EP<=128]
@@ -166,7 +168,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -249,6 +251,18 @@ extern "C" int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg) {
   return FSC_OK;
 }
 
+extern "C" int fsc_set_fused_unpermute(fsc_ctx* ctx, int on) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  ctx->fuse_unpermute = on < 0 ? -1 : (on ? 1 : 0);
+  return FSC_OK;
+}
+
+extern "C" int fsc_set_gemm_gather(fsc_ctx* ctx, int on) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  ctx->gather_a = on ? 1 : 0;
+  return FSC_OK;
+}
+
 extern "C" int fsc_set_gemm_ctas(fsc_ctx* ctx, int n) {
   if (!ctx) return FSC_ERR_SHAPE;
   REQUIRE(n >= 1 && n <= kNumSMs, FSC_ERR_CONFIG, "gemm ctas %d outside [1,148]", n);
@@ -282,9 +296,12 @@ static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float
 // shared_resid != nullptr (blocking schedule, EP = 1): the shared expert
 // (out = shared_resid + shared) runs on the compute stream right after the router
 // while the permutation maps and the permute run beside it on the aux stream.
+// fused_out != nullptr (blocking, EP = 1): GEMM2's epilogue also performs the
+// gate-weighted unpermute, fused_out = fused_resid + routed (bitwise the unpermute kernel).
 static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in,
                                  const fsc_moe_debug* dbg, cudaStream_t s, fsc_overlap_cb cb, void* user,
-                                 bool overlap, const float* shared_resid = nullptr, float* shared_out = nullptr) {
+                                 bool overlap, const float* shared_resid = nullptr, float* shared_out = nullptr,
+                                 float* fused_out = nullptr, const float* fused_resid = nullptr) {
   const fsc_moe_config& c = ctx->cfg;
   const int d = c.d, E = c.n_experts, k = c.top_k;
   RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
@@ -312,7 +329,24 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   long recv_rows = R;
   const int* recv_counts = ctx->counts;
   cudaStream_t cs = overlap ? ctx->comm : s;
-  if (ctx->ep == 1) {
+  const int* a_idx = nullptr;
+  if (ctx->ep == 1 && ctx->gather_a) {
+    // EP = 1 with fsc_set_gemm_gather(ctx, 1): no dispatch copy; the permutation is
+    // fused into GEMM1's operand load, whose producer gathers the expert-sorted rows of
+    // xn through src_row (TMA gather4, only the valid rows of each tile). Off by
+    // default: measured slower than the explicit permute at prefill AND decode sizes
+    // (4 rows per TMA instruction cannot keep the 256-row MMA tile fed).
+    recv = ctx->xn;
+    recv_rows = T;
+    a_idx = ctx->src_row;
+    if (early_shared) {
+      CK(cudaEventRecord(ctx->ev_d, ps));
+      int rc = moe_shared(ctx, w, T, shared_resid, shared_out, dbg, s);   // beside the permutation maps
+      if (rc) return rc;
+      CK(cudaStreamWaitEvent(s, ctx->ev_d, 0));
+    }
+  } else if (ctx->ep == 1) {
+    // EP = 1: explicit permute into the expert-sorted send buffer (full-bandwidth SM copy)
     PH_BEGIN_ON(PH_DISPATCH, ps);
     CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, ps));
     PH_END_ON(PH_DISPATCH, ps);
@@ -355,14 +389,19 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   g1.A = recv; g1.a_rows = recv_rows; g1.B0 = w->w1; g1.B1 = w->w2; g1.b_rows = (long)ctx->e_loc * c.ffn;
   g1.b_group_rows = c.ffn; g1.K = d; g1.N = c.ffn; g1.G = ctx->e_loc; g1.counts = recv_counts; g1.m_total = 0;
   g1.out = ctx->h; g1.ldo = c.ffn; g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas; g1.cta_group = ctx->gemm_cg;
+  g1.a_idx = a_idx;
   PH_BEGIN(PH_GEMM1);
   CK(launch_grouped_gemm(g1, s));
   PH_END(PH_GEMM1);
   GemmLaunch g2{};
-  g2.A = ctx->h; g2.a_rows = recv_rows; g2.B0 = w->w3; g2.B1 = nullptr; g2.b_rows = (long)ctx->e_loc * d;
+  g2.A = ctx->h; g2.a_rows = a_idx ? (long)R : recv_rows; g2.B0 = w->w3; g2.B1 = nullptr; g2.b_rows = (long)ctx->e_loc * d;
   g2.b_group_rows = d; g2.K = c.ffn; g2.N = d; g2.G = ctx->e_loc; g2.counts = recv_counts; g2.m_total = 0;
   g2.out = ctx->y; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = ctx->gemm_cg;
   if (ctx->ep > 1) fsc_transport_scatter_target(ctx, &g2.ret, g2.peer_out);  // P:100 Combine, fused
+  if (fused_out && ctx->ep == 1) {   // P:100 "sum the routed experts", fused into the down GEMM
+    g2.comb_out = fused_out; g2.comb_resid = fused_resid; g2.src_row = ctx->src_row; g2.pos = ctx->pos;
+    g2.topk_w = ctx->topk_w; g2.comb_cnt = ctx->comb_cnt; g2.top_k = k;
+  }
   PH_BEGIN(PH_GEMM2);
   CK(launch_grouped_gemm(g2, s));
   PH_END(PH_GEMM2);
@@ -415,7 +454,8 @@ static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float
 }
 
 // Gate-weighted unpermute (+ far-skip residual add), after the combine landed.
-static int moe_finish(fsc_ctx* ctx, int T, const float* resid, float* out, const fsc_moe_debug* dbg, cudaStream_t s) {
+static int moe_finish(fsc_ctx* ctx, int T, const float* resid, float* out, const fsc_moe_debug* dbg, cudaStream_t s,
+                      bool fused = false) {
   const fsc_moe_config& c = ctx->cfg;
   const uint16_t* ysrc = ctx->y;
   if (ctx->ep > 1) {
@@ -425,9 +465,11 @@ static int moe_finish(fsc_ctx* ctx, int T, const float* resid, float* out, const
     PH_END(PH_COMBINE_WAIT);
     ysrc = ctx->ys;
   }
-  PH_BEGIN(PH_UNPERMUTE);
-  CK(launch_unpermute(ysrc, ctx->pos, ctx->topk_w, resid, out, T, c.top_k, c.d, s));
-  PH_END(PH_UNPERMUTE);
+  if (!fused) {   // (fused: done by GEMM2's epilogue)
+    PH_BEGIN(PH_UNPERMUTE);
+    CK(launch_unpermute(ysrc, ctx->pos, ctx->topk_w, resid, out, T, c.top_k, c.d, s));
+    PH_END(PH_UNPERMUTE);
+  }
   if (dbg && dbg->routed_out)
     CK(launch_unpermute(ysrc, ctx->pos, ctx->topk_w, nullptr, dbg->routed_out, T, c.top_k, c.d, s));
   return FSC_OK;
@@ -446,16 +488,22 @@ extern "C" int fsc_moe_forward_blocking(fsc_ctx* ctx, const fsc_moe_weights* w, 
   memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
   // Regular order (C-amb-12): tmp = x_in + shared; out = tmp + routed. The shared
   // expert overlaps the permutation (EP = 1) or follows the routed experts (EP > 1).
+  // fused unpermute: auto (-1) = top-1 routing only (measured: at k = 6 / 8 the per-tile
+  // counter + cooperative finish costs the down GEMM more than the separate kernel)
+  const int fu = ctx->fuse_unpermute < 0 ? (ctx->cfg.top_k == 1) : ctx->fuse_unpermute;
+  const bool fuse = ctx->ep == 1 && fu && ctx->cfg.top_k <= 8;   // (the epilogue holds <= 8 slots)
   if (ctx->cfg.shared_ffn == 0) {   // no shared expert: out = x_in + routed, straight from x_in
-    rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false);
+    rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false, nullptr, nullptr,
+                               fuse ? out : nullptr, x_in);
     if (rc) return rc;
     rc = moe_shared(ctx, w, T, x_in, const_cast<float*>(x_in), dbg, s);   // debug shared_out = 0 only
     if (rc) return rc;
-    return moe_finish(ctx, T, x_in, out, dbg, s);
+    return moe_finish(ctx, T, x_in, out, dbg, s, fuse);
   }
-  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false, x_in, ctx->tmp);
+  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false, x_in, ctx->tmp,
+                             fuse ? out : nullptr, ctx->tmp);
   if (rc) return rc;
-  return moe_finish(ctx, T, ctx->tmp, out, dbg, s);
+  return moe_finish(ctx, T, ctx->tmp, out, dbg, s, fuse);
 }
 
 extern "C" int fsc_moe_forward_blocking_host(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in_host,
@@ -594,9 +642,20 @@ extern "C" int fsc_op_permute(fsc_ctx* ctx, const void* xn, const int* src_row, 
   return FSC_OK;
 }
 
+extern "C" int fsc_op_grouped_gemm_gather(fsc_ctx* ctx, int epi, const void* A, long a_rows, const int* a_idx,
+                                          const void* B0, const void* B1, int G, const int* counts, int m_total, int N,
+                                          int K, void* out, const float* resid, void* stream);
+
 extern "C" int fsc_op_grouped_gemm(fsc_ctx* ctx, int epi, const void* A, long a_rows, const void* B0, const void* B1,
                                    int G, const int* counts, int m_total, int N, int K, void* out, const float* resid,
                                    void* stream) {
+  return fsc_op_grouped_gemm_gather(ctx, epi, A, a_rows, nullptr, B0, B1, G, counts, m_total, N, K, out, resid,
+                                    stream);
+}
+
+extern "C" int fsc_op_grouped_gemm_gather(fsc_ctx* ctx, int epi, const void* A, long a_rows, const int* a_idx,
+                                          const void* B0, const void* B1, int G, const int* counts, int m_total, int N,
+                                          int K, void* out, const float* resid, void* stream) {
   if (!ctx) return FSC_ERR_SHAPE;
   REQUIRE(epi >= 0 && epi <= 2, FSC_ERR_CONFIG, "epi");
   REQUIRE(K % 64 == 0 && K > 0 && gemm_pick_bn(epi, N) > 0, FSC_ERR_CONFIG, "GEMM needs K%%64==0 and N%%64==0");
@@ -607,6 +666,7 @@ extern "C" int fsc_op_grouped_gemm(fsc_ctx* ctx, int epi, const void* A, long a_
   L.G = G; L.counts = counts; L.m_total = m_total; L.out = out; L.ldo = N; L.resid = resid; L.ldr = N; L.epi = epi;
   L.num_ctas = ctx->gemm_ctas;
   L.cta_group = ctx->gemm_cg;
+  L.a_idx = a_idx;
   CK(launch_grouped_gemm(L, static_cast<cudaStream_t>(stream)));
   return FSC_OK;
 }

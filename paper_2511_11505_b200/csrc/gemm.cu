@@ -67,6 +67,128 @@ FSC_DEVINL TileInfo decode_tile(int t, int n_tiles, int G, const int* s_row_off,
   ti.rows = min(TILE_M, m - ti.mb * TILE_M);
   return ti;
 }
+// Fused gate-weighted unpermute (see GemmParams::comb_out). Called by an epilogue
+// warp after each lane stored the y columns [c0, c0 + BN/2) of its row (token
+// `tok`, -1 = no row): each lane bumps its (token, column block) counter with a
+// release RMW (orders its y stores); the lane that brings it to k acquires (the RMW
+// chain makes every copy's stores visible) and __syncwarp passes that on to the
+// warp, which then finishes those tokens cooperatively, up to 4 at a time with all
+// their k row loads in flight (lane i owns columns c0 + CPL*i ...), in slot order
+// exactly as unpermute_kernel: acc = 0; acc = fma(w_j, y_j, acc), j = 0..k-1;
+// out = resid + acc. Requires k <= 8.
+FSC_DEVINL int atom_add_release_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+FSC_DEVINL void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+template <int BN>
+FSC_DEVINL void fused_unpermute(const GemmParams& p, long tok, int c0, int lane) {
+  constexpr int CPL = BN / 2 / 32;      // columns per lane: 4 (BN 256), 2 (128), 1 (64)
+  constexpr int TQ = 4;                 // tokens finished together
+  const int k = p.top_k;
+  bool last = false;
+  if (tok >= 0) {
+    int* cp = p.comb_cnt + tok * p.n_cb + c0 / (BN / 2);
+    last = atom_add_release_gpu(cp, 1) == k - 1;
+    if (last) {
+      fence_acquire_gpu();
+      *cp = 0;                          // every copy arrived: reset for the next call
+    }
+  }
+  uint32_t m = __ballot_sync(0xffffffffu, last);
+  if (!m) return;
+  __syncwarp();
+  const int ld = p.n_cb * (BN / 2);     // = d
+  const uint16_t* y = reinterpret_cast<const uint16_t*>(p.out);
+  const int col = c0 + CPL * lane;
+  while (m) {
+    long tq[TQ];
+    int nq = 0;
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      tq[q] = -1;
+      if (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        tq[q] = __shfl_sync(0xffffffffu, tok, src);
+        ++nq;
+      }
+    }
+    // lane q*k + j holds pos / w of (token q, slot j)
+    int pj = 0;
+    float wj = 0.f;
+    {
+      const int q = lane / k, j = lane - (lane / k) * k;
+      if (q < nq) {
+        long tt = tq[0];
+#pragma unroll
+        for (int u = 1; u < TQ; ++u)
+          if (q == u) tt = tq[u];
+        pj = __ldcg(p.pos + tt * k + j);
+        wj = __ldcg(p.topk_w + tt * k + j);
+      }
+    }
+    uint32_t yv[TQ][8][(CPL + 1) / 2];
+    float rv[TQ][CPL];
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int pr = __shfl_sync(0xffffffffu, pj, (q * k + j) & 31);
+        if (q < nq && j < k) {
+          const uint16_t* yr = y + (long)pr * ld + col;
+          if (CPL == 4) {
+            const uint2 u = __ldcg(reinterpret_cast<const uint2*>(yr));
+            yv[q][j][0] = u.x;
+            yv[q][j][(CPL + 1) / 2 - 1] = u.y;
+          } else if (CPL == 2) {
+            yv[q][j][0] = __ldcg(reinterpret_cast<const unsigned int*>(yr));
+          } else {
+            yv[q][j][0] = (uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(yr));
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < CPL; ++i)
+        rv[q][i] = (q < nq && p.comb_resid) ? __ldcg(p.comb_resid + tq[q] * ld + col + i) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      if (q >= nq) break;
+      float acc[CPL];
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) acc[i] = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float g = __shfl_sync(0xffffffffu, wj, (q * k + j) & 31);
+        if (j < k) {
+          if (CPL == 4) {
+            acc[0] = fmaf(g, bf16lo(yv[q][j][0]), acc[0]);
+            acc[1 % CPL] = fmaf(g, bf16hi(yv[q][j][0]), acc[1 % CPL]);
+            acc[2 % CPL] = fmaf(g, bf16lo(yv[q][j][(CPL + 1) / 2 - 1]), acc[2 % CPL]);
+            acc[3 % CPL] = fmaf(g, bf16hi(yv[q][j][(CPL + 1) / 2 - 1]), acc[3 % CPL]);
+          } else if (CPL == 2) {
+            acc[0] = fmaf(g, bf16lo(yv[q][j][0]), acc[0]);
+            acc[1 % CPL] = fmaf(g, bf16hi(yv[q][j][0]), acc[1 % CPL]);
+          } else {
+            acc[0] = fmaf(g, bf16lo(yv[q][j][0]), acc[0]);
+          }
+        }
+      }
+      float* oo = p.comb_out + tq[q] * ld + col;
+      if (CPL == 4) {
+        *reinterpret_cast<float4*>(oo) =
+            make_float4(rv[q][0] + acc[0], rv[q][1 % CPL] + acc[1 % CPL], rv[q][2 % CPL] + acc[2 % CPL],
+                        rv[q][3 % CPL] + acc[3 % CPL]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) oo[i] = rv[q][i] + acc[i];
+      }
+    }
+  }
+}
 }  // namespace
 
 // CG = 1: one CTA per 128-row tile (tcgen05 cta_group::1).
@@ -147,7 +269,67 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kblocks = p.K / BK;
   const int t_first = blockIdx.x / CG, t_step = gridDim.x / CG;
 
-  if (warp == 0) {
+  if (warp == 0 && p.a_idx) {
+    // ------------------------------------------------ TMA producer, gathered A (whole warp 0):
+    // lane j gathers rows 4j..4j+3 of this CTA's 128-row slice (fused permute, EP = 1)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = t_first; t < total; t += t_step) {
+      TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
+      const int arow = ti.row0 + (int)rank * BM;
+      const int rend = ti.row0 + ti.rows;
+      // only the groups of 4 rows that hold valid rows are gathered (rows past the
+      // group end are never stored, so stale shared memory there is harmless)
+      const int v0 = min(BM, max(0, ti.rows)), v1 = min(BM, max(0, ti.rows - BM));
+      const int my_valid = rank ? v1 : v0;
+      const uint32_t a_bytes = (uint32_t)((v0 + 3) / 4 + (CG == 2 ? (v1 + 3) / 4 : 0)) * 4 * BK * 2;
+      int ri[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = arow + 4 * lane + u;
+        ri[u] = r < rend ? __ldg(p.a_idx + r) : 0;   // rows past the group: any valid row (not stored)
+      }
+      int brow0, brow1 = 0;
+      const CUtensorMap* mb0 = &tmB0;
+      const CUtensorMap* mb1 = &tmB0;
+      if (CG == 2) {
+        if (EPI == EPI_SWIGLU) {
+          brow0 = ti.g * p.b_group_rows + ti.nb * C::HALF;
+          mb0 = rank ? &tmB1 : &tmB0;
+        } else {
+          brow0 = ti.g * p.b_group_rows + ti.nb * BN + (int)rank * C::HALF;
+        }
+      } else {
+        if (EPI == EPI_SWIGLU) {
+          brow0 = ti.g * p.b_group_rows + ti.nb * C::HALF;
+          brow1 = brow0;
+          mb1 = &tmB1;
+        } else {
+          brow0 = ti.g * p.b_group_rows + ti.nb * BN;
+          brow1 = brow0 + C::HALF;
+        }
+      }
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* b = sB + stage * C::B_BYTES;
+        if (lane == 0) {
+          if (CG == 2) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::B_BYTES + a_bytes);
+            tma_load_2d_2sm(b, mb0, &full[stage], kb * BK, brow0, kEvictLast);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::B_BYTES + a_bytes);
+            tma_load_2d(b, mb0, &full[stage], kb * BK, brow0, kEvictLast);
+            tma_load_2d(b + C::HALF * BK * 2, mb1, &full[stage], kb * BK, brow1, kEvictLast);
+          }
+        }
+        __syncwarp();
+        if (4 * lane < my_valid)
+          tma_gather4<CG>(sA + stage * C::A_BYTES + lane * 4 * BK * 2, &tmA, &full[stage], kb * BK, ri[0], ri[1],
+                          ri[2], ri[3], kEvictNormal);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs of a pair)
     if (elect_one()) {
       int stage = 0;
@@ -276,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           out = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + ti.nb * BN;
         }
+        const long tok = (p.comb_out && valid) ? (long)__ldg(p.src_row + grow) : -1;
 #pragma unroll 1
         for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
           uint32_t v[32];
@@ -290,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               st_global_v4(out + c + 8 * i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
           }
         }
+        if (p.comb_out) fused_unpermute<BN>(p, tok, ti.nb * BN + half * (BN / 2), lane);
       } else {
         float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo + ti.nb * BN;
         const float* res = (p.resid && valid) ? p.resid + grow * p.ldr + ti.nb * BN : nullptr;
@@ -377,7 +561,7 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   using C = Cfg<BN, CG>;
   CUtensorMap ma, mb0, mb1;
   long a_rows = L.a_rows > 0 ? L.a_rows : 1;
-  if (!make_map(&ma, L.A, a_rows, L.K, BM)) return cudaErrorInvalidValue;
+  if (!make_map(&ma, L.A, a_rows, L.K, L.a_idx ? 1 : BM)) return cudaErrorInvalidValue;   // gather4: {64, 1} box
   if (!make_map(&mb0, L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
   if (!make_map(&mb1, L.B1 ? L.B1 : L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
   auto kern = grouped_gemm_kernel<BN, EPI, CG>;
@@ -400,6 +584,15 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   p.ldr = L.ldr;
   p.ret = L.ret;
   for (int i = 0; i < 8; ++i) p.peer_out[i] = L.peer_out[i];
+  p.a_idx = L.a_idx;
+  p.comb_out = L.comb_out;
+  p.comb_resid = L.comb_resid;
+  p.src_row = L.src_row;
+  p.pos = L.pos;
+  p.topk_w = L.topk_w;
+  p.comb_cnt = L.comb_cnt;
+  p.top_k = L.top_k;
+  p.n_cb = L.N / (BN / 2);
   int grid = L.num_ctas > 0 ? L.num_ctas : kNumSMs;
   if (CG == 2) grid &= ~1;
   if (grid < CG) grid = CG;

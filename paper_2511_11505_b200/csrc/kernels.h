@@ -25,6 +25,20 @@ struct GemmParams {
   // (ret[r] >> 24), row (ret[r] & 0xFFFFFF) of peer_out[rank]; nullptr = local store
   const int* ret;
   void* peer_out[8];
+  // A gather (EP = 1, fused permute): row r of the grouped problem is row a_idx[r]
+  // of A (TMA gather4); nullptr = A rows are contiguous in group order
+  const int* a_idx;
+  // EPI_BF16 fused gate-weighted unpermute (EP = 1 blocking): after a
+  // row's y columns are stored, its (token, column block) counter is bumped; the
+  // k-th arrival computes comb_out[t] = comb_resid[t] + sum_j w[t,j] y[pos[t,j]]
+  // (slot order, fp32, bitwise the unpermute kernel) for that column block.
+  float* comb_out;             // nullptr: no fusion
+  const float* comb_resid;
+  const int* src_row;          // [R] token of send row
+  const int* pos;              // [T, k]
+  const float* topk_w;         // [T, k]
+  int* comb_cnt;               // [T, n_cb] zero between calls (the last arrival resets)
+  int top_k, n_cb;
 };
 
 struct GemmLaunch {
@@ -46,6 +60,14 @@ struct GemmLaunch {
   int cta_group = 2;  // 2: CTA pairs, MMA M=256 (default); 1: single-CTA M=128 tiles
   const int* ret = nullptr;           // scatter map (see GemmParams)
   void* peer_out[8] = {};
+  const int* a_idx = nullptr;         // A gather map (see GemmParams); A then has a_rows source rows
+  float* comb_out = nullptr;          // fused unpermute (see GemmParams)
+  const float* comb_resid = nullptr;
+  const int* src_row = nullptr;
+  const int* pos = nullptr;
+  const float* topk_w = nullptr;
+  int* comb_cnt = nullptr;
+  int top_k = 0;
 };
 
 cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s);

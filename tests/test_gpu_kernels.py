@@ -88,6 +88,37 @@ def test_grouped_gemm_swiglu(ctx, counts, N, K, cg):
         r += m
 
 
+@pytest.mark.parametrize("counts,N,K,src", [([1], 128, 64, 5), ([0, 130, 257], 128, 128, 100),
+                                            ([333, 900, 17], 1408, 2048, 700), ([600, 0, 257, 255], 768, 2048, 1111),
+                                            ([517, 64, 1, 129, 0, 255, 256, 1000], 256, 1408, 300)])
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("epi", [0, 1])
+def test_grouped_gemm_gather(ctx, counts, N, K, src, cg, epi):
+    """Fused permute (EP = 1): row r of the grouped GEMM reads A[a_idx[r]] through TMA
+    gather4; equals the GEMM of the explicitly permuted rows."""
+    ctx.set_gemm_cta_group(cg)
+    rng = np.random.default_rng(11 + N + K + epi)
+    G, M = len(counts), sum(counts)
+    A = rand_bf16(rng, (src, K))
+    a_idx = rng.integers(0, src, size=M).astype(np.int32)
+    W1 = rand_bf16(rng, (G * N, K), 1.0 / np.sqrt(K))
+    W2 = rand_bf16(rng, (G * N, K), 1.0 / np.sqrt(K)) if epi == 1 else None
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    cnt = torch.tensor(counts, dtype=torch.int32, device="cuda")
+    ctx.op_grouped_gemm_gather(epi, dev_bf16(A), torch.from_numpy(a_idx).cuda(), dev_bf16(W1),
+                               dev_bf16(W2) if W2 is not None else None, G, cnt, 0, N, K, out)
+    torch.cuda.synchronize()
+    got = host_bf16_to_f64(out)
+    Af = synth.bf16_bits_to_f64(A)[a_idx]
+    r = 0
+    for g, m in enumerate(counts):
+        if m:
+            u = Af[r:r + m] @ synth.bf16_bits_to_f64(W1[g * N:(g + 1) * N]).T
+            ref = u * om.silu(Af[r:r + m] @ synth.bf16_bits_to_f64(W2[g * N:(g + 1) * N]).T) if epi == 1 else u
+            assert rel_l2(got[r:r + m], ref) < 5e-3, (g, rel_l2(got[r:r + m], ref))
+        r += m
+
+
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("with_resid", [True, False])
 def test_gemm_resid_f32_single_group(ctx, with_resid, cg):

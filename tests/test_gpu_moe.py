@@ -212,3 +212,37 @@ def test_decode_regime_parity(base, T):
     np.testing.assert_array_equal(dbg["topk_idx"], r.idx)
     sh, ro, _ = om.moe_block(x, lay, router=r)
     assert rel_l2(out, (x.astype(np.float64) + sh) + ro) < TOL
+
+
+@pytest.mark.parametrize("name,T", [("dsv2lite", 300), ("qwen3", 512)])
+def test_fused_gather_permute_is_bitwise_identical(name, T):
+    """fsc_set_gemm_gather: GEMM1 gathers the xn rows through src_row (TMA gather4)
+    instead of reading the explicitly permuted buffer; the same operand rows reach
+    the same MMA, so the layer output is bit-identical."""
+    shape = synth.CONFIGS[name]
+    ctx = make_ctx(shape, T)
+    w = moe_weights_dev(synth.moe_weights(shape, seed=9))
+    x = synth.tokens(shape, seed=9, T=T)
+    out0, _ = run_blocking(ctx, w, x)
+    ctx.set_gemm_gather(True)
+    out1, _ = run_blocking(ctx, w, x)
+    ctx.close()
+    assert np.array_equal(out0, out1)
+
+
+@pytest.mark.parametrize("name,T", [("tiny", 32), ("dsv2lite", 300), ("qwen3", 257), ("scout", 200)])
+def test_fused_unpermute_is_bitwise_identical(name, T):
+    """Blocking EP = 1 fuses the gate-weighted unpermute into the down GEMM's epilogue
+    (last-arriving copy finishes the token); it must equal the separate unpermute
+    kernel bit for bit, in slot order (C-amb-12), on repeated calls (counters reset)."""
+    shape = synth.CONFIGS[name]
+    ctx = make_ctx(shape, T)
+    w = moe_weights_dev(synth.moe_weights(shape, seed=4))
+    x = synth.tokens(shape, seed=4, T=T)
+    ctx.set_fused_unpermute(False)
+    ref, _ = run_blocking(ctx, w, x)
+    ctx.set_fused_unpermute(True)
+    for _ in range(3):
+        got, _ = run_blocking(ctx, w, x)
+        assert np.array_equal(got, ref)
+    ctx.close()
