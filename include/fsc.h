@@ -62,6 +62,12 @@ typedef enum {
 enum { FSC_REGULAR = 0, FSC_HYBRID = 1 };
 /* Stream schedule of the stack (P:103 vs P:198). */
 enum { FSC_BLOCKING = 0, FSC_OVERLAPPED = 1 };
+/* EP data movement: FSC_EP_ALLTOALL = Dispatch / Combine (training
+ * path, each rank owns its T tokens); FSC_EP_ALLREDUCE = the inference variant of
+ * P:215-217 (vLLM): every rank holds the SAME T tokens (replicated activations),
+ * computes only its local experts' contributions and the partial outputs are
+ * all-reduced (reduce-scatter + all-gather over peer memory, rank-order sums). */
+enum { FSC_EP_ALLTOALL = 0, FSC_EP_ALLREDUCE = 1 };
 
 /* MoE layer shape. d % 64 == 0, ffn % 64 == 0, shared_ffn % 64 == 0 (0 = no shared
  * expert; n shared experts = one SwiGLU of concatenated width, C-amb-7),
@@ -151,6 +157,20 @@ FSC_API int fsc_set_gemm_gather(fsc_ctx* ctx, int on);
  * runs the separate unpermute kernel, on < 0 (default) fuses for top-1 routing only.
  * Bitwise the same result either way. */
 FSC_API int fsc_set_fused_unpermute(fsc_ctx* ctx, int on);
+/* Router (K1) on the int8 tensor cores (E <= 64, d % 128 == 0, k <= 8): x and
+ * gamma (.) W_R split into three exact 7-bit fixed-point planes, the plane products
+ * summed exactly in int32 (tcgen05 kind::i8), combined in fp64; the same selection,
+ * fp64 band refinement and results contract as the default fp32 SIMT router (both
+ * equal the fp64 oracle's selection). Allocates its workspace on first use.
+ * Default off: measured slower than the SIMT router on the BASELINE shapes. */
+FSC_API int fsc_set_router_int8(fsc_ctx* ctx, int on);
+/* Select the EP data movement (FSC_EP_ALLTOALL default, FSC_EP_ALLREDUCE). Must be
+ * called before fsc_bootstrap_export (it re-creates the peer region). In
+ * FSC_EP_ALLREDUCE the shared expert is computed replicated on every rank (no
+ * extra collective), the routed partials are all-reduced; the FarSkip entry
+ * returns with the all-reduce in flight and fsc_moe_wait completes it (the
+ * "synchronize only before the next MoE computation" of P:217). */
+FSC_API int fsc_set_ep_mode(fsc_ctx* ctx, int mode);
 
 /* Per-phase CUDA-event timing of the MoE calls (bench / profiling). When enabled,
  * events are recorded on the call's stream around every phase; fsc_get_timings

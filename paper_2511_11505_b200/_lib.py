@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("FSC_LIB", os.path.join(HERE, "libfsc.so"))
 FSC_OK, FSC_ERR_CONFIG, FSC_ERR_SHAPE, FSC_ERR_CUDA, FSC_ERR_COMM, FSC_ERR_NONFINITE, FSC_ERR_STATE = 0, -1, -2, -3, -4, -5, -6
 FSC_REGULAR, FSC_HYBRID = 0, 1
 FSC_BLOCKING, FSC_OVERLAPPED = 0, 1
+FSC_EP_ALLTOALL, FSC_EP_ALLREDUCE = 0, 1
 EPI_BF16, EPI_SWIGLU, EPI_RESID_F32 = 0, 1, 2
 
 _STATUS = {FSC_ERR_CONFIG: "CONFIG", FSC_ERR_SHAPE: "SHAPE", FSC_ERR_CUDA: "CUDA", FSC_ERR_COMM: "COMM",
@@ -69,6 +70,8 @@ _SIGS = {
     "fsc_set_gemm_cta_group": (_I, [_P, _I]),
     "fsc_set_gemm_gather": (_I, [_P, _I]),
     "fsc_set_fused_unpermute": (_I, [_P, _I]),
+    "fsc_set_router_int8": (_I, [_P, _I]),
+    "fsc_set_ep_mode": (_I, [_P, _I]),
     "fsc_set_timing": (_I, [_P, _I]),
     "fsc_set_timing_mask": (_I, [_P, ctypes.c_uint]),
     "fsc_get_timings": (_I, [_P, ctypes.POINTER(ctypes.c_float), _I]),
@@ -244,6 +247,15 @@ class Context:
     def set_gemm_gather(self, on: bool):
         """EP = 1: fuse the permute into GEMM1 (TMA gather4 of the xn rows)."""
         self._ck(self.lib.fsc_set_gemm_gather(self.h, int(on)))
+
+    def set_ep_mode(self, mode: int):
+        """FSC_EP_ALLTOALL (Dispatch / Combine) or FSC_EP_ALLREDUCE (replicated tokens,
+        P:215-217). Call before connect()."""
+        self._ck(self.lib.fsc_set_ep_mode(self.h, mode))
+
+    def set_router_int8(self, on: bool):
+        """Router on the int8 tensor cores (exact fixed-point planes); E <= 64, d % 128 == 0."""
+        self._ck(self.lib.fsc_set_router_int8(self.h, int(on)))
 
     def set_fused_unpermute(self, on):
         """Blocking EP = 1: gate-weighted unpermute fused into the down GEMM epilogue

@@ -27,6 +27,8 @@ struct fsc_ctx {
   int gemm_ctas = 148;
   int gemm_cg = 2;
   int fuse_unpermute = -1;     // blocking EP = 1: unpermute fused into GEMM2 (-1 auto: top-1)
+  int ep_mode = 0;             // FSC_EP_ALLTOALL (dispatch / combine) or FSC_EP_ALLREDUCE (replicated tokens)
+  int router_i8 = 0;           // exact int8 tensor-core router (fsc_set_router_int8)
   int gather_a = 0;            // EP = 1: GEMM1 gathers A through src_row (fused permute)
   int sticky = 0;
   char err[512] = {0};
@@ -42,6 +44,13 @@ struct fsc_ctx {
   int* counts = nullptr;       // [E]                copies per global expert (this rank)
   int* offsets = nullptr;      // [E+1]
   int* comb_cnt = nullptr;     // [T, d/32]         fused-unpermute arrival counters
+  int8_t* i8_x = nullptr;      // exact int8 router workspace (E <= 64): planes of x, W'
+  int8_t* i8_w = nullptr;
+  float* i8_tok = nullptr;
+  double* i8_r = nullptr;
+  float* i8_exp = nullptr;
+  int* i8_part = nullptr;
+  int* i8_cnt = nullptr;
   float* r_part = nullptr;     // [kRouterSplitRows, 128] split-d partial logits (small T)
   double* r_part_sq = nullptr; // [kRouterSplitRows]      split-d partial sums of x^2
   float* w_scaled = nullptr;   // [E, d]             gamma * W_R
@@ -105,3 +114,7 @@ int fsc_transport_dispatch_wait(fsc_ctx* ctx, cudaStream_t s);
 int fsc_transport_combine(fsc_ctx* ctx, int T, cudaStream_t s);
 int fsc_transport_combine_wait(fsc_ctx* ctx, cudaStream_t s);
 void fsc_transport_scatter_target(fsc_ctx* ctx, const int** ret, void** peer_out);
+float* fsc_transport_ar_partial(fsc_ctx* ctx);
+int fsc_transport_ar_start(fsc_ctx* ctx, int T, cudaStream_t s);
+int fsc_transport_ar_finish(fsc_ctx* ctx, int T, const float* resid, float* out, cudaStream_t s);
+int fsc_transport_reinit(fsc_ctx* ctx);

@@ -2,6 +2,7 @@
 // two MoE schedules of the paper (blocking; FarSkip).
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <new>
@@ -72,6 +73,8 @@ static cudaError_t ph_record(cudaEvent_t ev, cudaStream_t st) {
   }
 #define PH_BEGIN(i) PH_BEGIN_ON(i, s)
 #define PH_END(i) PH_END_ON(i, s)
+
+constexpr int TB_DEFAULT = 32;   // RouterLaunch::rpb (set by launch_router)
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -168,7 +171,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->i8_x, ctx->i8_w, ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -251,6 +254,42 @@ extern "C" int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg) {
   return FSC_OK;
 }
 
+extern "C" int fsc_set_ep_mode(fsc_ctx* ctx, int mode) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(mode == FSC_EP_ALLTOALL || mode == FSC_EP_ALLREDUCE, FSC_ERR_CONFIG, "unknown EP mode %d", mode);
+  REQUIRE(!ctx->pending, FSC_ERR_STATE, "a FarSkip handle is outstanding");
+  if (mode == ctx->ep_mode) return FSC_OK;
+  ctx->ep_mode = mode;
+  if (ctx->ep == 1) return FSC_OK;
+  CK(cudaSetDevice(ctx->device));
+  return fsc_transport_reinit(ctx);   // new symmetric layout: bootstrap (export / import) after this
+}
+
+extern "C" int fsc_set_router_int8(fsc_ctx* ctx, int on) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  const fsc_moe_config& c = ctx->cfg;
+  const long T = c.max_tokens, d = c.d;
+  if (!on) {
+    ctx->router_i8 = 0;
+    return FSC_OK;
+  }
+  REQUIRE(c.n_experts <= 64 && d % 128 == 0 && c.top_k <= 8, FSC_ERR_CONFIG,
+          "int8 router needs E <= 64, d %% 128 == 0, k <= 8");
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->i8_x) {   // workspace on first use
+    CK(dalloc(&ctx->i8_x, 3 * T * d));
+    CK(dalloc(&ctx->i8_w, 3 * 64 * d));
+    CK(dalloc(&ctx->i8_part, (long)kI8SplitRows * 256));
+    CK(dalloc(&ctx->i8_cnt, (T + 127) / 128 + 1));
+    CK(cudaMemset(ctx->i8_cnt, 0, sizeof(int) * ((T + 127) / 128 + 1)));
+    CK(dalloc(&ctx->i8_tok, 3 * T));
+    CK(dalloc(&ctx->i8_r, T));
+    CK(dalloc(&ctx->i8_exp, 3 * 64));
+  }
+  ctx->router_i8 = 1;
+  return FSC_OK;
+}
+
 extern "C" int fsc_set_fused_unpermute(fsc_ctx* ctx, int on) {
   if (!ctx) return FSC_ERR_SHAPE;
   ctx->fuse_unpermute = on < 0 ? -1 : (on ? 1 : 0);
@@ -306,11 +345,13 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   const int d = c.d, E = c.n_experts, k = c.top_k;
   RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
                   dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr,
-                  ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq};
+                  ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, TB_DEFAULT,
+                  ctx->router_i8 ? ctx->i8_x : nullptr, ctx->i8_w,
+                  ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt};
   PH_BEGIN(PH_ROUTER);
   CK(launch_router(rl, s));
   PH_END(PH_ROUTER);
-  const bool early_shared = shared_out && ctx->ep == 1;
+  const bool early_shared = shared_out && (ctx->ep == 1 || ctx->ep_mode == FSC_EP_ALLREDUCE);
   cudaStream_t ps = early_shared ? ctx->aux : s;   // stream of the permutation work
   if (early_shared) {
     CK(cudaEventRecord(ctx->ev_c, s));
@@ -330,7 +371,27 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   const int* recv_counts = ctx->counts;
   cudaStream_t cs = overlap ? ctx->comm : s;
   const int* a_idx = nullptr;
-  if (ctx->ep == 1 && ctx->gather_a) {
+  const bool allreduce = ctx->ep > 1 && ctx->ep_mode == FSC_EP_ALLREDUCE;
+  const int* row_base = nullptr;
+  int G_loc = ctx->e_loc;
+  if (allreduce) {
+    // replicated tokens, local experts only. Their rows are the contiguous
+    // range [offsets[e0], offsets[e0 + E_loc]) of the global expert-sorted order.
+    const int e0 = ctx->rank * ctx->e_loc;
+    PH_BEGIN_ON(PH_DISPATCH, ps);
+    CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, ps, ctx->offsets + e0, ctx->e_loc));
+    PH_END_ON(PH_DISPATCH, ps);
+    recv = ctx->xs;
+    recv_rows = R;
+    recv_counts = ctx->counts + e0;
+    row_base = ctx->offsets + e0;
+    if (early_shared) {
+      CK(cudaEventRecord(ctx->ev_d, ps));
+      int rc = moe_shared(ctx, w, T, shared_resid, shared_out, dbg, s);   // replicated shared expert
+      if (rc) return rc;
+      CK(cudaStreamWaitEvent(s, ctx->ev_d, 0));
+    }
+  } else if (ctx->ep == 1 && ctx->gather_a) {
     // EP = 1 with fsc_set_gemm_gather(ctx, 1): no dispatch copy; the permutation is
     // fused into GEMM1's operand load, whose producer gathers the expert-sorted rows of
     // xn through src_row (TMA gather4, only the valid rows of each tile). Off by
@@ -390,6 +451,8 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   g1.b_group_rows = c.ffn; g1.K = d; g1.N = c.ffn; g1.G = ctx->e_loc; g1.counts = recv_counts; g1.m_total = 0;
   g1.out = ctx->h; g1.ldo = c.ffn; g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas; g1.cta_group = ctx->gemm_cg;
   g1.a_idx = a_idx;
+  g1.row_base = row_base;
+  (void)G_loc;
   PH_BEGIN(PH_GEMM1);
   CK(launch_grouped_gemm(g1, s));
   PH_END(PH_GEMM1);
@@ -397,7 +460,8 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   g2.A = ctx->h; g2.a_rows = a_idx ? (long)R : recv_rows; g2.B0 = w->w3; g2.B1 = nullptr; g2.b_rows = (long)ctx->e_loc * d;
   g2.b_group_rows = d; g2.K = c.ffn; g2.N = d; g2.G = ctx->e_loc; g2.counts = recv_counts; g2.m_total = 0;
   g2.out = ctx->y; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = ctx->gemm_cg;
-  if (ctx->ep > 1) fsc_transport_scatter_target(ctx, &g2.ret, g2.peer_out);  // P:100 Combine, fused
+  g2.row_base = row_base;
+  if (ctx->ep > 1 && !allreduce) fsc_transport_scatter_target(ctx, &g2.ret, g2.peer_out);  // P:100 Combine, fused
   if (fused_out && ctx->ep == 1) {   // P:100 "sum the routed experts", fused into the down GEMM
     g2.comb_out = fused_out; g2.comb_resid = fused_resid; g2.src_row = ctx->src_row; g2.pos = ctx->pos;
     g2.topk_w = ctx->topk_w; g2.comb_cnt = ctx->comb_cnt; g2.top_k = k;
@@ -405,7 +469,24 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   PH_BEGIN(PH_GEMM2);
   CK(launch_grouped_gemm(g2, s));
   PH_END(PH_GEMM2);
-  if (ctx->ep > 1) {
+  if (allreduce) {
+    // local partial of the routed sum (fp32, slot order) into the peer-visible buffer,
+    // then the all-reduce on the comm stream (FarSkip) or in line (blocking)
+    const int e0 = ctx->rank * ctx->e_loc;
+    PH_BEGIN(PH_UNPERMUTE);
+    CK(launch_unpermute_local(ctx->y, ctx->pos, ctx->topk_w, ctx->topk_idx, e0, e0 + ctx->e_loc,
+                              fsc_transport_ar_partial(ctx), T, k, d, s));
+    PH_END(PH_UNPERMUTE);
+    if (overlap) {
+      CK(cudaEventRecord(ctx->ev_a, s));
+      CK(cudaStreamWaitEvent(cs, ctx->ev_a, 0));
+    }
+    PH_BEGIN_ON(PH_COMBINE, cs);
+    int rc = fsc_transport_ar_start(ctx, T, cs);
+    if (rc) return rc;
+    PH_END_ON(PH_COMBINE, cs);
+    if (overlap) CK(cudaEventRecord(ctx->ev_b, cs));
+  } else if (ctx->ep > 1) {
     PH_BEGIN(PH_COMBINE);
     int rc = fsc_transport_combine(ctx, T, s);  // P:198 step 7: Combine completes asynchronously
     if (rc) return rc;
@@ -458,6 +539,18 @@ static int moe_finish(fsc_ctx* ctx, int T, const float* resid, float* out, const
                       bool fused = false) {
   const fsc_moe_config& c = ctx->cfg;
   const uint16_t* ysrc = ctx->y;
+  if (ctx->ep > 1 && ctx->ep_mode == FSC_EP_ALLREDUCE) {   // out = resid + all-reduced routed sum
+    PH_BEGIN(PH_COMBINE_WAIT);
+    CK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
+    int rc = fsc_transport_ar_finish(ctx, T, resid, out, s);
+    if (rc) return rc;
+    PH_END(PH_COMBINE_WAIT);
+    if (dbg && dbg->routed_out) {
+      rc = fsc_transport_ar_finish(ctx, T, nullptr, dbg->routed_out, s);
+      if (rc) return rc;
+    }
+    return FSC_OK;
+  }
   if (ctx->ep > 1) {
     PH_BEGIN(PH_COMBINE_WAIT);
     int rc = fsc_transport_combine_wait(ctx, s);
@@ -620,7 +713,8 @@ extern "C" int fsc_op_router(fsc_ctx* ctx, const float* x, const float* gamma, c
   REQUIRE(T >= 0 && T <= ctx->cfg.max_tokens && E <= ctx->cfg.n_experts && d <= ctx->cfg.d, FSC_ERR_CONFIG,
           "router shape beyond the context workspace");
   RouterLaunch rl{x, gamma, w_router, T, d, E, k, ctx->cfg.rms_eps, static_cast<uint16_t*>(xn), topk_idx, topk_w,
-                  logits, n_refined, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq};
+                  logits, n_refined, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, TB_DEFAULT,
+                  (ctx->router_i8 && d % 128 == 0) ? ctx->i8_x : nullptr, ctx->i8_w, ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt};
   CK(launch_router(rl, static_cast<cudaStream_t>(stream)));
   return FSC_OK;
 }

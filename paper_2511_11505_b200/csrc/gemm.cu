@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
 
   const uint32_t tmem_base = *s_tmem;
+  const int rbase = p.row_base ? __ldg(p.row_base) : 0;
   const int n_tiles = (EPI == EPI_SWIGLU) ? p.N / C::HALF : p.N / BN;
   const int total = s_tile_off[G] * n_tiles;
   const int kblocks = p.K / BK;
@@ -276,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     for (int t = t_first; t < total; t += t_step) {
       TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
+      ti.row0 += rbase;
       const int arow = ti.row0 + (int)rank * BM;
       const int rend = ti.row0 + ti.rows;
       // only the groups of 4 rows that hold valid rows are gathered (rows past the
@@ -336,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int t = t_first; t < total; t += t_step) {
         TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
+      ti.row0 += rbase;
         const int arow = ti.row0 + (int)rank * BM;
         int brow0, brow1 = 0;
         const CUtensorMap* mb0 = &tmB0;
@@ -418,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;
     for (int t = t_first; t < total; t += t_step, ++it) {
       TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
+      ti.row0 += rbase;
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       const int rr = r + (int)rank * BM;          // row inside the pair tile
@@ -585,6 +589,7 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   p.ret = L.ret;
   for (int i = 0; i < 8; ++i) p.peer_out[i] = L.peer_out[i];
   p.a_idx = L.a_idx;
+  p.row_base = L.row_base;
   p.comb_out = L.comb_out;
   p.comb_resid = L.comb_resid;
   p.src_row = L.src_row;

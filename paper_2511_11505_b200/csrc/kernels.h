@@ -32,6 +32,9 @@ struct GemmParams {
   // row's y columns are stored, its (token, column block) counter is bumped; the
   // k-th arrival computes comb_out[t] = comb_resid[t] + sum_j w[t,j] y[pos[t,j]]
   // (slot order, fp32, bitwise the unpermute kernel) for that column block.
+  // all-reduce EP mode: the local experts' rows sit at [*row_base, ...) of the
+  // globally expert-sorted A / out buffers (device int, nullptr = 0)
+  const int* row_base;
   float* comb_out;             // nullptr: no fusion
   const float* comb_resid;
   const int* src_row;          // [R] token of send row
@@ -61,6 +64,7 @@ struct GemmLaunch {
   const int* ret = nullptr;           // scatter map (see GemmParams)
   void* peer_out[8] = {};
   const int* a_idx = nullptr;         // A gather map (see GemmParams); A then has a_rows source rows
+  const int* row_base = nullptr;      // device row offset of group 0 (see GemmParams)
   float* comb_out = nullptr;          // fused unpermute (see GemmParams)
   const float* comb_resid = nullptr;
   const int* src_row = nullptr;
@@ -90,7 +94,16 @@ struct RouterLaunch {
   float* w_scaled;       // workspace [E, d]: gamma * W_R
   float* w_sq;           // workspace [E]: ||gamma * W_R[e]||^2
   int rpb = 32;          // tokens per CTA (set by launch_router)
+  // exact int8 tensor-core path (E <= 64, d % 128 == 0); nullptr planes = fp32 SIMT path
+  int8_t* i8_x;          // workspace [3, T, d]: 7-bit planes of x_t / s_t
+  int8_t* i8_w;          // workspace [3, 64, d]: 7-bit planes of (gamma W_R)_e / s_e
+  float* i8_tok;         // workspace [3, T]: s_t, ||x_t / s_t||_1, (float) r_t
+  double* i8_r;          // workspace [T]: r_t (fp64)
+  float* i8_exp;         // workspace [3, 64]: s_e and the two per-expert error-bound coefficients
+  int* i8_part;          // workspace [kI8SplitRows, 256]: split-d int32 partial sums
+  int* i8_cnt;           // workspace [ceil(T/128)]: split arrival tickets, zero between calls
 };
+constexpr int kI8SplitRows = 148 * 128;
 // split-d partials: (token blocks) x (d splits) <= 2 x 148 CTAs of <= 32 rows
 constexpr int kRouterSplitRows = 2 * 148 * 32;
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s);
@@ -111,13 +124,18 @@ struct PermLaunch {
 cudaError_t launch_perm_maps(const PermLaunch& L, cudaStream_t s);
 inline int perm_chunks(int T) { return (T + 31) / 32; }
 
-// K3: xs[p] = xn[src_row[p]]  (bf16 rows of d)
+// K3: xs[p] = xn[src_row[p]]  (bf16 rows of d); rng != nullptr: only rows p in
+// [rng[0], rng[rng_n]) (device offsets of a range of experts)
 cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t* xs, int R, int d,
-                                cudaStream_t s);
+                                cudaStream_t s, const int* rng = nullptr, int rng_n = 0);
 
 // K5: out[t] = resid[t] + sum_j w[t,j] * y[pos[t,j]]   (fp32 out, bf16 y, slot order)
 cudaError_t launch_unpermute(const uint16_t* y, const int* pos, const float* w, const float* resid,
                              float* out, int T, int k, int d, cudaStream_t s);
+// K5, local experts only (all-reduce EP mode): out[t] = sum over slots j with
+// e_lo <= idx[t,j] < e_hi of w[t,j] * y[pos[t,j]], from 0 in slot order
+cudaError_t launch_unpermute_local(const uint16_t* y, const int* pos, const float* w, const int* idx, int e_lo,
+                                   int e_hi, float* out, int T, int k, int d, cudaStream_t s);
 
 // attention filler (attention.cu)
 cudaError_t launch_rmsnorm_bf16(const float* x, const float* gamma, uint16_t* y, int T, int d, float eps,

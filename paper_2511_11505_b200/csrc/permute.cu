@@ -143,10 +143,12 @@ cudaError_t launch_perm_maps(const PermLaunch& L, cudaStream_t s) {
 // ------------------------------------------------------------------ K3 permute
 __global__ void __launch_bounds__(256) permute_rows_kernel(const uint4* __restrict__ xn,
                                                            const int* __restrict__ src_row,
-                                                           uint4* __restrict__ xs, int R, int dv) {
+                                                           uint4* __restrict__ xs, int R, int dv,
+                                                           const int* __restrict__ rng, int rng_n) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long r = (long)blockIdx.x * 8 + w;
   if (r >= R) return;
+  if (rng && (r < rng[0] || r >= rng[rng_n])) return;
   const long src = src_row[r];
   const uint4* a = xn + src * dv;
   uint4* b = xs + r * dv;
@@ -154,12 +156,12 @@ __global__ void __launch_bounds__(256) permute_rows_kernel(const uint4* __restri
 }
 
 cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t* xs, int R, int d,
-                                cudaStream_t s) {
+                                cudaStream_t s, const int* rng, int rng_n) {
   if (R == 0) return cudaSuccess;
   const int dv = d / 8;
   ++g_launches;
   permute_rows_kernel<<<(R + 7) / 8, 256, 0, s>>>(reinterpret_cast<const uint4*>(xn), src_row,
-                                                  reinterpret_cast<uint4*>(xs), R, dv);
+                                                  reinterpret_cast<uint4*>(xs), R, dv, rng, rng_n);
   return cudaGetLastError();
 }
 
@@ -207,6 +209,50 @@ cudaError_t launch_unpermute(const uint16_t* y, const int* pos, const float* w, 
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
   ++g_launches;
   unpermute_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, resid, out, items, dv, k);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) unpermute_local_kernel(const uint4* __restrict__ y, const int* __restrict__ pos,
+                                                              const float* __restrict__ w, const int* __restrict__ idx,
+                                                              int e_lo, int e_hi, float* __restrict__ out, long items,
+                                                              int dv, int k) {
+  for (long it = (long)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (long)gridDim.x * blockDim.x) {
+    const long t = it / dv;
+    const int c = (int)(it - t * dv);
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const int e = idx[t * k + j];
+      if (e < e_lo || e >= e_hi) continue;
+      const long p = pos[t * k + j];
+      const float g = w[t * k + j];
+      const uint4 v = y[p * dv + c];
+      acc[0] = fmaf(g, bf16lo(v.x), acc[0]);
+      acc[1] = fmaf(g, bf16hi(v.x), acc[1]);
+      acc[2] = fmaf(g, bf16lo(v.y), acc[2]);
+      acc[3] = fmaf(g, bf16hi(v.y), acc[3]);
+      acc[4] = fmaf(g, bf16lo(v.z), acc[4]);
+      acc[5] = fmaf(g, bf16hi(v.z), acc[5]);
+      acc[6] = fmaf(g, bf16lo(v.w), acc[6]);
+      acc[7] = fmaf(g, bf16hi(v.w), acc[7]);
+    }
+    float4* oo = reinterpret_cast<float4*>(out + t * (long)dv * 8 + c * 8);
+    oo[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    oo[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+cudaError_t launch_unpermute_local(const uint16_t* y, const int* pos, const float* w, const int* idx, int e_lo,
+                                   int e_hi, float* out, int T, int k, int d, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int dv = d / 8;
+  const long items = (long)T * dv;
+  long blocks = (items + 255) / 256;
+  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+  ++g_launches;
+  unpermute_local_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, idx, e_lo, e_hi, out,
+                                                     items, dv, k);
   return cudaGetLastError();
 }
 

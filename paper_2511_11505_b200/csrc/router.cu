@@ -23,6 +23,7 @@
 // sm_100). sum x^2 is accumulated from the staged chunks (no extra pass over x).
 // Small T (decode): the grid also splits d (gridDim.y), raw partials go to a
 // workspace and router_finish_kernel sums them in a fixed order and selects.
+#include <cudaTypedefs.h>
 #include <float.h>
 
 #include "common.cuh"
@@ -75,14 +76,16 @@ FSC_DEVINL void cp_async16(void* smem, const void* gmem, bool valid) {
 FSC_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 FSC_DEVINL void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-// Per-CTA state of the in-block band refinement (see refine_block).
-struct RefineSmem {
-  int flag[TB];          // token of the block has an ambiguous top-k boundary
-  float thr[TB][3];      // {2B + 4u(|l_(k)| + |l_(k+1)|), l_(k), l_(k+1)} of flagged tokens
+// Per-CTA state of the in-block band refinement (see refine_block), for blocks of ROWS tokens.
+template <int ROWS>
+struct RefineSmemT {
+  int flag[ROWS];        // token of the block has an ambiguous top-k boundary
+  float thr[ROWS][3];    // {2B + 4u(|l_(k)| + |l_(k+1)|), l_(k), l_(k+1)} of flagged tokens
   int band[128];
   int nb;
   double l64[128];
 };
+using RefineSmem = RefineSmemT<TB>;
 }  // namespace
 
 // W'[e][i] = gamma_i * W_R[e][i] and ||W'_e||^2 (error bound). One CTA per expert.
@@ -138,9 +141,8 @@ FSC_DEVINL void ffma2_bcast(float2& acc, float a, float2 b) {
 
 // Phase C for one token (one warp): top-k over the fp32 logits of row `lg`, gates,
 // or hand-off of the token to the band refinement when its boundary is ambiguous.
-template <int QN>
-FSC_DEVINL void select_token(const float* lg, long t, int tt, float B, const RouterLaunch& L, RefineSmem& rs,
-                             int lane) {
+template <int QN, class RS>
+FSC_DEVINL void select_token(const float* lg, long t, int tt, float B, const RouterLaunch& L, RS& rs, int lane) {
   const int E = L.E, k = L.k;
   float v[QN];
 #pragma unroll
@@ -217,9 +219,8 @@ FSC_DEVINL void select_token(const float* lg, long t, int tt, float B, const Rou
 // exact ties), then the boundary test, gates and ascending-id slots exactly as in
 // select_token. A warp selects 32 tokens at once with no shuffles (the warp
 // version above is latency-bound on k+1 rounds of 64-bit shuffle argmax).
-template <int K1>   // K1 = k + 1 (compile time: every register array index is static)
-FSC_DEVINL void select_token_thread(const float* lg, long t, int tt, float B, const RouterLaunch& L,
-                                    RefineSmem& rs) {
+template <int K1, class RS>   // K1 = k + 1 (compile time: every register array index is static)
+FSC_DEVINL void select_token_thread(const float* lg, long t, int tt, float B, const RouterLaunch& L, RS& rs) {
   constexpr int k = K1 - 1;
   const int E = L.E;
   float val[K1];
@@ -347,9 +348,9 @@ FSC_DEVINL void write_xn(const RouterLaunch& L, long t0, int rows, const float* 
 // their order; x_i gamma_i is exact in fp64); warp 0 fills the k - |certain| open
 // slots with the best band experts (fp64 value, ties -> lower id) and writes the
 // indices and gates (from the fp32 logits, as for every other token).
-template <int QN>
-FSC_DEVINL void refine_block(const RouterLaunch& L, const float* lg, int lgs, RefineSmem& rs, long t0, int rows) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+template <int QN, class RS>
+FSC_DEVINL void refine_block(const RouterLaunch& L, const float* lg, int lgs, RS& rs, long t0, int rows) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int d = L.d, E = L.E, k = L.k;
   for (int tt = 0; tt < rows; ++tt) {
     if (!rs.flag[tt]) continue;                  // block-uniform
@@ -378,7 +379,7 @@ FSC_DEVINL void refine_block(const RouterLaunch& L, const float* lg, int lgs, Re
     const int nb = rs.nb;
     const float4* x4 = reinterpret_cast<const float4*>(L.x + t * d);
     const float4* g4 = reinterpret_cast<const float4*>(L.gamma);
-    for (int b = warp; b < nb; b += 8) {
+    for (int b = warp; b < nb; b += nwarps) {
       const int e = rs.band[b];
       const float4* w4 = reinterpret_cast<const float4*>(L.w_router + (long)e * d);
       double a0 = 0.0, a1 = 0.0;
@@ -688,6 +689,404 @@ __global__ void __launch_bounds__(256) router_finish_kernel(RouterLaunch L, int 
   router_select_and_xn<EW>(L, lg, s_r, s_xn, s_wsq, rs, t0, rows, chain);
 }
 
+// ============================================================================
+// Exact int8 tensor-core router (E <= 64, d % 128 == 0, k <= 8).
+//
+// Fixed point, exactly: with s_t, s_e powers of two (|x_t| / s_t < 1, |w_e| / s_e < 1,
+// w_e = gamma (.) W_R[e] formed exactly in fp64), truncating base-2^7 digits give
+//   x_t / s_t = sum_{i<3} a_i 2^{-7(i+1)} + dx,   w_e / s_e = sum_{j<3} b_j 2^{-7(j+1)} + dw,
+// a_i, b_j in [-127, 127] (int8), |dx|, |dw| < 2^-21 per element. Then
+//   l_te = r_t s_t s_e ( sum_{i+j<=3} 2^{-7(i+j+2)} <a_i, b_j>  + err ),
+//   |err| <= 2^-21 (||x_t/s_t||_1 + ||w_e/s_e||_1 + 2d 2^-21) + d 2^-42 + 2^-42 127^2 d
+// where every <a_i, b_j> is an exact int32 tensor-core sum (|.| <= 127^2 d), pairs with
+// equal i + j share one TMEM accumulator (4 x 64 columns) and the one dropped pair
+// (2, 2) is bounded by the last term. That bound (~2e-4 of the logit scale, vs ~7e-4
+// for the fp32 SIMT chain) decides the band exactly as in the SIMT path; flagged
+// tokens go through the same fp64 refine_block. One CTA = 128 tokens (TMEM lanes) x
+// 64 padded experts x a 1/nsplit slice of d: warp 0 TMA (3-stage ring of 3 + 3
+// planes), warp 1 MMA (8 plane pairs x 4 K-steps of 32 per 128-wide k-block), warps
+// 2-5 epilogue (one thread per token). nsplit > 1 (to fill the SMs): each CTA writes
+// its int32 partial sums; the last CTA of a token block (ticket) adds them - integer
+// sums, so exact and order-free - then combines in fp64, selects and refines.
+namespace {
+constexpr int I8_BM = 128, I8_EP = 64, I8_BK = 128, I8_NP = 3, I8_NACC = 2 * I8_NP - 2;   // 4 accumulators
+constexpr int I8_A_TILE = I8_BM * I8_BK;                    // 16 KB
+constexpr int I8_B_TILE = I8_EP * I8_BK;                    // 8 KB
+constexpr int I8_STAGE = I8_NP * (I8_A_TILE + I8_B_TILE);   // 72 KB
+constexpr int I8_STAGES = 3;
+constexpr int I8_LGS = I8_EP + 4;
+constexpr int I8_THREADS = 192;
+constexpr int I8_SMEM = 1024 + I8_STAGES * I8_STAGE + 256;
+constexpr int I8_ACC_COLS = I8_NACC * I8_EP;                // 256 int32 per token
+constexpr int I8_MAX_SPLIT = 8;
+
+template <typename F>
+FSC_DEVINL void split3(F v, int8_t (&q)[I8_NP]) {   // |v| < 1: truncating base-128 digits, exact
+#pragma unroll
+  for (int i = 0; i < I8_NP; ++i) {
+    v *= (F)128;
+    const F t = trunc(v);
+    q[i] = (int8_t)(int)t;
+    v -= t;
+  }
+}
+}  // namespace
+
+// Per token (one warp): r_t, s_t, ||x_t/s_t||_1, xn = bf16(x gamma r) and the planes of x_t/s_t.
+__global__ void __launch_bounds__(256) router_i8_quant_x_kernel(RouterLaunch L) {
+  const int lane = threadIdx.x & 31;
+  const long t = (long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= L.T) return;
+  const int d = L.d, dv = d / 4;
+  const float4* x4 = reinterpret_cast<const float4*>(L.x + t * d);
+  const float4* g4 = reinterpret_cast<const float4*>(L.gamma);
+  double ss = 0.0;
+  float mx = 0.f;
+  for (int c0 = lane; c0 < dv; c0 += 128) {           // 4 float4 per lane in flight
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = c0 + 32 * u < dv ? x4[c0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      ss += ((double)v[u].x * v[u].x + (double)v[u].y * v[u].y) + ((double)v[u].z * v[u].z + (double)v[u].w * v[u].w);
+      mx = fmaxf(fmaxf(mx, fmaxf(fabsf(v[u].x), fabsf(v[u].y))), fmaxf(fabsf(v[u].z), fabsf(v[u].w)));
+    }
+  }
+  ss = warp_sum_f64(ss);
+  mx = warp_max_f32(mx);
+  const double r = 1.0 / sqrt(ss / (double)d + (double)L.eps);
+  const float rf = (float)r;
+  int ex = 0;
+  frexpf(mx, &ex);                                   // mx = m 2^ex, m in [0.5, 1)
+  const float st = mx > 0.f ? ldexpf(1.f, ex) : 1.f;  // |x| / st < 1
+  const float inv = 1.f / st;                        // exact (power of two)
+  float l1 = 0.f;
+  uint2* xo = reinterpret_cast<uint2*>(L.xn + t * d);
+  for (int c0 = lane; c0 < dv; c0 += 128) {
+    float4 v[4], g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = c0 + 32 * u < dv;
+      v[u] = ok ? x4[c0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+      g[u] = ok ? g4[c0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 32 * u;
+      if (c >= dv) break;
+      xo[c] = make_uint2(pack_bf16x2(v[u].x * g[u].x * rf, v[u].y * g[u].y * rf),
+                         pack_bf16x2(v[u].z * g[u].z * rf, v[u].w * g[u].w * rf));
+      int8_t q0[I8_NP], q1[I8_NP], q2[I8_NP], q3[I8_NP];
+      split3(v[u].x * inv, q0);
+      split3(v[u].y * inv, q1);
+      split3(v[u].z * inv, q2);
+      split3(v[u].w * inv, q3);
+      l1 += (fabsf(v[u].x) + fabsf(v[u].y) + fabsf(v[u].z) + fabsf(v[u].w)) * inv;
+#pragma unroll
+      for (int i = 0; i < I8_NP; ++i) {
+        const uint32_t pk = (uint32_t)(uint8_t)q0[i] | ((uint32_t)(uint8_t)q1[i] << 8) |
+                            ((uint32_t)(uint8_t)q2[i] << 16) | ((uint32_t)(uint8_t)q3[i] << 24);
+        reinterpret_cast<uint32_t*>(L.i8_x + ((long)i * L.T + t) * d)[c] = pk;
+      }
+    }
+  }
+  l1 = warp_sum_f32(l1);
+  if (lane == 0) {
+    L.i8_tok[t] = st;
+    L.i8_tok[L.T + t] = l1 * 1.0001f + 1e-6f;          // rounding of the fp32 sum, upward
+    L.i8_tok[2 * L.T + t] = rf;
+    L.i8_r[t] = r;
+  }
+}
+
+// Per padded expert (one CTA): w = gamma (.) W_R[e] exactly in fp64, s_e, the planes of
+// w / s_e and the per-expert error-bound coefficients; zero planes for e >= E.
+__global__ void __launch_bounds__(256) router_i8_quant_w_kernel(RouterLaunch L) {
+  __shared__ double red_l1[8];
+  __shared__ float red_mx[8];
+  const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int d = L.d;
+  float mx = 0.f;
+  if (e < L.E)
+    for (int c = tid; c < d; c += 256)
+      mx = fmaxf(mx, (float)fabs((double)L.gamma[c] * (double)L.w_router[(long)e * d + c]));
+  mx = warp_max_f32(mx);
+  if (lane == 0) red_mx[warp] = mx;
+  __syncthreads();
+  mx = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) mx = fmaxf(mx, red_mx[w]);
+  // (float)|w| may round up to the next power of two: frexp of the rounded max is then
+  // one binade higher, which still satisfies |w| / s_e < 1
+  int ex = 0;
+  frexpf(mx, &ex);
+  const double se = mx > 0.f ? ldexp(1.0, ex) : 1.0;
+  const double inv = 1.0 / se;
+  double l1 = 0.0;
+  for (int c = tid; c < d; c += 256) {
+    int8_t q[I8_NP] = {};
+    if (e < L.E) {
+      const double v = (double)L.gamma[c] * (double)L.w_router[(long)e * d + c] * inv;
+      split3(v, q);
+      l1 += fabs(v);
+    }
+#pragma unroll
+    for (int j = 0; j < I8_NP; ++j) L.i8_w[((long)j * I8_EP + e) * d + c] = q[j];
+  }
+  l1 = warp_sum_f64(l1);
+  if (lane == 0) red_l1[warp] = l1;
+  __syncthreads();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < 8; ++w) tot += red_l1[w];
+    const double u21 = ldexp(1.0, -21), u42 = ldexp(1.0, -42);
+    L.i8_exp[e] = (float)se;
+    L.i8_exp[I8_EP + e] = e < L.E ? (float)(se * u21 * 1.0001) : 0.f;
+    L.i8_exp[2 * I8_EP + e] =
+        e < L.E ? (float)(se * (u21 * (tot * 1.0001 + 2.0 * d * u21) + d * u42 + u42 * 127.0 * 127.0 * d) * 1.0001)
+                : 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(I8_THREADS, 1)
+    router_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, RouterLaunch L) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                        // [stage][plane][128][128]
+  uint8_t* sB = smem + I8_STAGES * I8_NP * I8_A_TILE;        // [stage][plane][64][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + I8_STAGES * I8_STAGE);
+  uint64_t* empty = full + I8_STAGES;
+  uint64_t* tfull = empty + I8_STAGES;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tfull + 1);
+  int* s_last = reinterpret_cast<int*>(s_tmem + 1);
+  float* lg = reinterpret_cast<float*>(smem);                // [128][I8_LGS] after the MMAs (stages free)
+  __shared__ RefineSmemT<I8_BM> rs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
+  const int blk = blockIdx.x, nsplit = gridDim.y, split = blockIdx.y;
+  const long t0 = (long)blk * I8_BM;
+  const int rows = (int)min((long)I8_BM, (long)L.T - t0);
+  const int nkb = L.d / I8_BK;
+  const int kb0 = split * nkb / nsplit, kb1 = (split + 1) * nkb / nsplit;
+  if (tid < I8_BM) rs.flag[tid] = 0;
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int st = 0; st < I8_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  } else if (warp == 1) {
+    tmem_alloc<I8_ACC_COLS>(s_tmem);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+  if (warp == 0) {
+    if (elect_one()) {                                     // TMA producer
+      int st = 0;
+      uint32_t ph = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full[st], I8_STAGE);
+#pragma unroll
+        for (int i = 0; i < I8_NP; ++i)
+          tma_load_2d(sA + (st * I8_NP + i) * I8_A_TILE, &tmA, &full[st], kb * I8_BK, (int)(i * L.T + t0),
+                      kEvictNormal);
+#pragma unroll
+        for (int j = 0; j < I8_NP; ++j)
+          tma_load_2d(sB + (st * I8_NP + j) * I8_B_TILE, &tmB, &full[st], kb * I8_BK, j * I8_EP, kEvictLast);
+        if (++st == I8_STAGES) { st = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {                                     // MMA issuer
+      const uint32_t idesc = idesc_s8_s32(I8_BM, I8_EP);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[st], ph);
+        tc_fence_after();
+        uint32_t touched = kb > kb0 ? 0xFu : 0u;
+#pragma unroll
+        for (int i = 0; i < I8_NP; ++i)
+#pragma unroll
+          for (int j = 0; j < I8_NP; ++j) {
+            if (i + j >= I8_NACC) continue;               // the dropped pair (2, 2)
+            const uint32_t a = smem_u32(sA + (st * I8_NP + i) * I8_A_TILE);
+            const uint32_t b = smem_u32(sB + (st * I8_NP + j) * I8_B_TILE);
+#pragma unroll
+            for (int kk = 0; kk < I8_BK / 32; ++kk)
+              umma_s8_ss(tmem + (i + j) * I8_EP, umma_desc_sw128(a + kk * 32), umma_desc_sw128(b + kk * 32), idesc,
+                         (kk > 0 || ((touched >> (i + j)) & 1u)) ? 1u : 0u);
+            touched |= 1u << (i + j);
+          }
+        umma_commit(&empty[st]);
+        if (++st == I8_STAGES) { st = 0; ph ^= 1; }
+      }
+      umma_commit(tfull);
+    }
+  } else if (nsplit > 1) {                                 // warps 2-5: write this split's int32 partials
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int q = warp & 3, row = q * 32 + lane;
+    const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
+    uint4* dst = reinterpret_cast<uint4*>(L.i8_part + ((long)split * L.T + t0 + row) * I8_ACC_COLS);
+#pragma unroll 1
+    for (int c = 0; c < I8_ACC_COLS; c += 16) {
+      uint32_t S[16];
+      tmem_ld16(tb + c, S);
+      tmem_ld_wait();
+      if (row < rows)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dst[c / 4 + u] = make_uint4(S[4 * u], S[4 * u + 1], S[4 * u + 2], S[4 * u + 3]);
+    }
+  }
+  tc_fence_before();
+  if (nsplit > 1) {                                        // last CTA of the token block finishes it
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const int prev = atomicAdd(L.i8_cnt + blk, 1);
+      *s_last = prev == nsplit - 1;
+      if (prev == nsplit - 1) L.i8_cnt[blk] = 0;
+    }
+    __syncthreads();
+    if (!*s_last) {
+      if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<I8_ACC_COLS>(tmem);
+      }
+      return;
+    }
+    __threadfence();
+  }
+  if (warp >= 2) {                                         // combine in fp64 (thread = token)
+    if (nsplit == 1) {
+      mbar_wait(tfull, 0);
+      tc_fence_after();
+    }
+    const int q = warp & 3, row = q * 32 + lane;
+    const long t = t0 + row;
+    const bool valid = row < rows;
+    const double sc = valid ? L.i8_r[t] * (double)L.i8_tok[t] : 0.0;
+    const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+    for (int e0 = 0; e0 < I8_EP; e0 += 16) {
+      int S[I8_NACC][16];
+      if (nsplit == 1) {
+#pragma unroll
+        for (int a = 0; a < I8_NACC; ++a) tmem_ld16(tb + a * I8_EP + e0, reinterpret_cast<uint32_t(&)[16]>(S[a]));
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int a = 0; a < I8_NACC; ++a)
+#pragma unroll
+          for (int u = 0; u < 16; ++u) S[a][u] = 0;
+        if (valid)
+          for (int sp = 0; sp < nsplit; ++sp) {
+            const int4* src = reinterpret_cast<const int4*>(L.i8_part + ((long)sp * L.T + t) * I8_ACC_COLS);
+#pragma unroll
+            for (int a = 0; a < I8_NACC; ++a)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int4 v = __ldcg(src + (a * I8_EP + e0) / 4 + u);
+                S[a][4 * u] += v.x;
+                S[a][4 * u + 1] += v.y;
+                S[a][4 * u + 2] += v.z;
+                S[a][4 * u + 3] += v.w;
+              }
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const double v = (double)S[0][u] * 0x1p-14 + (double)S[1][u] * 0x1p-21 + (double)S[2][u] * 0x1p-28 +
+                         (double)S[3][u] * 0x1p-35;
+        lg[row * I8_LGS + e0 + u] = (float)(sc * (double)L.i8_exp[e0 + u] * v);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();                                         // all logits in shared memory
+  if (warp >= 2) {
+    const int q = warp & 3, row = q * 32 + lane;
+    if (row < rows) {
+      const long t = t0 + row;
+      const float l1x = L.i8_tok[L.T + t];
+      float bmax = 0.f;
+      for (int e = 0; e < L.E; ++e) bmax = fmaxf(bmax, fmaf(L.i8_exp[I8_EP + e], l1x, L.i8_exp[2 * I8_EP + e]));
+      const float B = (float)(L.i8_r[t] * (double)L.i8_tok[t] * (double)bmax * 1.0001) + 1e-12f;
+      const float* rowp = lg + row * I8_LGS;
+      switch (L.k) {
+        case 1: select_token_thread<2>(rowp, t, row, B, L, rs); break;
+        case 2: select_token_thread<3>(rowp, t, row, B, L, rs); break;
+        case 3: select_token_thread<4>(rowp, t, row, B, L, rs); break;
+        case 4: select_token_thread<5>(rowp, t, row, B, L, rs); break;
+        case 5: select_token_thread<6>(rowp, t, row, B, L, rs); break;
+        case 6: select_token_thread<7>(rowp, t, row, B, L, rs); break;
+        case 7: select_token_thread<8>(rowp, t, row, B, L, rs); break;
+        default: select_token_thread<9>(rowp, t, row, B, L, rs); break;
+      }
+    }
+  }
+  __syncthreads();
+  refine_block<2>(L, lg, I8_LGS, rs, t0, rows);
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<I8_ACC_COLS>(tmem);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 i8_get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// int8 [rows, cols] row-major map, {128 cols x box_rows} box, 128B swizzle
+static bool i8_make_map(CUtensorMap* m, const void* base, long rows, long cols, int box_rows) {
+  auto enc = i8_get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols};
+  cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static cudaError_t launch_router_i8(const RouterLaunch& L, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  if (!i8_make_map(&ma, L.i8_x, (long)I8_NP * L.T, L.d, I8_BM)) return cudaErrorInvalidValue;
+  if (!i8_make_map(&mb, L.i8_w, (long)I8_NP * I8_EP, L.d, I8_EP)) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(router_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int nblk = (L.T + I8_BM - 1) / I8_BM;
+  int nsplit = kNumSMs / nblk;                                 // fill the SMs: split d across CTAs
+  if (nsplit > I8_MAX_SPLIT) nsplit = I8_MAX_SPLIT;
+  if (nsplit > L.d / I8_BK) nsplit = L.d / I8_BK;
+  if (nsplit < 1 || (long)nsplit * L.T > kI8SplitRows) nsplit = 1;
+  router_i8_quant_w_kernel<<<I8_EP, 256, 0, s>>>(L);
+  router_i8_quant_x_kernel<<<(L.T + 7) / 8, 256, 0, s>>>(L);
+  router_i8_kernel<<<dim3(nblk, nsplit), I8_THREADS, I8_SMEM, s>>>(ma, mb, L);
+  g_launches += 3;
+  return cudaGetLastError();
+}
+
 template <int EW>
 static cudaError_t launch_router_t(const RouterLaunch& L, cudaStream_t s) {
   constexpr int EP = 32 * EW, NS = EW >= 4 ? 2 : 4, NEH = EP >= 64 ? EP / 64 : 1, KS = 8 / NEH;
@@ -736,6 +1135,7 @@ cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s) {
   if (L.d % DC || L.d > kMaxD || L.E < 1 || L.E > 128 || L.k < 1 || L.k > L.E) return cudaErrorInvalidValue;
   if (!L.part || !L.part_sq || !L.w_scaled || !L.w_sq)
     return cudaErrorInvalidValue;
+  if (L.i8_x && L.E <= 64 && L.d % 128 == 0 && L.k <= 8) return launch_router_i8(L, s);
   if (L.E <= 32) return launch_router_t<1>(L, s);   // padded to 32 / 64 / 128 (zero W' columns)
   if (L.E <= 64) return launch_router_t<2>(L, s);
   return launch_router_t<4>(L, s);

@@ -35,19 +35,28 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Layout {  // byte offsets inside every rank's symmetric region
-  size_t flags, cnt, ret, xr, ys, total;
+  size_t flags, cnt, ret, xr, ys, part, red, total;
 };
+
+constexpr int kFlagRows = 5;   // FLAG_CNT, FLAG_DISP, FLAG_COMB, FLAG_AR_READY, FLAG_AR_DONE
 
 Layout layout_for(const fsc_ctx* c) {
   Layout L{};
-  const size_t P = c->ep, E = c->cfg.n_experts, d = c->cfg.d;
-  const size_t Tk = (size_t)c->cfg.max_tokens * c->cfg.top_k;
-  L.flags = 0;                                       // int [3][kMaxP]
-  L.cnt = align_up(L.flags + (3 * kMaxP + 1) * sizeof(int));   // 3 flag rows + epoch
+  const size_t P = c->ep, E = c->cfg.n_experts, d = c->cfg.d, T = c->cfg.max_tokens;
+  const size_t Tk = T * c->cfg.top_k;
+  L.flags = 0;                                       // int [kFlagRows][kMaxP] + epoch
+  L.cnt = align_up(L.flags + (kFlagRows * kMaxP + 1) * sizeof(int));
+  if (c->ep_mode == FSC_EP_ALLREDUCE) {              // replicated tokens: fp32 partial + reduced rows
+    L.ret = L.xr = L.ys = L.cnt;
+    L.part = L.cnt;
+    L.red = align_up(L.part + T * d * sizeof(float));
+    L.total = align_up(L.red + T * d * sizeof(float));
+    return L;
+  }
   L.ret = align_up(L.cnt + P * E * sizeof(int));     // int [max_recv]
   L.xr = align_up(L.ret + (size_t)c->max_recv * sizeof(int));
   L.ys = align_up(L.xr + (size_t)c->max_recv * d * 2);
-  L.total = align_up(L.ys + Tk * d * 2);
+  L.part = L.red = L.total = align_up(L.ys + Tk * d * 2);
   return L;
 }
 
@@ -55,8 +64,8 @@ struct Peers {
   char* base[kMaxP];
 };
 
-enum { FLAG_CNT = 0, FLAG_DISP = 1, FLAG_COMB = 2 };
-constexpr int kEpochSlot = 3 * kMaxP;   // int index of the epoch counter in the flags area
+enum { FLAG_CNT = 0, FLAG_DISP = 1, FLAG_COMB = 2, FLAG_AR_READY = 3, FLAG_AR_DONE = 4 };
+constexpr int kEpochSlot = kFlagRows * kMaxP;   // int index of the epoch counter in the flags area
 
 FSC_DEVINL int read_epoch(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
@@ -183,6 +192,73 @@ __global__ void ep_wait_kernel(char* mybase, int slot, int P, const int* epoch_p
   __syncthreads();
 }
 
+// ----------------------------------------------------------------------------- EP all-reduce (inference variant)
+// PAPER.md:215-217 (vLLM): activations replicated on every rank, experts EP-sharded;
+// each rank's local-expert partial sum is all-reduced. Reduce-scatter + all-gather
+// over peer memory in one kernel: rank p sums rows [p T/P, (p+1) T/P) of the P
+// partials IN RANK ORDER (deterministic, identical on every rank) and stores the
+// result into every rank's `red` buffer; the last CTA raises FLAG_AR_DONE there.
+
+// bump the epoch and announce "my partial is complete" (stream order after the unpermute)
+__global__ void ar_begin_kernel(Peers peers, int rank, int P, int* epoch_ptr) {
+  __shared__ int s_epoch;
+  if (threadIdx.x == 0) {
+    s_epoch = read_epoch(epoch_ptr) + 1;
+    *epoch_ptr = s_epoch;
+  }
+  __syncthreads();
+  __threadfence_system();
+  if (threadIdx.x < P) st_release_sys(flag_ptr(peers.base[threadIdx.x], FLAG_AR_READY, rank), s_epoch);
+}
+
+__global__ void __launch_bounds__(256) ar_reduce_kernel(Peers peers, int rank, int P, long rows0, long rows1, int d,
+                                                        size_t off_part, size_t off_red, const int* epoch_ptr,
+                                                        int* ticket) {
+  const int epoch = read_epoch(epoch_ptr);
+  if (threadIdx.x == 0) wait_flags(peers.base[rank], FLAG_AR_READY, P, epoch);
+  __syncthreads();
+  const long dv = d / 4;
+  const long n = (rows1 - rows0) * dv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const long off = rows0 * dv + i;
+    float4 acc = __ldcv(reinterpret_cast<const float4*>(peers.base[0] + off_part) + off);
+    for (int p = 1; p < P; ++p) {
+      const float4 v = __ldcv(reinterpret_cast<const float4*>(peers.base[p] + off_part) + off);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    for (int p = 0; p < P; ++p) reinterpret_cast<float4*>(peers.base[p] + off_red)[off] = acc;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(ticket, 1) == (int)gridDim.x - 1) {
+      *ticket = 0;
+      __threadfence_system();
+      for (int p = 0; p < P; ++p) st_release_sys(flag_ptr(peers.base[p], FLAG_AR_DONE, rank), epoch);
+    }
+  }
+}
+
+// wait every rank's slice, then out = resid + reduced (fp32; resid may alias out)
+__global__ void __launch_bounds__(256) ar_finish_kernel(char* mybase, int P, const int* epoch_ptr, size_t off_red,
+                                                        const float* resid, float* out, long n4) {
+  if (threadIdx.x == 0) wait_flags(mybase, FLAG_AR_DONE, P, read_epoch(epoch_ptr));
+  __syncthreads();
+  const float4* red = reinterpret_cast<const float4*>(mybase + off_red);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+    const float4 r = __ldcv(red + i);
+    float4 a = resid ? reinterpret_cast<const float4*>(resid)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    a.x += r.x;
+    a.y += r.y;
+    a.z += r.z;
+    a.w += r.w;
+    reinterpret_cast<float4*>(out)[i] = a;
+  }
+}
+
 // ----------------------------------------------------------------------------- host side
 
 size_t fsc_transport_blob_size() { return sizeof(cudaIpcMemHandle_t); }
@@ -207,7 +283,7 @@ int fsc_transport_init(fsc_ctx* ctx) {
   ctx->peer = st;
   st->lay = layout_for(ctx);
   TCK(cudaMalloc(&st->local, st->lay.total));
-  TCK(cudaMemset(st->local, 0, st->lay.flags + (3 * kMaxP + 1) * sizeof(int)));
+  TCK(cudaMemset(st->local, 0, st->lay.flags + (kFlagRows * kMaxP + 1) * sizeof(int)));
   TCK(cudaIpcGetMemHandle(&st->my_handle, st->local));
   TCK(cudaMalloc(&st->send_base, sizeof(int) * ctx->cfg.n_experts));
   TCK(cudaMalloc(&st->ticket, sizeof(int)));
@@ -320,4 +396,47 @@ void fsc_transport_scatter_target(fsc_ctx* ctx, const int** ret, void** peer_out
   *ret = reinterpret_cast<const int*>(st->local + st->lay.ret);
   for (int p = 0; p < kMaxP; ++p)
     peer_out[p] = (p < ctx->ep && st->peers.base[p]) ? st->peers.base[p] + st->lay.ys : nullptr;
+}
+
+// ----------------------------------------------------------------------------- EP all-reduce (host)
+float* fsc_transport_ar_partial(fsc_ctx* ctx) {
+  return reinterpret_cast<float*>(ctx->peer->local + ctx->peer->lay.part);
+}
+
+int fsc_transport_ar_start(fsc_ctx* ctx, int T, cudaStream_t s) {
+  fsc_peer_state* st = ctx->peer;
+  if (!connected(ctx)) {
+    fsc_set_error(ctx, "EP transport not bootstrapped (fsc_bootstrap_export/import)");
+    return FSC_ERR_STATE;
+  }
+  const int P = ctx->ep, d = ctx->cfg.d;
+  const long r0 = (long)T * ctx->rank / P, r1 = (long)T * (ctx->rank + 1) / P;
+  g_launches += 2;
+  ar_begin_kernel<<<1, 32, 0, s>>>(st->peers, ctx->rank, P, epoch_ptr(ctx));
+  TCK(cudaGetLastError());
+  long blocks = ((r1 - r0) * (d / 4) + 255) / 256;
+  if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
+  if (blocks < 1) blocks = 1;
+  ar_reduce_kernel<<<(int)blocks, 256, 0, s>>>(st->peers, ctx->rank, P, r0, r1, d, st->lay.part, st->lay.red,
+                                                epoch_ptr(ctx), st->ticket);
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+int fsc_transport_ar_finish(fsc_ctx* ctx, int T, const float* resid, float* out, cudaStream_t s) {
+  fsc_peer_state* st = ctx->peer;
+  const long n4 = (long)T * ctx->cfg.d / 4;
+  long blocks = (n4 + 255) / 256;
+  if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+  if (blocks < 1) blocks = 1;
+  ++g_launches;
+  ar_finish_kernel<<<(int)blocks, 256, 0, s>>>(st->local, ctx->ep, epoch_ptr(ctx), st->lay.red, resid, out, n4);
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+// re-create the symmetric region for a new EP mode (before fsc_bootstrap_export)
+int fsc_transport_reinit(fsc_ctx* ctx) {
+  fsc_transport_finalize(ctx);
+  return fsc_transport_init(ctx);
 }

@@ -187,3 +187,88 @@ def test_ep_stack_schedules_bitwise_and_ep_invariant(world):
         for r in range(world):
             np.testing.assert_array_equal(res[r][f"{name}_ovl"], o1[r * sh.tokens:(r + 1) * sh.tokens])
     c1.close()
+
+
+# ----------------------------------------------------------------------------- EP all-reduce (inference variant)
+def _ar_worker(rank, world, port, shape, seed, outdir):
+    """every rank holds the SAME tokens; local experts only; all-reduce."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2511_11505_b200 import FSC_EP_ALLREDUCE, Context, MoeDebug
+    from tests.gpu_util import dev_f32, moe_weights_dev
+    e_loc = shape.n_experts // world
+    w = synth.moe_weights(shape, seed=seed, e0=rank * e_loc, e_loc=e_loc)
+    x = synth.tokens(shape, seed=seed, rank=0)            # replicated activations
+    T = x.shape[0]
+    ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
+                  shared_ffn=shape.shared_ffn, max_tokens=T, rank=rank, ep_size=world, device=0)
+    ctx.set_ep_mode(FSC_EP_ALLREDUCE)
+    ctx.connect()
+    wd = moe_weights_dev(w)
+    xin = dev_f32(x)
+    outs = []
+    for _ in range(2):                                    # epochs advance, buffers reused
+        out = torch.empty_like(xin)
+        dbg = MoeDebug(topk_idx=torch.empty(T, shape.top_k, dtype=torch.int32, device="cuda"),
+                       routed_out=torch.empty(T, shape.d, dtype=torch.float32, device="cuda"))
+        ctx.moe_forward_blocking(wd, xin, out, dbg)
+        outs.append(out)
+    fulls = []
+    for _ in range(2):
+        partial = xin.clone()
+        h = ctx.moe_forward_farskip(wd, xin, partial)
+        full = torch.empty_like(xin)
+        ctx.moe_wait(h, partial, full)
+        fulls.append(full)
+    torch.cuda.synchronize()
+    np.savez(os.path.join(outdir, f"a{rank}.npz"), out0=outs[0].cpu().numpy(), out1=outs[1].cpu().numpy(),
+             idx=dbg.tensors["topk_idx"].cpu().numpy(), routed=dbg.tensors["routed_out"].cpu().numpy(),
+             full0=fulls[0].cpu().numpy(), full1=fulls[1].cpu().numpy())
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_allreduce_variant(world):
+    """Inference variant: replicated tokens, EP-sharded experts, routed
+    partials all-reduced over peer memory. Every rank ends with the SAME output (bit
+    for bit), equal to the dense MoE block (oracle) within the BJ tolerance and to
+    the EP=1 result within fp32 re-association; FarSkip (all-reduce in flight, waited
+    one sub-block later) == blocking bitwise; repeated calls identical."""
+    from paper_2511_11505_b200 import Context, build
+    from tests.gpu_util import dev_f32, moe_weights_dev
+    build.build()
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as td:
+        ps = [ctx.Process(target=_ar_worker, args=(r, world, port, SHAPE, 0, td)) for r in range(world)]
+        for p in ps:
+            p.start()
+        for p in ps:
+            p.join(timeout=600)
+        assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+        res = [dict(np.load(os.path.join(td, f"a{r}.npz"))) for r in range(world)]
+    x = synth.tokens(SHAPE, seed=0, rank=0)
+    wfull = synth.moe_weights(SHAPE, seed=0)
+    lay = om.layer_from_synth(wfull, SHAPE.top_k)
+    sh, ro, rt = om.moe_block(x, lay)
+    ref = (x.astype(np.float64) + sh) + ro
+    for r in range(world):
+        np.testing.assert_array_equal(res[r]["idx"], rt.idx)
+        assert rel_l2(res[r]["out0"], ref) < 1e-2
+        assert rel_l2(res[r]["routed"], ro) < 1e-2
+        for key in ("out1", "full0", "full1"):
+            np.testing.assert_array_equal(res[r][key], res[r]["out0"])
+        np.testing.assert_array_equal(res[r]["out0"], res[0]["out0"])   # replicated result
+    c1 = Context(d=SHAPE.d, n_experts=SHAPE.n_experts, top_k=SHAPE.top_k, ffn=SHAPE.ffn,
+                 shared_ffn=SHAPE.shared_ffn, max_tokens=x.shape[0])
+    xin = dev_f32(x)
+    o1 = torch.empty_like(xin)
+    c1.moe_forward_blocking(moe_weights_dev(wfull), xin, o1)
+    torch.cuda.synchronize()
+    c1.close()
+    assert rel_l2(res[0]["out0"], o1.cpu().numpy()) < 1e-6

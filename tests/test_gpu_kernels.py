@@ -160,8 +160,32 @@ ROUTER_CASES = [("tiny", 32), ("tiny", 1), ("dsv2lite", 700), ("qwen3", 513), ("
                 ("qwen3", 2400), ("dsv2lite", 4800), ("qwen3", 6000), ("scout", 5000)]
 
 
+@pytest.fixture(scope="module")
+def ctx_i8():
+    """E <= 64 and d % 128 == 0: the exact int8 tensor-core router (router_i8_kernel)."""
+    from paper_2511_11505_b200 import Context
+    c = Context(d=5120, n_experts=64, top_k=8, ffn=128, shared_ffn=0, max_tokens=8192)
+    c.set_router_int8(True)
+    yield c
+    c.close()
+
+
 @pytest.mark.parametrize("name,T", ROUTER_CASES)
 def test_router_parity(ctx, name, T):
+    _router_parity(ctx, name, T)
+
+
+@pytest.mark.parametrize("name,T", [c for c in ROUTER_CASES if c[0] in ("dsv2lite", "scout")] +
+                         [("dsv2lite", 8192), ("scout", 8192), ("dsv2lite", 129)])
+def test_router_parity_int8(ctx_i8, name, T):
+    """Exact int8 tensor-core path: same bit-exact indices; the logits' error is bounded
+    by ~2e-4 of their scale (three 7-bit planes), so few tokens need the fp64 refinement."""
+    nref, e_max = _router_parity(ctx_i8, name, T)
+    assert e_max < 5e-5
+    assert nref <= max(4, T // 50)
+
+
+def _router_parity(ctx, name, T):
     shape = synth.CONFIGS[name]
     w = synth.moe_weights(dataclass_replace_small(shape), seed=1)
     x = synth.tokens(shape, seed=1, T=T)
@@ -191,6 +215,7 @@ def test_router_parity(ctx, name, T):
     got = host_bf16_to_f64(xn)
     assert np.all(np.abs(got - xo) <= np.abs(xo) * 2.0 ** -7 + 1e-30)
     print(f"{name} T={T}: excluded={int(excl.sum())} refined={int(nref.item())} e_max={e_max:.2e}")
+    return int(nref.item()), e_max
 
 
 def dataclass_replace_small(shape):

@@ -246,3 +246,26 @@ def test_fused_unpermute_is_bitwise_identical(name, T):
         got, _ = run_blocking(ctx, w, x)
         assert np.array_equal(got, ref)
     ctx.close()
+
+
+@pytest.mark.parametrize("name,T", [("dsv2lite", 512), ("scout", 300)])
+def test_int8_router_moe_parity(name, T):
+    """The whole MoE block with the int8 tensor-core router: routing bit-exact against
+    the fp64 oracle and the output within tolerance; identical to the SIMT-router run
+    whenever both select the same experts (they do here: both equal the oracle)."""
+    shape = synth.CONFIGS[name]
+    ctx = make_ctx(shape, T)
+    w = synth.moe_weights(shape, seed=6)
+    wd = moe_weights_dev(w)
+    x = synth.tokens(shape, seed=6, T=T)
+    ref_out, ref_dbg = run_blocking(ctx, wd, x)
+    ctx.set_router_int8(True)
+    out, dbg = run_blocking(ctx, wd, x)
+    ctx.close()
+    np.testing.assert_array_equal(dbg["topk_idx"], ref_dbg["topk_idx"])
+    lay = _layer_f32(w, shape.top_k)
+    r, _ = om.adopt_router(lay, x, dbg["topk_idx"])
+    np.testing.assert_array_equal(dbg["topk_idx"], r.idx)
+    sh, ro, _ = om.moe_block(x, lay, router=r)
+    assert rel_l2(out, (x.astype(np.float64) + sh) + ro) < TOL
+    assert rel_l2(out, ref_out) < 1e-5
