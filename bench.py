@@ -208,12 +208,18 @@ def run_gpu(args):
     w = synth.moe_weights(shape, seed=args.seed, e0=erank * e_loc, e_loc=e_loc)
     wd = moe_weights_dev(w, dev)
     del w
-    x = torch.from_numpy(synth.tokens(shape, seed=args.seed, rank=rank)).to(dev)
+    allreduce = args.ep_mode == "allreduce" and ep > 1
+    # all-reduce variant: every rank holds the same (replicated) tokens
+    x = torch.from_numpy(synth.tokens(shape, seed=args.seed, rank=0 if allreduce else rank)).to(dev)
     out = torch.empty_like(x)
     ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
                   shared_ffn=shape.shared_ffn, max_tokens=T, rank=erank, ep_size=ep, device=local)
     if ep > 1:
+        if allreduce:
+            from paper_2511_11505_b200 import FSC_EP_ALLREDUCE
+            ctx.set_ep_mode(FSC_EP_ALLREDUCE)
         ctx.connect()
+    tok_world = 1 if allreduce else world      # replicated tokens count once
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -287,7 +293,7 @@ def run_gpu(args):
     total_ms = float(sum(ms))
     total_ms = allreduce_max([total_ms], dev)[0]
     ms_per_step = total_ms / args.steps
-    value = T * world * args.steps / (total_ms / 1e3)
+    value = T * tok_world * args.steps / (total_ms / 1e3)
 
     # ---------------- per-phase (per-kernel) times
     phase = {}
@@ -334,7 +340,7 @@ def run_gpu(args):
     ctx.host_flush()
     e2e_s = time.perf_counter() - t0
     e2e_s = allreduce_max([e2e_s], dev)[0]
-    e2e_value = T * world * e2e_steps / e2e_s
+    e2e_value = T * tok_world * e2e_steps / e2e_s
     # synchronous variant (one call = H2D + forward + D2H + stream sync), for reference
     t0 = time.perf_counter()
     for i in range(3):
@@ -342,7 +348,7 @@ def run_gpu(args):
     e2e_sync_value = T * 3 / (time.perf_counter() - t0)
 
     stack = None
-    if args.stack_layers > 0 and shape.tokens % shape.seq_len == 0:
+    if args.stack_layers > 0 and shape.tokens % shape.seq_len == 0 and not allreduce:
         stack = stack_measure(ctx, shape, wd, x, args.stack_layers, max(3, min(args.steps, 8)), world, dev,
                               rank, args.seed)
 
@@ -362,6 +368,8 @@ def run_gpu(args):
     peak = peaks["bf16_tflops"]
     # dominant kernel: routed-expert GEMM1 with the fused SwiGLU epilogue (row a7)
     R = T * shape.top_k                                        # balanced routing: rows received per rank = T*k
+    if allreduce:
+        R = T * shape.top_k // ep                              # replicated tokens: local experts' rows only
     g1_flop = 2.0 * R * shape.d * 2 * shape.ffn
     g1_bytes = 2.0 * e_loc * 2 * shape.ffn * shape.d + 2.0 * R * shape.d + 2.0 * R * shape.ffn  # W1|W2, xs, h
     if gemm1_live:    # event-record nodes around GEMM1 in every replayed graph of the timed region
@@ -399,14 +407,19 @@ def run_gpu(args):
         roof["frac_of_sustained_peak"] = achieved / peaks.get("bf16_tflops_sustained", peak)
     exp_flop = 2.0 * R * shape.d * 3 * shape.ffn + 2.0 * T * shape.d * 3 * shape.shared_ffn
     a2a_bytes = 2.0 * 2 * R * shape.d * (ep - 1) / ep          # dispatch + combine bytes leaving a rank
+    if allreduce:
+        a2a_bytes = 2.0 * (ep - 1) / ep * T * shape.d * 4     # fp32 reduce-scatter + all-gather per rank
     w_bytes = 2.0 * 3 * shape.d * (e_loc * shape.ffn + shape.shared_ffn)
     layer_roof_ms = max(exp_flop / (peaks["bf16_tflops"] * 1e12), a2a_bytes / 770e9,
                         w_bytes / (peaks["hbm_gbs"] * 1e9)) * 1e3
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if allreduce else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": workload_config(shape, ep, world, "blocking"),
+        "config": dict(workload_config(shape, ep, world, "blocking"),
+                       **({"ep_mode": "allreduce (replicated tokens, P:215-217)", "global_tokens": T}
+                          if allreduce else {"ep_mode": "all-to-all (dispatch / combine)"})),
         "roofline": roof,
         "layer_roofline": {"expert_flop": exp_flop, "t_roof_ms": layer_roof_ms,
                            "a2a_bytes": a2a_bytes, "frac": layer_roof_ms / ms_per_step,
@@ -550,6 +563,8 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of a CUDA graph")
+    ap.add_argument("--ep-mode", default="a2a", choices=["a2a", "allreduce"],
+                    help="N > 1: all-to-all dispatch/combine (training path) or the all-reduce inference variant")
     ap.add_argument("--no-live-timing", action="store_true", help="no CUDA events inside the timed graphs")
     ap.add_argument("--stack-layers", type=int, default=4, help="0 disables the FarSkip-vs-blocking stack timing")
     args = ap.parse_args()

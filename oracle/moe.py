@@ -253,6 +253,34 @@ def moe_block_ep(x_per_rank: Sequence[np.ndarray], layer: EpLayer, n_ranks: int)
     return out
 
 
+def moe_block_allreduce(x: np.ndarray, layer: EpLayer, n_ranks: int):
+    """Inference variant of the EP MoE block (vLLM): the activations x
+    are replicated on every rank, rank p evaluates only its contiguous expert
+    block E_p (C-amb-9) and the partial outputs are summed by an all-reduce.
+
+    Per rank p: partial_p[t] = sum over slots j with e_j in E_p of g_tj MLP^{e_j}(xn_t);
+    result = sum_p partial_p (rank order). Returns (shared_out, routed_out, router,
+    [partial_p]); the shared expert is evaluated replicated (no collective)."""
+    if layer.n_experts % n_ranks:
+        raise ValueError(f"n_experts={layer.n_experts} not divisible by n_ranks={n_ranks} (S:178)")
+    xn = rmsnorm(x, layer.gamma)
+    r = route(xn, layer.w_router, layer.top_k)
+    e_loc = layer.n_experts // n_ranks
+    partials = []
+    for p in range(n_ranks):
+        part = np.zeros_like(xn)
+        for j in range(layer.top_k):
+            for t in range(x.shape[0]):
+                e = int(r.idx[t, j])
+                if p * e_loc <= e < (p + 1) * e_loc:
+                    part[t] += r.gates[t, j] * swiglu(xn[t:t + 1], layer.w1[e], layer.w2[e], layer.w3[e])[0]
+        partials.append(part)
+    routed = np.zeros_like(xn)
+    for part in partials:
+        routed = routed + part
+    return shared_expert(xn, layer), routed, r, partials
+
+
 def moe_block(x: np.ndarray, layer: EpLayer, router: Optional[RouterOutput] = None):
     """Single-rank MoE block (EP=1) -> (shared_out, routed_out, RouterOutput).
 

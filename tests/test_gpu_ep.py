@@ -255,7 +255,7 @@ def test_ep_allreduce_variant(world):
     x = synth.tokens(SHAPE, seed=0, rank=0)
     wfull = synth.moe_weights(SHAPE, seed=0)
     lay = om.layer_from_synth(wfull, SHAPE.top_k)
-    sh, ro, rt = om.moe_block(x, lay)
+    sh, ro, rt, _ = om.moe_block_allreduce(x, lay, world)
     ref = (x.astype(np.float64) + sh) + ro
     for r in range(world):
         np.testing.assert_array_equal(res[r]["idx"], rt.idx)

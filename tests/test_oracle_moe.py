@@ -181,6 +181,31 @@ def test_ep_invariance(P):
     np.testing.assert_allclose(shared, ref[0], rtol=0, atol=1e-12)
 
 
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_allreduce_variant_equals_dense_and_partials_are_disjoint(P):
+    """P:215-217 inference variant: the all-reduced sum of the per-rank local-expert
+    partials is the dense brute-force MoE output (every token through every expert,
+    masked by its gates); each partial only holds its own experts' contributions
+    (zeroing every other rank's experts leaves it unchanged)."""
+    lay = _layer(12, 16, 8, 3, 10, 6, seed=7)
+    x = rng(8).standard_normal((12, 16))
+    sh, ro, r, parts = om.moe_block_allreduce(x, lay, P)
+    sh2, ro2, r2 = om.moe_block_dense(x, lay)
+    np.testing.assert_allclose(ro, ro2, rtol=0, atol=1e-12 * max(1, np.abs(ro2).max()))
+    np.testing.assert_allclose(sh, sh2, rtol=0, atol=0)
+    e_loc = 8 // P
+    for p in range(P):
+        lay_p = om.EpLayer(lay.gamma, lay.w_router, lay.w1.copy(), lay.w2.copy(), lay.w3.copy(), lay.ws1, lay.ws2,
+                           lay.ws3, top_k=lay.top_k)
+        mask = np.ones(8, bool)
+        mask[p * e_loc:(p + 1) * e_loc] = False
+        lay_p.w3[mask] = 0.0                    # other ranks' experts contribute exactly 0
+        _, ro_p, _ = om.moe_block(x, lay_p, router=r)
+        np.testing.assert_allclose(parts[p], ro_p, rtol=0, atol=1e-12 * max(1, np.abs(ro_p).max()))
+    with pytest.raises(ValueError):
+        om.moe_block_allreduce(x, lay, 3)
+
+
 def test_moe_block_equals_dense_brute_force():
     for (T, d, E, k, c, cs) in [(32, 64, 4, 2, 128, 0), (40, 16, 8, 3, 24, 32), (9, 8, 6, 6, 4, 0), (7, 8, 5, 1, 4, 4)]:
         lay = _layer(T, d, E, k, c, cs, seed=T)
