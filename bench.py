@@ -214,6 +214,8 @@ def run_gpu(args):
     out = torch.empty_like(x)
     ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
                   shared_ffn=shape.shared_ffn, max_tokens=T, rank=erank, ep_size=ep, device=local)
+    if args.cta_group:
+        ctx.set_gemm_cta_group(args.cta_group)
     if ep > 1:
         if allreduce:
             from paper_2511_11505_b200 import FSC_EP_ALLREDUCE
@@ -565,6 +567,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of a CUDA graph")
     ap.add_argument("--ep-mode", default="a2a", choices=["a2a", "allreduce"],
                     help="N > 1: all-to-all dispatch/combine (training path) or the all-reduce inference variant")
+    ap.add_argument("--cta-group", type=int, default=0, choices=[0, 1, 2], help="GEMM tcgen05 cta_group (0 = auto)")
     ap.add_argument("--no-live-timing", action="store_true", help="no CUDA events inside the timed graphs")
     ap.add_argument("--stack-layers", type=int, default=4, help="0 disables the FarSkip-vs-blocking stack timing")
     args = ap.parse_args()

@@ -145,8 +145,10 @@ FSC_API const char* fsc_last_error(const fsc_ctx* ctx);
  * co-running comm kernels ("communication operations only utilizing a
  * fraction of the total available units"). */
 FSC_API int fsc_set_gemm_ctas(fsc_ctx* ctx, int n);
-/* Grouped-GEMM tile mode: 2 (default) = CTA pairs with tcgen05 cta_group::2,
- * 256-row tiles; 1 = single-CTA 128-row tiles. Results are identical. */
+/* Grouped-GEMM tile mode: 2 = CTA pairs with tcgen05 cta_group::2, 256-row
+ * tiles; 1 = single-CTA 128-row tiles; 0 (default) = auto: the routed-expert
+ * GEMMs use pairs when the experts receive >= 256 rows on average (prefill) and
+ * single CTAs below (decode), every other GEMM uses pairs. Results are identical. */
 FSC_API int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg);
 /* EP = 1: on != 0 fuses the permute into GEMM1 (its TMA producer gathers the rows of
  * xn through src_row with tile::gather4) instead of the explicit permute kernel.

@@ -25,7 +25,7 @@ struct fsc_ctx {
   int e_loc = 0;
   long max_recv = 0;
   int gemm_ctas = 148;
-  int gemm_cg = 2;
+  int gemm_cg = 0;             // 0 = auto (routed GEMMs: pairs at prefill, single CTAs at decode), 1, 2
   int fuse_unpermute = -1;     // blocking EP = 1: unpermute fused into GEMM2 (-1 auto: top-1)
   int ep_mode = 0;             // FSC_EP_ALLTOALL (dispatch / combine) or FSC_EP_ALLREDUCE (replicated tokens)
   int router_i8 = 0;           // exact int8 tensor-core router (fsc_set_router_int8)

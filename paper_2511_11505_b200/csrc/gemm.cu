@@ -199,7 +199,8 @@ FSC_DEVINL void fused_unpermute(const GemmParams& p, long tok, int c0, int lane)
 template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-                        const __grid_constant__ CUtensorMap tmB1, GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmA32,
+                        const __grid_constant__ CUtensorMap tmA64, GemmParams p) {
   using C = Cfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -222,6 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (elect_one()) {
       tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmA32);
+      tma_prefetch_desc(&tmA64);
       tma_prefetch_desc(&tmB0);
       tma_prefetch_desc(&tmB1);
       for (int s = 0; s < C::STAGES; ++s) {
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int t = t_first; t < total; t += t_step) {
         TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
-      ti.row0 += rbase;
+        ti.row0 += rbase;
         const int arow = ti.row0 + (int)rank * BM;
         int brow0, brow1 = 0;
         const CUtensorMap* mb0 = &tmB0;
@@ -360,16 +363,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             brow1 = brow0 + C::HALF;
           }
         }
+        // A rows actually needed by each CTA of the tile: a ragged group end (decode:
+        // a few rows per expert) loads a 32 / 64-row box or nothing instead of 128 rows
+        // (rows past the group end are never stored; stale shared memory is harmless)
+        const int v0 = min(BM, ti.rows), v1 = min(BM, max(0, ti.rows - BM));
+        auto box_rows = [](int v) { return v == 0 ? 0 : (v <= 32 ? 32 : (v <= 64 ? 64 : BM)); };
+        const int mybox = box_rows(rank ? v1 : v0);
+        const CUtensorMap* ma = mybox == 32 ? &tmA32 : (mybox == 64 ? &tmA64 : &tmA);
+        const uint32_t a_bytes = (uint32_t)(box_rows(v0) + (CG == 2 ? box_rows(v1) : 0)) * BK * 2;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* b = sB + stage * C::B_BYTES;
           if (CG == 2) {
-            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-            tma_load_2d_2sm(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, arow, kEvictNormal);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::B_BYTES + a_bytes);
+            if (mybox) tma_load_2d_2sm(sA + stage * C::A_BYTES, ma, &full[stage], kb * BK, arow, kEvictNormal);
             tma_load_2d_2sm(b, mb0, &full[stage], kb * BK, brow0, kEvictLast);
           } else {
-            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, arow, kEvictNormal);
+            mbar_arrive_expect_tx(&full[stage], C::B_BYTES + a_bytes);
+            if (mybox) tma_load_2d(sA + stage * C::A_BYTES, ma, &full[stage], kb * BK, arow, kEvictNormal);
             tma_load_2d(b, mb0, &full[stage], kb * BK, brow0, kEvictLast);
             tma_load_2d(b + C::HALF * BK * 2, mb1, &full[stage], kb * BK, brow1, kEvictLast);
           }
@@ -563,9 +574,11 @@ static bool make_map(CUtensorMap* m, const void* base, long rows, long cols, int
 template <int BN, int EPI, int CG>
 static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   using C = Cfg<BN, CG>;
-  CUtensorMap ma, mb0, mb1;
+  CUtensorMap ma, mb0, mb1, ma32, ma64;
   long a_rows = L.a_rows > 0 ? L.a_rows : 1;
   if (!make_map(&ma, L.A, a_rows, L.K, L.a_idx ? 1 : BM)) return cudaErrorInvalidValue;   // gather4: {64, 1} box
+  if (!make_map(&ma32, L.A, a_rows, L.K, 32)) return cudaErrorInvalidValue;               // ragged group ends
+  if (!make_map(&ma64, L.A, a_rows, L.K, 64)) return cudaErrorInvalidValue;
   if (!make_map(&mb0, L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
   if (!make_map(&mb1, L.B1 ? L.B1 : L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
   auto kern = grouped_gemm_kernel<BN, EPI, CG>;
@@ -614,7 +627,7 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ++g_launches;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb0, mb1, p);
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb0, mb1, ma32, ma64, p);
 }
 
 int gemm_pick_bn(int epi, int N) {

@@ -91,7 +91,7 @@ int attention_a(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, co
   GemmLaunch g{};
   g.A = ctx->hn; g.a_rows = T; g.B0 = aw->w_qkv; g.b_rows = nqkv; g.b_group_rows = nqkv; g.K = d; g.N = nqkv;
   g.G = 1; g.m_total = T; g.out = ctx->qkv; g.ldo = nqkv; g.epi = EPI_BF16; g.num_ctas = ctx->gemm_ctas;
-  g.cta_group = ctx->gemm_cg;
+  g.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
   SCK(launch_grouped_gemm(g, s));
   SCK(launch_rope(ctx->qkv, T, Hq, Hkv, hd, seq_len, aw->rope_theta, s));
   return FSC_OK;
@@ -105,7 +105,7 @@ int attention_b(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, co
   GemmLaunch g{};
   g.A = ctx->ao; g.a_rows = T; g.B0 = aw->w_o; g.b_rows = d; g.b_group_rows = d; g.K = Hq * hd; g.N = d;
   g.G = 1; g.m_total = T; g.out = out; g.ldo = d; g.resid = resid; g.ldr = d; g.epi = EPI_RESID_F32;
-  g.num_ctas = ctx->gemm_ctas; g.cta_group = ctx->gemm_cg;
+  g.num_ctas = ctx->gemm_ctas; g.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
   SCK(launch_grouped_gemm(g, s));
   if (cache_attn_out) {
     g.out = cache_attn_out;
