@@ -191,6 +191,17 @@ FSC_DEVINL uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 FSC_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Relaxed arrives: no ordering of this thread's generic memory operations (no MEMBAR).
+// For the TMEM-empty handoff of the GEMM epilogue: the TMEM loads are complete
+// (tcgen05.wait::ld) and fenced (tcgen05.fence::before_thread_sync); the epilogue's
+// global stores need no ordering w.r.t. the MMA warp, and a release here would make
+// every epilogue warp wait for its stores to drain before the accumulator is reused.
+FSC_DEVINL void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+FSC_DEVINL void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // 2-SM TMA load: both CTAs of the pair load into their own smem; the bytes are
 // accounted on the leader CTA's barrier (peer bit cleared, as CUTLASS SM100_TMA_2SM_LOAD).
 FSC_DEVINL void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,

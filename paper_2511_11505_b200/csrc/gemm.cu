@@ -527,8 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
-        else mbar_arrive(&tempty[acc]);
+        if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
+        else mbar_arrive_relaxed(&tempty[acc]);
       }
     }
   }
