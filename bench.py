@@ -217,6 +217,8 @@ def run_gpu(args):
     if args.cta_group:
         ctx.set_gemm_cta_group(args.cta_group)
     if ep > 1:
+        if args.dispatch_fp8 and not allreduce:
+            ctx.set_dispatch_fp8(True)
         if allreduce:
             from paper_2511_11505_b200 import FSC_EP_ALLREDUCE
             ctx.set_ep_mode(FSC_EP_ALLREDUCE)
@@ -409,6 +411,8 @@ def run_gpu(args):
         roof["frac_of_sustained_peak"] = achieved / peaks.get("bf16_tflops_sustained", peak)
     exp_flop = 2.0 * R * shape.d * 3 * shape.ffn + 2.0 * T * shape.d * 3 * shape.shared_ffn
     a2a_bytes = 2.0 * 2 * R * shape.d * (ep - 1) / ep          # dispatch + combine bytes leaving a rank
+    if args.dispatch_fp8 and not allreduce:                    # dispatch: 1 B / element + scales
+        a2a_bytes = (R * shape.d * (1 + 4 / 128) + 2.0 * R * shape.d) * (ep - 1) / ep
     if allreduce:
         a2a_bytes = 2.0 * (ep - 1) / ep * T * shape.d * 4     # fp32 reduce-scatter + all-gather per rank
     w_bytes = 2.0 * 3 * shape.d * (e_loc * shape.ffn + shape.shared_ffn)
@@ -421,7 +425,9 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": dict(workload_config(shape, ep, world, "blocking"),
                        **({"ep_mode": "allreduce (replicated tokens, P:215-217)", "global_tokens": T}
-                          if allreduce else {"ep_mode": "all-to-all (dispatch / combine)"})),
+                          if allreduce else {"ep_mode": "all-to-all (dispatch / combine)",
+                                             "dispatch_payload": "fp8 e4m3 + per-128-col scales"
+                                             if (args.dispatch_fp8 and ep > 1) else "bf16"})),
         "roofline": roof,
         "layer_roofline": {"expert_flop": exp_flop, "t_roof_ms": layer_roof_ms,
                            "a2a_bytes": a2a_bytes, "frac": layer_roof_ms / ms_per_step,
@@ -567,6 +573,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of a CUDA graph")
     ap.add_argument("--ep-mode", default="a2a", choices=["a2a", "allreduce"],
                     help="N > 1: all-to-all dispatch/combine (training path) or the all-reduce inference variant")
+    ap.add_argument("--dispatch-fp8", action="store_true", help="N > 1 all-to-all: FP8 e4m3 dispatch payload")
     ap.add_argument("--cta-group", type=int, default=0, choices=[0, 1, 2], help="GEMM tcgen05 cta_group (0 = auto)")
     ap.add_argument("--no-live-timing", action="store_true", help="no CUDA events inside the timed graphs")
     ap.add_argument("--stack-layers", type=int, default=4, help="0 disables the FarSkip-vs-blocking stack timing")

@@ -173,6 +173,12 @@ FSC_API int fsc_set_router_int8(fsc_ctx* ctx, int on);
  * returns with the all-reduce in flight and fsc_moe_wait completes it (the
  * "synchronize only before the next MoE computation" of P:217). */
 FSC_API int fsc_set_ep_mode(fsc_ctx* ctx, int mode);
+/* EP > 1 all-to-all: on != 0 sends the Dispatch payload as FP8 e4m3 with one fp32
+ * scale per 128 columns (s = amax / 448, q = e4m3_rn_satfinite(x / s); the receiver
+ * rebuilds bf16(q * s)), halving the dispatch bytes (the paper's
+ * inference runs FP8). Lossy (e4m3): its own tolerance, parity against the
+ * oracle's moe_block_ep_fp8. d % 128 == 0. Call before fsc_bootstrap_export. */
+FSC_API int fsc_set_dispatch_fp8(fsc_ctx* ctx, int on);
 
 /* Per-phase CUDA-event timing of the MoE calls (bench / profiling). When enabled,
  * events are recorded on the call's stream around every phase; fsc_get_timings

@@ -225,6 +225,69 @@ def combine_sim(y_per_rank: Sequence[np.ndarray], gates: np.ndarray, dst_rank: n
     return out
 
 
+# ----------------------------------------------------------------------------
+# FP8 dispatch payload (the paper's inference runs FP8)
+# ----------------------------------------------------------------------------
+E4M3_MAX = 448.0
+FP8_BLOCK = 128
+
+
+def e4m3_rne(v: np.ndarray) -> np.ndarray:
+    """Round to the nearest OCP FP8 E4M3 value, ties to even, saturating to +-448
+    (cvt.rn.satfinite.e4m3). Normals 2^-6 .. 1.75 * 2^8 with 3 mantissa bits;
+    subnormals k * 2^-9, k = 1..7."""
+    v = np.asarray(v, np.float64)
+    a = np.abs(v)
+    with np.errstate(divide="ignore"):
+        e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+    e = np.maximum(e, -6.0)                                   # below 2^-6: the subnormal quantum 2^-9
+    quantum = np.exp2(e - 3.0)
+    q = np.rint(a / quantum) * quantum                        # rint = round half to even
+    q = np.minimum(q, E4M3_MAX)
+    return np.sign(v) * q
+
+
+def f32(x):
+    return np.asarray(x, np.float32)
+
+
+def bf16_rne(x) -> np.ndarray:
+    """Round float32 values to bfloat16, nearest-even (the kernels' cvt.rn.bf16.f32),
+    returned as float64. Finite inputs only."""
+    u = f32(x).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def fp8_dispatch_payload(xn_bf16: np.ndarray) -> np.ndarray:
+    """The FP8 dispatch payload as the receiving rank's GEMM sees it: per row and per
+    128-column block b, s_b = fp32(amax_b / 448) (1 if amax_b = 0), q = e4m3(fp32(x / s_b)),
+    x_hat = bf16(fp32(q * s_b)). Input: the bf16 rows (as float values)."""
+    x = f32(xn_bf16)
+    T, d = x.shape
+    if d % FP8_BLOCK:
+        raise ValueError("d must be a multiple of 128 for the FP8 payload")
+    xb = x.reshape(T, d // FP8_BLOCK, FP8_BLOCK)
+    amax = np.abs(xb).max(axis=2, keepdims=True)
+    s = np.where(amax > 0, f32(amax) / f32(E4M3_MAX), f32(1.0)).astype(np.float32)
+    q = e4m3_rne((xb / s).astype(np.float32))
+    xh = (f32(q) * s).astype(np.float32)
+    return bf16_rne(xh.reshape(T, d))
+
+
+def moe_block_ep_fp8(x_per_rank: Sequence[np.ndarray], layer: EpLayer, n_ranks: int):
+    """moe_block_ep with the FP8 dispatch payload: the rows sent to the experts are
+    fp8_dispatch_payload(bf16(xn)) instead of xn; the shared expert (local) and the
+    combine are unchanged. Returns [(shared_out_s, routed_out_s, RouterOutput_s)]."""
+    xns = [rmsnorm(x, layer.gamma) for x in x_per_rank]
+    routers = [route(xn, layer.w_router, layer.top_k) for xn in xns]
+    payload = [fp8_dispatch_payload(bf16_rne(xn)) for xn in xns]
+    recv, rc, dst_rank, dst_row, _ = dispatch_sim(payload, [r.idx for r in routers], layer.n_experts, n_ranks)
+    ys = [experts_on_rank(recv[p], rc[p], layer, p, n_ranks) for p in range(n_ranks)]
+    return [(shared_expert(xns[s], layer), combine_sim(ys, routers[s].gates, dst_rank[s], dst_row[s]), routers[s])
+            for s in range(n_ranks)]
+
+
 def shared_expert(xn: np.ndarray, layer: EpLayer) -> np.ndarray:
     """Shared experts 'process all tokens' (P:100-101) on the same xn (C-amb-7);
     n shared experts == one SwiGLU of concatenated width. Width 0 -> exact zeros."""

@@ -72,6 +72,7 @@ _SIGS = {
     "fsc_set_fused_unpermute": (_I, [_P, _I]),
     "fsc_set_router_int8": (_I, [_P, _I]),
     "fsc_set_ep_mode": (_I, [_P, _I]),
+    "fsc_set_dispatch_fp8": (_I, [_P, _I]),
     "fsc_set_timing": (_I, [_P, _I]),
     "fsc_set_timing_mask": (_I, [_P, ctypes.c_uint]),
     "fsc_get_timings": (_I, [_P, ctypes.POINTER(ctypes.c_float), _I]),
@@ -247,6 +248,10 @@ class Context:
     def set_gemm_gather(self, on: bool):
         """EP = 1: fuse the permute into GEMM1 (TMA gather4 of the xn rows)."""
         self._ck(self.lib.fsc_set_gemm_gather(self.h, int(on)))
+
+    def set_dispatch_fp8(self, on: bool):
+        """EP > 1 all-to-all: FP8 e4m3 dispatch payload with per-128-column scales. Call before connect()."""
+        self._ck(self.lib.fsc_set_dispatch_fp8(self.h, int(on)))
 
     def set_ep_mode(self, mode: int):
         """FSC_EP_ALLTOALL (Dispatch / Combine) or FSC_EP_ALLREDUCE (replicated tokens,

@@ -27,6 +27,7 @@ struct fsc_ctx {
   int gemm_ctas = 148;
   int gemm_cg = 0;             // 0 = auto (routed GEMMs: pairs at prefill, single CTAs at decode), 1, 2
   int fuse_unpermute = -1;     // blocking EP = 1: unpermute fused into GEMM2 (-1 auto: top-1)
+  int dispatch_fp8 = 0;        // FP8 (e4m3, per-128-column scales) dispatch payload, EP > 1 all-to-all
   int ep_mode = 0;             // FSC_EP_ALLTOALL (dispatch / combine) or FSC_EP_ALLREDUCE (replicated tokens)
   int router_i8 = 0;           // exact int8 tensor-core router (fsc_set_router_int8)
   int gather_a = 0;            // EP = 1: GEMM1 gathers A through src_row (fused permute)

@@ -265,6 +265,17 @@ extern "C" int fsc_set_ep_mode(fsc_ctx* ctx, int mode) {
   return fsc_transport_reinit(ctx);   // new symmetric layout: bootstrap (export / import) after this
 }
 
+extern "C" int fsc_set_dispatch_fp8(fsc_ctx* ctx, int on) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(!ctx->pending, FSC_ERR_STATE, "a FarSkip handle is outstanding");
+  REQUIRE(!on || ctx->cfg.d % 128 == 0, FSC_ERR_CONFIG, "FP8 dispatch needs d %% 128 == 0");
+  if ((on ? 1 : 0) == ctx->dispatch_fp8) return FSC_OK;
+  ctx->dispatch_fp8 = on ? 1 : 0;
+  if (ctx->ep == 1) return FSC_OK;
+  CK(cudaSetDevice(ctx->device));
+  return fsc_transport_reinit(ctx);   // new symmetric layout: bootstrap (export / import) after this
+}
+
 extern "C" int fsc_set_router_int8(fsc_ctx* ctx, int on) {
   if (!ctx) return FSC_ERR_SHAPE;
   const fsc_moe_config& c = ctx->cfg;

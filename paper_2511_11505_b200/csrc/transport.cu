@@ -21,6 +21,7 @@
 // memory (bumped by the counts kernel, read by the others), so a captured CUDA graph
 // of a whole layer replays correctly. The same code serves
 // P processes on one GPU (tests) and one process per GPU over NVLink/NVSwitch.
+#include <cuda_fp16.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -35,7 +36,7 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Layout {  // byte offsets inside every rank's symmetric region
-  size_t flags, cnt, ret, xr, ys, part, red, total;
+  size_t flags, cnt, ret, xr, ys, part, red, xq, xsc, total;
 };
 
 constexpr int kFlagRows = 5;   // FLAG_CNT, FLAG_DISP, FLAG_COMB, FLAG_AR_READY, FLAG_AR_DONE
@@ -56,7 +57,12 @@ Layout layout_for(const fsc_ctx* c) {
   L.ret = align_up(L.cnt + P * E * sizeof(int));     // int [max_recv]
   L.xr = align_up(L.ret + (size_t)c->max_recv * sizeof(int));
   L.ys = align_up(L.xr + (size_t)c->max_recv * d * 2);
-  L.part = L.red = L.total = align_up(L.ys + Tk * d * 2);
+  L.part = L.red = L.xq = L.xsc = L.total = align_up(L.ys + Tk * d * 2);
+  if (c->dispatch_fp8) {                             // FP8 payload: e4m3 rows + fp32 per-128-column scales
+    L.xq = L.total;
+    L.xsc = align_up(L.xq + (size_t)c->max_recv * d);
+    L.total = align_up(L.xsc + (size_t)c->max_recv * (d / 128) * sizeof(float));
+  }
   return L;
 }
 
@@ -178,6 +184,107 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(Peers peers, int rank,
       __threadfence_system();
       for (int p = 0; p < P; ++p) st_release_sys(flag_ptr(peers.base[p], FLAG_DISP, rank), epoch);
     }
+  }
+}
+
+// a4 + a6 with the FP8 payload: every row is sent as e4m3 with
+// one fp32 scale per 128 columns: s_b = amax_b / 448, q = e4m3_rn_satfinite(x / s_b)
+// (oracle/moe.py fp8_dispatch_payload). One warp per send row; a lane's 8 columns
+// lie in one 128-column block, so a half-warp reduction gives the block amax.
+FSC_DEVINL uint32_t f32x2_to_e4m3x2(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__global__ void __launch_bounds__(256) ep_dispatch_fp8_kernel(Peers peers, int rank, int P, int R, int d, int E,
+                                                              int e_loc, const int* epoch_ptr, size_t off_xq,
+                                                              size_t off_xsc, size_t off_ret,
+                                                              const uint4* __restrict__ xn,
+                                                              const int* __restrict__ src_row,
+                                                              const int* __restrict__ offsets,
+                                                              const int* __restrict__ send_base, int* ticket) {
+  __shared__ int s_off[129];
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) s_off[i] = offsets[i];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dv = d / 8;
+  for (long q = (long)blockIdx.x * 8 + w; q < R; q += (long)gridDim.x * 8) {
+    int lo = 0, hi = E;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[mid] <= q) lo = mid; else hi = mid;
+    }
+    const int e = lo, p = e / e_loc;
+    const long dst = send_base[e] + (q - s_off[e]);
+    const uint4* a = xn + (long)src_row[q] * dv;
+    uint2* bq = reinterpret_cast<uint2*>(peers.base[p] + off_xq) + dst * dv;
+    float* bs = reinterpret_cast<float*>(peers.base[p] + off_xsc) + dst * (d / 128);
+    for (int c0 = 0; c0 < dv; c0 += 32) {          // warp-uniform trip count (half-warp shuffles below)
+      const int c = c0 + lane;
+      const bool ok = c < dv;
+      const uint4 u = ok ? a[c] : make_uint4(0u, 0u, 0u, 0u);
+      float v[8] = {bf16lo(u.x), bf16hi(u.x), bf16lo(u.y), bf16hi(u.y),
+                    bf16lo(u.z), bf16hi(u.z), bf16lo(u.w), bf16hi(u.w)};
+      float m = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf(v[i]));
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));   // 16 lanes = 128 cols
+      const float sc = m > 0.f ? __fdiv_rn(m, 448.f) : 1.f;
+      uint32_t w01 = f32x2_to_e4m3x2(__fdiv_rn(v[0], sc), __fdiv_rn(v[1], sc));
+      uint32_t w23 = f32x2_to_e4m3x2(__fdiv_rn(v[2], sc), __fdiv_rn(v[3], sc));
+      uint32_t w45 = f32x2_to_e4m3x2(__fdiv_rn(v[4], sc), __fdiv_rn(v[5], sc));
+      uint32_t w67 = f32x2_to_e4m3x2(__fdiv_rn(v[6], sc), __fdiv_rn(v[7], sc));
+      if (ok) {
+        bq[c] = make_uint2(w01 | (w23 << 16), w45 | (w67 << 16));
+        if ((c & 15) == 0) bs[c / 16] = sc;
+      }
+    }
+    if (lane == 0) reinterpret_cast<int*>(peers.base[p] + off_ret)[dst] = (rank << 24) | (int)q;
+  }
+  const int epoch = read_epoch(epoch_ptr);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(ticket, 1) == (int)gridDim.x - 1) {
+      *ticket = 0;
+      __threadfence_system();
+      for (int p = 0; p < P; ++p) st_release_sys(flag_ptr(peers.base[p], FLAG_DISP, rank), epoch);
+    }
+  }
+}
+
+// receiver: xr = bf16(fp32(q * s)) for every received row (after the dispatch flags)
+__global__ void __launch_bounds__(256) ep_dequant_fp8_kernel(const uint2* __restrict__ xq, const float* __restrict__ xsc,
+                                                             const int* __restrict__ recv_counts, int e_loc,
+                                                             uint4* __restrict__ xr, int d) {
+  __shared__ long s_rows;
+  if (threadIdx.x == 0) {
+    long n = 0;
+    for (int i = 0; i < e_loc; ++i) n += recv_counts[i];
+    s_rows = n;
+  }
+  __syncthreads();
+  const int dv = d / 8;
+  const long items = s_rows * dv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < items; i += (long)gridDim.x * blockDim.x) {
+    const long r = i / dv;
+    const int c = (int)(i - r * dv);
+    const uint2 qq = __ldcv(xq + i);
+    const float sc = __ldcv(xsc + r * (d / 128) + c / 16);
+    float f[8];
+    const uint32_t wds[2] = {qq.x, qq.y};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const uint16_t pair = (uint16_t)(wds[h / 2] >> (16 * (h & 1)));
+      uint32_t hx2;
+      asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(hx2) : "h"(pair));
+      const __half2 h2 = *reinterpret_cast<const __half2*>(&hx2);
+      f[2 * h] = __low2float(h2) * sc;
+      f[2 * h + 1] = __high2float(h2) * sc;
+    }
+    xr[i] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                       pack_bf16x2(f[6], f[7]));
   }
 }
 
@@ -360,9 +467,15 @@ int fsc_transport_dispatch(fsc_ctx* ctx, int T, cudaStream_t s) {
   if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
   if (blocks < 1) blocks = 1;
   ++g_launches;
-  ep_dispatch_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, P, R, c.d, E, ctx->e_loc, epoch_ptr(ctx), st->lay.xr,
-                                            st->lay.ret, reinterpret_cast<const uint4*>(ctx->xn), ctx->src_row,
-                                            ctx->offsets, st->send_base, st->ticket);
+  if (ctx->dispatch_fp8)
+    ep_dispatch_fp8_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, P, R, c.d, E, ctx->e_loc, epoch_ptr(ctx),
+                                                  st->lay.xq, st->lay.xsc, st->lay.ret,
+                                                  reinterpret_cast<const uint4*>(ctx->xn), ctx->src_row, ctx->offsets,
+                                                  st->send_base, st->ticket);
+  else
+    ep_dispatch_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, P, R, c.d, E, ctx->e_loc, epoch_ptr(ctx),
+                                              st->lay.xr, st->lay.ret, reinterpret_cast<const uint4*>(ctx->xn),
+                                              ctx->src_row, ctx->offsets, st->send_base, st->ticket);
   TCK(cudaGetLastError());
   return FSC_OK;
 }
@@ -371,6 +484,16 @@ int fsc_transport_dispatch_wait(fsc_ctx* ctx, cudaStream_t s) {
   ++g_launches;
   ep_wait_kernel<<<1, 32, 0, s>>>(ctx->peer->local, FLAG_DISP, ctx->ep, epoch_ptr(ctx));
   TCK(cudaGetLastError());
+  if (ctx->dispatch_fp8) {
+    fsc_peer_state* st = ctx->peer;
+    const int d = ctx->cfg.d;
+    ++g_launches;
+    ep_dequant_fp8_kernel<<<4 * kNumSMs, 256, 0, s>>>(reinterpret_cast<const uint2*>(st->local + st->lay.xq),
+                                                      reinterpret_cast<const float*>(st->local + st->lay.xsc),
+                                                      ctx->recv_counts, ctx->e_loc,
+                                                      reinterpret_cast<uint4*>(st->local + st->lay.xr), d);
+    TCK(cudaGetLastError());
+  }
   return FSC_OK;
 }
 

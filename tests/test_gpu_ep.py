@@ -272,3 +272,69 @@ def test_ep_allreduce_variant(world):
     torch.cuda.synchronize()
     c1.close()
     assert rel_l2(res[0]["out0"], o1.cpu().numpy()) < 1e-6
+
+
+# ----------------------------------------------------------------------------- FP8 dispatch payload (NEXT-4)
+def _fp8_worker(rank, world, port, shape, seed, outdir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2511_11505_b200 import Context, MoeDebug
+    from tests.gpu_util import dev_f32, moe_weights_dev
+    e_loc = shape.n_experts // world
+    w = synth.moe_weights(shape, seed=seed, e0=rank * e_loc, e_loc=e_loc)
+    x = synth.tokens(shape, seed=seed, rank=rank)
+    T = x.shape[0]
+    ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
+                  shared_ffn=shape.shared_ffn, max_tokens=T, rank=rank, ep_size=world, device=0)
+    ctx.set_dispatch_fp8(True)
+    ctx.connect()
+    wd = moe_weights_dev(w)
+    xin = dev_f32(x)
+    out = torch.empty_like(xin)
+    dbg = MoeDebug(topk_idx=torch.empty(T, shape.top_k, dtype=torch.int32, device="cuda"),
+                   routed_out=torch.empty(T, shape.d, dtype=torch.float32, device="cuda"))
+    ctx.moe_forward_blocking(wd, xin, out, dbg)
+    partial = xin.clone()
+    h = ctx.moe_forward_farskip(wd, xin, partial)
+    full = torch.empty_like(xin)
+    ctx.moe_wait(h, partial, full)
+    torch.cuda.synchronize()
+    np.savez(os.path.join(outdir, f"f{rank}.npz"), out=out.cpu().numpy(), full=full.cpu().numpy(),
+             idx=dbg.tensors["topk_idx"].cpu().numpy(), routed=dbg.tensors["routed_out"].cpu().numpy())
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_fp8_dispatch_payload(world):
+    """FP8 e4m3 dispatch payload (per-128-column scales): the routed output matches the
+    oracle's moe_block_ep_fp8 (same quantisation step, fp64 experts) within the BJ
+    tolerance, and the exact (bf16-payload) oracle only within the FP8 error; FarSkip ==
+    blocking bitwise."""
+    from paper_2511_11505_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as td:
+        ps = [ctx.Process(target=_fp8_worker, args=(r, world, port, SHAPE, 0, td)) for r in range(world)]
+        for p in ps:
+            p.start()
+        for p in ps:
+            p.join(timeout=600)
+        assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+        res = [dict(np.load(os.path.join(td, f"f{r}.npz"))) for r in range(world)]
+    xs = [synth.tokens(SHAPE, seed=0, rank=r) for r in range(world)]
+    lay = om.layer_from_synth(synth.moe_weights(SHAPE, seed=0), SHAPE.top_k)
+    q = om.moe_block_ep_fp8(xs, lay, world)
+    exact = om.moe_block_ep(xs, lay, world)
+    for r in range(world):
+        sh, ro, rt = q[r]
+        np.testing.assert_array_equal(res[r]["idx"], rt.idx)
+        assert rel_l2(res[r]["routed"], ro) < 1e-2
+        assert rel_l2(res[r]["out"], (xs[r].astype(np.float64) + sh) + ro) < 1e-2
+        assert rel_l2(res[r]["routed"], exact[r][1]) < 8e-2
+        np.testing.assert_array_equal(res[r]["full"], res[r]["out"])

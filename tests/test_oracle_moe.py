@@ -261,3 +261,65 @@ def test_synth_bf16_roundtrip_and_layer():
     # experts regenerate identically when drawn per rank slice
     w2 = synth.moe_weights(synth.CONFIGS["tiny"], seed=0, e0=2, e_loc=2)
     np.testing.assert_array_equal(w2.w3, w.w3[2:4])
+
+
+# ----------------------------------------------------------------------------- FP8 dispatch payload (NEXT-4)
+def _e4m3_table():
+    """All finite OCP E4M3 values decoded from their bit patterns (the format's
+    definition: bias 7, 3 mantissa bits, exponent field 0 = subnormal, S.1111.111 = NaN)."""
+    vals = []
+    for code in range(256):
+        sgn = -1.0 if code & 0x80 else 1.0
+        e, m = (code >> 3) & 0xF, code & 0x7
+        if e == 0xF and m == 0x7:
+            continue                                   # NaN
+        v = m * 2.0 ** -9 if e == 0 else (1 + m / 8.0) * 2.0 ** (e - 7)
+        vals.append(sgn * v)
+    return np.unique(np.array(vals))
+
+
+def test_e4m3_rne_against_the_format_table():
+    table = _e4m3_table()
+    assert table.max() == 448.0 and table.min() == -448.0 and len(table) == 253   # +0/-0 merge
+    np.testing.assert_array_equal(om.e4m3_rne(table), table)           # representable -> itself
+    pos = table[table >= 0]
+    mids = (pos[:-1] + pos[1:]) / 2                                      # exact ties
+    lo_code_even = np.array([int(round(v / (2.0 ** max(np.floor(np.log2(v)) - 3, -9)))) % 2 == 0
+                             if v > 0 else True for v in pos[:-1]])
+    want = np.where(lo_code_even, pos[:-1], pos[1:])                     # ties to the even mantissa
+    np.testing.assert_array_equal(om.e4m3_rne(mids), want)
+    np.testing.assert_array_equal(om.e4m3_rne(-mids), -want)
+    # brute force nearest on random values (no ties): the table's closest element
+    v = rng(3).uniform(-460, 460, 2000) * rng(4).choice([1, 1e-2, 1e-4], 2000)
+    near = table[np.abs(v[:, None] - table[None, :]).argmin(axis=1)]
+    np.testing.assert_array_equal(om.e4m3_rne(v), np.clip(near, -448, 448))
+    assert om.e4m3_rne(np.array([1e6, -1e6])).tolist() == [448.0, -448.0]   # satfinite
+
+
+def test_fp8_payload_block_scaling():
+    x = om.bf16_rne(rng(6).standard_normal((5, 256)).astype(np.float32))
+    x[2, :128] = 0.0                                                    # empty block: scale 1, exact zeros
+    xh = om.fp8_dispatch_payload(x)
+    assert np.all(xh[2, :128] == 0)
+    for t in range(5):
+        for b in range(2):
+            blk, hb = x[t, 128 * b:128 * (b + 1)], xh[t, 128 * b:128 * (b + 1)]
+            if np.abs(blk).max() == 0:
+                continue
+            i = np.abs(blk).argmax()
+            assert abs(hb[i] - blk[i]) <= 2 ** -8 * abs(blk[i])          # amax -> +-448 exactly, then bf16
+            big = np.abs(blk) >= np.abs(blk).max() * 2 ** -5             # normal-range e4m3 codes
+            rel = np.abs(hb[big] - blk[big]) / np.abs(blk[big])
+            assert rel.max() <= 2 ** -4 + 2 ** -8                        # half an e4m3 ulp (+ bf16)
+
+
+def test_fp8_dispatch_block_matches_exact_block_within_fp8_error():
+    lay = _layer(16, 256, 8, 2, 64, 32, seed=2)
+    xs = [rng(10 + s).standard_normal((16, 256)) for s in range(2)]
+    exact = om.moe_block_ep(xs, lay, 2)
+    q = om.moe_block_ep_fp8(xs, lay, 2)
+    for (sh0, ro0, r0), (sh1, ro1, r1) in zip(exact, q):
+        np.testing.assert_array_equal(r0.idx, r1.idx)
+        np.testing.assert_array_equal(sh0, sh1)                          # shared expert: local, unquantised
+        err = np.linalg.norm(ro1 - ro0) / np.linalg.norm(ro0)
+        assert 1e-3 < err < 8e-2                                         # FP8-level, not exact, not broken
