@@ -86,10 +86,23 @@ FSC_DEVINL int ld_acquire_sys(const int* p) {
   asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+FSC_DEVINL unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until every source's flag reached this call's epoch. A peer that never
+// arrives (dead rank, broken bootstrap) must not hang the GPU: after 30 s the kernel
+// traps, which surfaces as FSC_ERR_CUDA on the host instead of a hung stream.
+constexpr unsigned long long kFlagTimeoutNs = 30ull * 1000 * 1000 * 1000;
 FSC_DEVINL void wait_flags(char* mybase, int slot, int P, int epoch) {
+  const unsigned long long t0 = global_ns();
   for (int s = 0; s < P; ++s) {
     const int* f = flag_ptr(mybase, slot, s);
-    while (ld_acquire_sys(f) - epoch < 0) __nanosleep(64);
+    while (ld_acquire_sys(f) - epoch < 0) {
+      __nanosleep(64);
+      if (global_ns() - t0 > kFlagTimeoutNs) __trap();
+    }
   }
 }
 }  // namespace
