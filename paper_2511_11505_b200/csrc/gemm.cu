@@ -30,7 +30,7 @@ constexpr int kMaxGroups = 256;
 constexpr int kEpiWarps = 8;         // two warps per TMEM lane quarter, each half the columns
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
-template <int BN, int CG>
+template <int BN, int CG, int EPI = 0>
 struct Cfg {
   static constexpr int HALF = BN / 2;
   static constexpr int TILE_M = BM * CG;                       // rows per (pair) tile
@@ -38,10 +38,13 @@ struct Cfg {
   static constexpr int B_ROWS = CG == 2 ? BN / 2 : BN;         // B rows held per CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  // fp32 epilogue: per-warp 32 x 32 transpose scratch (rows padded to 36 floats) so the
+  // residual loads and output stores are row-contiguous 128-byte accesses
+  static constexpr int SCRATCH = EPI == EPI_RESID_F32 ? kEpiWarps * 32 * 36 * 4 : 0;
+  static constexpr int STAGES_RAW = (200 * 1024 - SCRATCH) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;                     // double-buffered accumulator
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + 2 * (kMaxGroups + 1) * 4;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + 2 * (kMaxGroups + 1) * 4 + 16 + SCRATCH;
 };
 
 FSC_DEVINL float silu_f(float g) { return g / (1.0f + __expf(-g)); }
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                         const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmA32,
                         const __grid_constant__ CUtensorMap tmA64, GemmParams p) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -213,6 +216,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
   int* s_row_off = reinterpret_cast<int*>(smem + C::STAGES * C::STAGE_BYTES + 256);
   int* s_tile_off = s_row_off + (kMaxGroups + 1);
+  float* s_scr = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_tile_off + (kMaxGroups + 1)) + 15) &
+                                          ~uintptr_t(15));   // EPI_RESID_F32 transpose scratch (16-byte rows)
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -490,38 +495,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (p.comb_out) fused_unpermute<BN>(p, tok, ti.nb * BN + half * (BN / 2), lane);
       } else {
-        float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo + ti.nb * BN;
-        const float* res = (p.resid && valid) ? p.resid + grow * p.ldr + ti.nb * BN : nullptr;
+        // thread = row after tcgen05.ld; transpose each 32 x 32 chunk through shared
+        // memory so that 8 lanes cover one row's 32 floats (128-byte residual loads and
+        // output stores, 4 rows per instruction)
+        float* scr = s_scr + (warp - 2) * 32 * 36;
+        const int rbase = (int)rank * BM + q * 32;              // first row of this warp inside the tile
+        const int sub = lane >> 3, c4 = (lane & 7) * 4;
         const int c_beg = half * (BN / 2), c_end = (half + 1) * (BN / 2);
-        float4 pre[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) pre[i] = res ? *reinterpret_cast<const float4*>(res + c_beg + 4 * i)
-                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        mbar_wait(&tfull[acc], aphase);   // first residual chunk loads overlap the MMA tail
+        mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
 #pragma unroll 1
         for (int c = c_beg; c < c_end; c += 32) {
           uint32_t v[32];
           tmem_ld32(tb + c, v);
-          float4 cur[8];
+          float4 rv[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) cur[i] = pre[i];
-          if (res && c + 32 < c_end) {   // residual of the next chunk in flight while this one drains
-#pragma unroll
-            for (int i = 0; i < 8; ++i) pre[i] = *reinterpret_cast<const float4*>(res + c + 32 + 4 * i);
+          for (int it = 0; it < 8; ++it) {                       // residual of rows it*4 + sub (in flight)
+            const int rr2 = rbase + it * 4 + sub;
+            rv[it] = (p.resid && rr2 < ti.rows)
+                         ? *reinterpret_cast<const float4*>(p.resid + ((long)ti.row0 + rr2) * p.ldr + ti.nb * BN + c + c4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
           }
           tmem_ld_wait();
-          if (valid) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              float4 a = cur[i];
-              a.x += __uint_as_float(v[4 * i]);
-              a.y += __uint_as_float(v[4 * i + 1]);
-              a.z += __uint_as_float(v[4 * i + 2]);
-              a.w += __uint_as_float(v[4 * i + 3]);
-              *reinterpret_cast<float4*>(out + c + 4 * i) = a;
+          for (int i = 0; i < 8; ++i)
+            *reinterpret_cast<float4*>(scr + lane * 36 + 4 * i) =
+                make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]), __uint_as_float(v[4 * i + 2]),
+                            __uint_as_float(v[4 * i + 3]));
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int r = it * 4 + sub;
+            if (rbase + r < ti.rows) {
+              const float4 d4 = *reinterpret_cast<const float4*>(scr + r * 36 + c4);
+              float4 a = rv[it];
+              a.x += d4.x;
+              a.y += d4.y;
+              a.z += d4.z;
+              a.w += d4.w;
+              *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + ((long)ti.row0 + rbase + r) * p.ldo +
+                                         ti.nb * BN + c + c4) = a;
             }
           }
+          __syncwarp();
         }
       }
       tc_fence_before();
@@ -573,7 +589,7 @@ static bool make_map(CUtensorMap* m, const void* base, long rows, long cols, int
 
 template <int BN, int EPI, int CG>
 static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, EPI>;
   CUtensorMap ma, mb0, mb1, ma32, ma64;
   long a_rows = L.a_rows > 0 ? L.a_rows : 1;
   if (!make_map(&ma, L.A, a_rows, L.K, L.a_idx ? 1 : BM)) return cudaErrorInvalidValue;   // gather4: {64, 1} box
