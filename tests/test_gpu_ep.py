@@ -338,3 +338,69 @@ def test_ep_fp8_dispatch_payload(world):
         assert rel_l2(res[r]["out"], (xs[r].astype(np.float64) + sh) + ro) < 1e-2
         assert rel_l2(res[r]["routed"], exact[r][1]) < 8e-2
         np.testing.assert_array_equal(res[r]["full"], res[r]["out"])
+
+
+def _ar_stack_worker(rank, world, port, shape, seed, outdir, L):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2511_11505_b200 import FSC_BLOCKING, FSC_EP_ALLREDUCE, FSC_HYBRID, FSC_OVERLAPPED, Context
+    from tests.gpu_util import attn_weights_dev, dev_f32, moe_weights_dev
+    e_loc = shape.n_experts // world
+    mw = [moe_weights_dev(synth.moe_weights(shape, seed=seed, layer=k, e0=rank * e_loc, e_loc=e_loc))
+          for k in range(L)]
+    aw = [attn_weights_dev(synth.attn_weights(shape, seed=seed, layer=k)) for k in range(L)]
+    x = synth.tokens(shape, seed=seed, rank=0)          # replicated activations
+    T = x.shape[0]
+    ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
+                  shared_ffn=shape.shared_ffn, max_tokens=T, rank=rank, ep_size=world, device=0)
+    ctx.set_ep_mode(FSC_EP_ALLREDUCE)
+    ctx.connect()
+    res = {}
+    for sname, sched in (("blk", FSC_BLOCKING), ("ovl", FSC_OVERLAPPED)):
+        o0 = dev_f32(x)
+        oL = torch.empty_like(o0)
+        ctx.layer_stack_forward(aw, mw, T, shape.seq_len, [FSC_HYBRID] * L, sched, o0, oL)
+        torch.cuda.synchronize()
+        res[sname] = oL.cpu().numpy()
+    np.savez(os.path.join(outdir, f"as{rank}.npz"), **res)
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_ep_allreduce_stack():
+    """FarSkip (Hybrid) stack in the all-reduce inference variant at EP = 2: the MoE
+    all-reduce of layer k is waited one sub-block later; every rank ends with
+    the same bits, BLOCKING == OVERLAPPED, and the result matches the EP = 1 stack on
+    the same tokens up to the fp32 re-association of the partial sums."""
+    from paper_2511_11505_b200 import FSC_HYBRID, FSC_OVERLAPPED, Context, build
+    from tests.gpu_util import attn_weights_dev, dev_f32, moe_weights_dev
+    build.build()
+    L, world, sh = 3, 2, STACK_SHAPE
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as td:
+        ps = [ctx.Process(target=_ar_stack_worker, args=(r, world, port, sh, 0, td, L)) for r in range(world)]
+        for p in ps:
+            p.start()
+        for p in ps:
+            p.join(timeout=600)
+        assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+        res = [dict(np.load(os.path.join(td, f"as{r}.npz"))) for r in range(world)]
+    for r in range(world):
+        np.testing.assert_array_equal(res[r]["blk"], res[r]["ovl"])
+        np.testing.assert_array_equal(res[r]["ovl"], res[0]["ovl"])
+    X = synth.tokens(sh, seed=0, rank=0)
+    c1 = Context(d=sh.d, n_experts=sh.n_experts, top_k=sh.top_k, ffn=sh.ffn, shared_ffn=sh.shared_ffn,
+                 max_tokens=X.shape[0])
+    mw = [moe_weights_dev(synth.moe_weights(sh, seed=0, layer=k)) for k in range(L)]
+    aw = [attn_weights_dev(synth.attn_weights(sh, seed=0, layer=k)) for k in range(L)]
+    o0 = dev_f32(X)
+    oL = torch.empty_like(o0)
+    c1.layer_stack_forward(aw, mw, X.shape[0], sh.seq_len, [FSC_HYBRID] * L, FSC_OVERLAPPED, o0, oL)
+    torch.cuda.synchronize()
+    c1.close()
+    assert rel_l2(res[0]["ovl"], oL.cpu().numpy()) < 1e-4

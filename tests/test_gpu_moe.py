@@ -269,3 +269,33 @@ def test_int8_router_moe_parity(name, T):
     sh, ro, _ = om.moe_block(x, lay, router=r)
     assert rel_l2(out, (x.astype(np.float64) + sh) + ro) < TOL
     assert rel_l2(out, ref_out) < 1e-5
+
+
+def test_error_paths_are_status_codes_not_crashes():
+    """Every misuse is reported through the C ABI status (FscError in Python) before
+    anything is enqueued, and the context stays usable afterwards."""
+    from paper_2511_11505_b200 import FSC_EP_ALLREDUCE, FscError
+    shape = synth.CONFIGS["tiny"]
+    T = 32
+    ctx = make_ctx(shape, T)
+    wd = moe_weights_dev(synth.moe_weights(shape, seed=0))
+    x = dev_f32(synth.tokens(shape, T=T))
+    out = torch.empty_like(x)
+    big = dev_f32(np.zeros((T + 1, shape.d), np.float32))
+    with pytest.raises(FscError):                       # T > max_tokens (FSC_ERR_CONFIG)
+        ctx.moe_forward_blocking(wd, big, torch.empty_like(big))
+    raw = torch.empty(T * shape.d + 1, dtype=torch.float32, device="cuda")
+    mis = raw[1:].view(T, shape.d)                      # 4-byte aligned only
+    with pytest.raises(FscError):                       # misaligned activation (FSC_ERR_SHAPE)
+        ctx.moe_forward_blocking(wd, mis, out)
+    with pytest.raises(FscError):                       # d = 64: no FP8 payload (d % 128)
+        ctx.set_dispatch_fp8(True)
+    with pytest.raises(FscError):                       # int8 router needs d % 128 == 0
+        ctx.set_router_int8(True)
+    with pytest.raises(FscError):
+        ctx.set_gemm_cta_group(3)
+    ctx.set_ep_mode(FSC_EP_ALLREDUCE)                   # EP = 1: accepted, no effect
+    ctx.moe_forward_blocking(wd, x, out)                # still usable
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    ctx.close()
