@@ -171,7 +171,11 @@ FSC_API int fsc_set_router_int8(fsc_ctx* ctx, int on);
  * FSC_EP_ALLREDUCE the shared expert is computed replicated on every rank (no
  * extra collective), the routed partials are all-reduced; the FarSkip entry
  * returns with the all-reduce in flight and fsc_moe_wait completes it (the
- * "synchronize only before the next MoE computation" of P:217). */
+ * "synchronize only before the next MoE computation" of P:217). In this mode
+ * fsc_layer_stack_forward runs the attention tensor-parallel: each rank passes its
+ * head slice (n_heads / P query and n_kv_heads / P kv heads, the matching w_qkv rows
+ * and w_o columns); the o-projection partials are all-reduced on a second channel
+ * and, in Hybrid layers, waited only before the next attention. */
 FSC_API int fsc_set_ep_mode(fsc_ctx* ctx, int mode);
 /* EP > 1 all-to-all: on != 0 sends the Dispatch payload as FP8 e4m3 with one fp32
  * scale per 128 columns (s = amax / 448, q = e4m3_rn_satfinite(x / s); the receiver

@@ -81,6 +81,10 @@ struct fsc_ctx {
   cudaEvent_t ev_in[2] = {}, ev_cdone[2] = {}, ev_out[2] = {};
   int io_slot = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_d = nullptr;
+  cudaEvent_t ev_t1 = nullptr, ev_t2 = nullptr;   // TP attention all-reduce (stack)
+  int attn_pending = 0;        // 1: attention all-reduce in line, 2: on the comm stream
+  float* attn_cache = nullptr;
+  int attn_T = 0;
 
   int pending = 0;
   int no_overlap = 0;          // FarSkip call made under the BLOCKING stack schedule
@@ -115,7 +119,8 @@ int fsc_transport_dispatch_wait(fsc_ctx* ctx, cudaStream_t s);
 int fsc_transport_combine(fsc_ctx* ctx, int T, cudaStream_t s);
 int fsc_transport_combine_wait(fsc_ctx* ctx, cudaStream_t s);
 void fsc_transport_scatter_target(fsc_ctx* ctx, const int** ret, void** peer_out);
-float* fsc_transport_ar_partial(fsc_ctx* ctx);
-int fsc_transport_ar_start(fsc_ctx* ctx, int T, cudaStream_t s);
-int fsc_transport_ar_finish(fsc_ctx* ctx, int T, const float* resid, float* out, cudaStream_t s);
+// EP all-reduce channels: 0 = MoE routed sum, 1 = TP attention o-projection (stack)
+float* fsc_transport_ar_partial(fsc_ctx* ctx, int ch = 0);
+int fsc_transport_ar_start(fsc_ctx* ctx, int T, cudaStream_t s, int ch = 0);
+int fsc_transport_ar_finish(fsc_ctx* ctx, int T, const float* resid, float* out, cudaStream_t s, int ch = 0);
 int fsc_transport_reinit(fsc_ctx* ctx);

@@ -149,6 +149,8 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_c, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_d, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_t1, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_t2, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
   rc = fsc_transport_init(ctx);
   if (rc) return rc;
@@ -179,6 +181,8 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
   if (ctx->ev_c) cudaEventDestroy(ctx->ev_c);
   if (ctx->ev_d) cudaEventDestroy(ctx->ev_d);
+  if (ctx->ev_t1) cudaEventDestroy(ctx->ev_t1);
+  if (ctx->ev_t2) cudaEventDestroy(ctx->ev_t2);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);

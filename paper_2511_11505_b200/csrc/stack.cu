@@ -13,6 +13,10 @@
 // partial, so layer k+1's attention overlaps layer k's combine, and the
 // dispatch overlaps the attention core (OVERLAPPED schedule, P:198 steps 1-8).
 // BLOCKING runs the same kernels with every collective waited on at once.
+// In the all-reduce inference variant (FSC_EP_ALLREDUCE) the attention is
+// tensor-parallel: each rank passes its head slice, the o-projection partials are
+// all-reduced on channel 1 and, in Hybrid layers, waited only before the next
+// attention (A_{k+1} = (M_k + shared_k) + attn_out_k in that variant).
 #include <stdio.h>
 #include <string.h>
 
@@ -97,11 +101,35 @@ int attention_a(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, co
   return FSC_OK;
 }
 
+bool tp_mode(const fsc_ctx* ctx) { return ctx->ep > 1 && ctx->ep_mode == FSC_EP_ALLREDUCE; }
+
 // Attention part (b): core attention + output projection into the residual.
+// TP (all-reduce inference variant): this rank holds a slice of the heads; its
+// o-projection partial goes to all-reduce channel 1, launched at once (comm stream
+// when overlapped); out = resid now and attn_finish adds the reduced attn_out later.
 int attention_b(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, const float* resid, float* out,
                 float* cache_attn_out, cudaStream_t s) {
   const int d = ctx->cfg.d, Hq = aw->n_heads, Hkv = aw->n_kv_heads, hd = aw->head_dim;
   SCK(launch_flash_attn(ctx->qkv, ctx->ao, T, Hq, Hkv, hd, seq_len, s));
+  if (tp_mode(ctx)) {
+    GemmLaunch g{};
+    g.A = ctx->ao; g.a_rows = T; g.B0 = aw->w_o; g.b_rows = d; g.b_group_rows = d; g.K = Hq * hd; g.N = d;
+    g.G = 1; g.m_total = T; g.out = fsc_transport_ar_partial(ctx, 1); g.ldo = d; g.resid = nullptr; g.ldr = d;
+    g.epi = EPI_RESID_F32; g.num_ctas = ctx->gemm_ctas; g.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
+    SCK(launch_grouped_gemm(g, s));
+    if (out != resid) SCK(cudaMemcpyAsync(out, resid, sizeof(float) * (long)T * d, cudaMemcpyDeviceToDevice, s));
+    cudaStream_t cs = ctx->no_overlap ? s : ctx->comm;
+    if (cs != s) {
+      SCK(cudaEventRecord(ctx->ev_t1, s));
+      SCK(cudaStreamWaitEvent(cs, ctx->ev_t1, 0));
+    }
+    SRC(fsc_transport_ar_start(ctx, T, cs, 1));
+    if (cs != s) SCK(cudaEventRecord(ctx->ev_t2, cs));
+    ctx->attn_pending = cs != s ? 2 : 1;
+    ctx->attn_cache = cache_attn_out;
+    ctx->attn_T = T;
+    return FSC_OK;
+  }
   GemmLaunch g{};
   g.A = ctx->ao; g.a_rows = T; g.B0 = aw->w_o; g.b_rows = d; g.b_group_rows = d; g.K = Hq * hd; g.N = d;
   g.G = 1; g.m_total = T; g.out = out; g.ldo = d; g.resid = resid; g.ldr = d; g.epi = EPI_RESID_F32;
@@ -112,6 +140,17 @@ int attention_b(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, co
     g.resid = nullptr;
     SCK(launch_grouped_gemm(g, s));
   }
+  return FSC_OK;
+}
+
+// TP: buf += reduced attn_out (waits the all-reduce of the last attention_b).
+int attn_finish(fsc_ctx* ctx, float* buf, cudaStream_t s) {
+  if (!ctx->attn_pending) return FSC_OK;
+  if (ctx->attn_pending == 2) SCK(cudaStreamWaitEvent(s, ctx->ev_t2, 0));
+  SRC(fsc_transport_ar_finish(ctx, ctx->attn_T, buf, buf, s, 1));
+  if (ctx->attn_cache) SRC(fsc_transport_ar_finish(ctx, ctx->attn_T, nullptr, ctx->attn_cache, s, 1));
+  ctx->attn_pending = 0;
+  ctx->attn_cache = nullptr;
   return FSC_OK;
 }
 
@@ -171,6 +210,7 @@ extern "C" int fsc_layer_stack_forward(fsc_ctx* ctx, const fsc_attn_weights* att
     dbg.shared_out = ck ? ck->shared_out : nullptr;
     dbg.routed_out = ck ? ck->routed_out : nullptr;
     const fsc_moe_debug* dbgp = (dbg.shared_out || dbg.routed_out) ? &dbg : nullptr;
+    SRC(attn_finish(ctx, bufA, s));   // TP: A_k += attn_out_{k-1} (synchronised before the next attention)
     if (modes[k] == FSC_REGULAR) {
       // o_{k-1} must be complete: wait the previous routed output into bufA
       if (h) {
@@ -181,6 +221,7 @@ extern "C" int fsc_layer_stack_forward(fsc_ctx* ctx, const fsc_attn_weights* att
       if (ck) SRC(copy_f32(ctx, ck->attn_in, bufA, n, s));
       SRC(attention_a(ctx, &attn[k], T, seq_len, bufA, s));
       SRC(attention_b(ctx, &attn[k], T, seq_len, bufA, bufM, ck ? ck->attn_out : nullptr, s));  // M = A + attn_out
+      SRC(attn_finish(ctx, bufM, s));   // Regular: the MoE input needs attn_out now
       if (ck) SRC(copy_f32(ctx, ck->mlp_in, bufM, n, s));
       // partial := M (+= shared inside); routed pending. Nothing can overlap the
       // dispatch here (Regular wiring), so it runs on the compute stream.
@@ -218,6 +259,7 @@ extern "C" int fsc_layer_stack_forward(fsc_ctx* ctx, const fsc_attn_weights* att
     prev_k = k;
   }
   // final o_L = A_{L+1} + routed_L: the last combine has nothing to overlap
+  SRC(attn_finish(ctx, bufA, s));
   SRC(fsc_moe_wait(ctx, h, bufA, oL, s));
   if (cache) SRC(copy_f32(ctx, cache[L - 1].o, oL, n, s));
   ctx->no_overlap = 0;

@@ -36,28 +36,35 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Layout {  // byte offsets inside every rank's symmetric region
-  size_t flags, cnt, ret, xr, ys, part, red, xq, xsc, total;
+  size_t flags, cnt, ret, xr, ys, part[2], red[2], xq, xsc, total;
 };
 
-constexpr int kFlagRows = 5;   // FLAG_CNT, FLAG_DISP, FLAG_COMB, FLAG_AR_READY, FLAG_AR_DONE
+// FLAG_CNT, FLAG_DISP, FLAG_COMB, then (READY, DONE) per all-reduce channel
+// (channel 0: MoE routed sum; channel 1: TP attention o-projection)
+constexpr int kFlagRows = 7;
+constexpr int kEpochs = 2;     // epoch counters: [0] all-to-all + AR channel 0, [1] AR channel 1
 
 Layout layout_for(const fsc_ctx* c) {
   Layout L{};
   const size_t P = c->ep, E = c->cfg.n_experts, d = c->cfg.d, T = c->cfg.max_tokens;
   const size_t Tk = T * c->cfg.top_k;
-  L.flags = 0;                                       // int [kFlagRows][kMaxP] + epoch
-  L.cnt = align_up(L.flags + (kFlagRows * kMaxP + 1) * sizeof(int));
-  if (c->ep_mode == FSC_EP_ALLREDUCE) {              // replicated tokens: fp32 partial + reduced rows
+  L.flags = 0;                                       // int [kFlagRows][kMaxP] + epochs
+  L.cnt = align_up(L.flags + (kFlagRows * kMaxP + kEpochs) * sizeof(int));
+  if (c->ep_mode == FSC_EP_ALLREDUCE) {              // replicated tokens: fp32 partial + reduced rows, x2
     L.ret = L.xr = L.ys = L.cnt;
-    L.part = L.cnt;
-    L.red = align_up(L.part + T * d * sizeof(float));
-    L.total = align_up(L.red + T * d * sizeof(float));
+    size_t o = L.cnt;
+    for (int ch = 0; ch < 2; ++ch) {
+      L.part[ch] = o;
+      L.red[ch] = align_up(L.part[ch] + T * d * sizeof(float));
+      o = align_up(L.red[ch] + T * d * sizeof(float));
+    }
+    L.xq = L.xsc = L.total = o;
     return L;
   }
   L.ret = align_up(L.cnt + P * E * sizeof(int));     // int [max_recv]
   L.xr = align_up(L.ret + (size_t)c->max_recv * sizeof(int));
   L.ys = align_up(L.xr + (size_t)c->max_recv * d * 2);
-  L.part = L.red = L.xq = L.xsc = L.total = align_up(L.ys + Tk * d * 2);
+  L.part[0] = L.part[1] = L.red[0] = L.red[1] = L.xq = L.xsc = L.total = align_up(L.ys + Tk * d * 2);
   if (c->dispatch_fp8) {                             // FP8 payload: e4m3 rows + fp32 per-128-column scales
     L.xq = L.total;
     L.xsc = align_up(L.xq + (size_t)c->max_recv * d);
@@ -70,8 +77,8 @@ struct Peers {
   char* base[kMaxP];
 };
 
-enum { FLAG_CNT = 0, FLAG_DISP = 1, FLAG_COMB = 2, FLAG_AR_READY = 3, FLAG_AR_DONE = 4 };
-constexpr int kEpochSlot = kFlagRows * kMaxP;   // int index of the epoch counter in the flags area
+enum { FLAG_CNT = 0, FLAG_DISP = 1, FLAG_COMB = 2, FLAG_AR_READY = 3, FLAG_AR_DONE = 4 };   // + 2 ch for AR
+constexpr int kEpochSlot = kFlagRows * kMaxP;   // int index of the epoch counters in the flags area
 
 FSC_DEVINL int read_epoch(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
@@ -320,7 +327,7 @@ __global__ void ep_wait_kernel(char* mybase, int slot, int P, const int* epoch_p
 // result into every rank's `red` buffer; the last CTA raises FLAG_AR_DONE there.
 
 // bump the epoch and announce "my partial is complete" (stream order after the unpermute)
-__global__ void ar_begin_kernel(Peers peers, int rank, int P, int* epoch_ptr) {
+__global__ void ar_begin_kernel(Peers peers, int rank, int P, int* epoch_ptr, int ready_slot) {
   __shared__ int s_epoch;
   if (threadIdx.x == 0) {
     s_epoch = read_epoch(epoch_ptr) + 1;
@@ -328,14 +335,14 @@ __global__ void ar_begin_kernel(Peers peers, int rank, int P, int* epoch_ptr) {
   }
   __syncthreads();
   __threadfence_system();
-  if (threadIdx.x < P) st_release_sys(flag_ptr(peers.base[threadIdx.x], FLAG_AR_READY, rank), s_epoch);
+  if (threadIdx.x < P) st_release_sys(flag_ptr(peers.base[threadIdx.x], ready_slot, rank), s_epoch);
 }
 
 __global__ void __launch_bounds__(256) ar_reduce_kernel(Peers peers, int rank, int P, long rows0, long rows1, int d,
                                                         size_t off_part, size_t off_red, const int* epoch_ptr,
-                                                        int* ticket) {
+                                                        int* ticket, int ready_slot, int done_slot) {
   const int epoch = read_epoch(epoch_ptr);
-  if (threadIdx.x == 0) wait_flags(peers.base[rank], FLAG_AR_READY, P, epoch);
+  if (threadIdx.x == 0) wait_flags(peers.base[rank], ready_slot, P, epoch);
   __syncthreads();
   const long dv = d / 4;
   const long n = (rows1 - rows0) * dv;
@@ -357,15 +364,15 @@ __global__ void __launch_bounds__(256) ar_reduce_kernel(Peers peers, int rank, i
     if (atomicAdd(ticket, 1) == (int)gridDim.x - 1) {
       *ticket = 0;
       __threadfence_system();
-      for (int p = 0; p < P; ++p) st_release_sys(flag_ptr(peers.base[p], FLAG_AR_DONE, rank), epoch);
+      for (int p = 0; p < P; ++p) st_release_sys(flag_ptr(peers.base[p], done_slot, rank), epoch);
     }
   }
 }
 
 // wait every rank's slice, then out = resid + reduced (fp32; resid may alias out)
 __global__ void __launch_bounds__(256) ar_finish_kernel(char* mybase, int P, const int* epoch_ptr, size_t off_red,
-                                                        const float* resid, float* out, long n4) {
-  if (threadIdx.x == 0) wait_flags(mybase, FLAG_AR_DONE, P, read_epoch(epoch_ptr));
+                                                        const float* resid, float* out, long n4, int done_slot) {
+  if (threadIdx.x == 0) wait_flags(mybase, done_slot, P, read_epoch(epoch_ptr));
   __syncthreads();
   const float4* red = reinterpret_cast<const float4*>(mybase + off_red);
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
@@ -403,11 +410,11 @@ int fsc_transport_init(fsc_ctx* ctx) {
   ctx->peer = st;
   st->lay = layout_for(ctx);
   TCK(cudaMalloc(&st->local, st->lay.total));
-  TCK(cudaMemset(st->local, 0, st->lay.flags + (kFlagRows * kMaxP + 1) * sizeof(int)));
+  TCK(cudaMemset(st->local, 0, st->lay.flags + (kFlagRows * kMaxP + kEpochs) * sizeof(int)));
   TCK(cudaIpcGetMemHandle(&st->my_handle, st->local));
   TCK(cudaMalloc(&st->send_base, sizeof(int) * ctx->cfg.n_experts));
-  TCK(cudaMalloc(&st->ticket, sizeof(int)));
-  TCK(cudaMemset(st->ticket, 0, sizeof(int)));
+  TCK(cudaMalloc(&st->ticket, 3 * sizeof(int)));            // [0] dispatch / AR channel 0, [1] AR channel 1
+  TCK(cudaMemset(st->ticket, 0, 3 * sizeof(int)));
   TCK(cudaMalloc(&ctx->recv_counts, sizeof(int) * ctx->e_loc));
   ctx->xr = reinterpret_cast<uint16_t*>(st->local + st->lay.xr);
   ctx->ys = reinterpret_cast<uint16_t*>(st->local + st->lay.ys);
@@ -535,11 +542,15 @@ void fsc_transport_scatter_target(fsc_ctx* ctx, const int** ret, void** peer_out
 }
 
 // ----------------------------------------------------------------------------- EP all-reduce (host)
-float* fsc_transport_ar_partial(fsc_ctx* ctx) {
-  return reinterpret_cast<float*>(ctx->peer->local + ctx->peer->lay.part);
+static int* epoch_ptr_ch(fsc_ctx* ctx, int ch) {
+  return reinterpret_cast<int*>(ctx->peer->local + ctx->peer->lay.flags) + kEpochSlot + ch;
 }
 
-int fsc_transport_ar_start(fsc_ctx* ctx, int T, cudaStream_t s) {
+float* fsc_transport_ar_partial(fsc_ctx* ctx, int ch) {
+  return reinterpret_cast<float*>(ctx->peer->local + ctx->peer->lay.part[ch]);
+}
+
+int fsc_transport_ar_start(fsc_ctx* ctx, int T, cudaStream_t s, int ch) {
   fsc_peer_state* st = ctx->peer;
   if (!connected(ctx)) {
     fsc_set_error(ctx, "EP transport not bootstrapped (fsc_bootstrap_export/import)");
@@ -547,26 +558,28 @@ int fsc_transport_ar_start(fsc_ctx* ctx, int T, cudaStream_t s) {
   }
   const int P = ctx->ep, d = ctx->cfg.d;
   const long r0 = (long)T * ctx->rank / P, r1 = (long)T * (ctx->rank + 1) / P;
+  const int ready = FLAG_AR_READY + 2 * ch, done = FLAG_AR_DONE + 2 * ch;
   g_launches += 2;
-  ar_begin_kernel<<<1, 32, 0, s>>>(st->peers, ctx->rank, P, epoch_ptr(ctx));
+  ar_begin_kernel<<<1, 32, 0, s>>>(st->peers, ctx->rank, P, epoch_ptr_ch(ctx, ch), ready);
   TCK(cudaGetLastError());
   long blocks = ((r1 - r0) * (d / 4) + 255) / 256;
   if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
   if (blocks < 1) blocks = 1;
-  ar_reduce_kernel<<<(int)blocks, 256, 0, s>>>(st->peers, ctx->rank, P, r0, r1, d, st->lay.part, st->lay.red,
-                                                epoch_ptr(ctx), st->ticket);
+  ar_reduce_kernel<<<(int)blocks, 256, 0, s>>>(st->peers, ctx->rank, P, r0, r1, d, st->lay.part[ch], st->lay.red[ch],
+                                                epoch_ptr_ch(ctx, ch), st->ticket + ch, ready, done);
   TCK(cudaGetLastError());
   return FSC_OK;
 }
 
-int fsc_transport_ar_finish(fsc_ctx* ctx, int T, const float* resid, float* out, cudaStream_t s) {
+int fsc_transport_ar_finish(fsc_ctx* ctx, int T, const float* resid, float* out, cudaStream_t s, int ch) {
   fsc_peer_state* st = ctx->peer;
   const long n4 = (long)T * ctx->cfg.d / 4;
   long blocks = (n4 + 255) / 256;
   if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
   if (blocks < 1) blocks = 1;
   ++g_launches;
-  ar_finish_kernel<<<(int)blocks, 256, 0, s>>>(st->local, ctx->ep, epoch_ptr(ctx), st->lay.red, resid, out, n4);
+  ar_finish_kernel<<<(int)blocks, 256, 0, s>>>(st->local, ctx->ep, epoch_ptr_ch(ctx, ch), st->lay.red[ch], resid, out,
+                                               n4, FLAG_AR_DONE + 2 * ch);
   TCK(cudaGetLastError());
   return FSC_OK;
 }

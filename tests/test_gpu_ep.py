@@ -340,6 +340,21 @@ def test_ep_fp8_dispatch_payload(world):
         np.testing.assert_array_equal(res[r]["full"], res[r]["out"])
 
 
+def _tp_slice(a, rank, world):
+    """Rank's head slice of the attention weights (TP, RowParallel o-projection):
+    q heads [r Hq/P, (r+1) Hq/P), kv heads [r Hkv/P, ...), the matching w_qkv rows and
+    w_o columns."""
+    import dataclasses
+    hq, hkv, hd = a.n_heads // world, a.n_kv_heads // world, a.head_dim
+    q = a.w_qkv[:a.n_heads * hd]
+    kk = a.w_qkv[a.n_heads * hd:(a.n_heads + a.n_kv_heads) * hd]
+    v = a.w_qkv[(a.n_heads + a.n_kv_heads) * hd:]
+    w_qkv = np.concatenate([q[rank * hq * hd:(rank + 1) * hq * hd], kk[rank * hkv * hd:(rank + 1) * hkv * hd],
+                            v[rank * hkv * hd:(rank + 1) * hkv * hd]])
+    w_o = np.ascontiguousarray(a.w_o[:, rank * hq * hd:(rank + 1) * hq * hd])
+    return dataclasses.replace(a, w_qkv=np.ascontiguousarray(w_qkv), w_o=w_o, n_heads=hq, n_kv_heads=hkv)
+
+
 def _ar_stack_worker(rank, world, port, shape, seed, outdir, L):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -351,7 +366,8 @@ def _ar_stack_worker(rank, world, port, shape, seed, outdir, L):
     e_loc = shape.n_experts // world
     mw = [moe_weights_dev(synth.moe_weights(shape, seed=seed, layer=k, e0=rank * e_loc, e_loc=e_loc))
           for k in range(L)]
-    aw = [attn_weights_dev(synth.attn_weights(shape, seed=seed, layer=k)) for k in range(L)]
+    aw = [attn_weights_dev(_tp_slice(synth.attn_weights(shape, seed=seed, layer=k), rank, world))
+          for k in range(L)]                            # tensor-parallel attention: this rank's heads
     x = synth.tokens(shape, seed=seed, rank=0)          # replicated activations
     T = x.shape[0]
     ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
@@ -372,10 +388,12 @@ def _ar_stack_worker(rank, world, port, shape, seed, outdir, L):
 
 
 def test_ep_allreduce_stack():
-    """FarSkip (Hybrid) stack in the all-reduce inference variant at EP = 2: the MoE
-    all-reduce of layer k is waited one sub-block later; every rank ends with
-    the same bits, BLOCKING == OVERLAPPED, and the result matches the EP = 1 stack on
-    the same tokens up to the fp32 re-association of the partial sums."""
+    """FarSkip (Hybrid) stack in the all-reduce inference variant at EP = TP = 2
+    (P:215-217): experts EP-sharded and the MoE partials all-reduced, attention heads
+    TP-sharded and the o-projection partials all-reduced on a second channel, each
+    waited only one sub-block later; every rank ends with the same bits, BLOCKING ==
+    OVERLAPPED, and the result matches the EP = 1 stack on the same tokens up to the
+    fp32 re-association of the partial sums."""
     from paper_2511_11505_b200 import FSC_HYBRID, FSC_OVERLAPPED, Context, build
     from tests.gpu_util import attn_weights_dev, dev_f32, moe_weights_dev
     build.build()
@@ -403,4 +421,6 @@ def test_ep_allreduce_stack():
     c1.layer_stack_forward(aw, mw, X.shape[0], sh.seq_len, [FSC_HYBRID] * L, FSC_OVERLAPPED, o0, oL)
     torch.cuda.synchronize()
     c1.close()
-    assert rel_l2(res[0]["ovl"], oL.cpu().numpy()) < 1e-4
+    # fp32 re-association (split o-projection, residual order) flips occasional bf16
+    # roundings of the next layers' GEMM operands: ~2e-4 after 3 layers, far below 1e-2
+    assert rel_l2(res[0]["ovl"], oL.cpu().numpy()) < 2e-3
