@@ -528,9 +528,12 @@ def run_reference(args):
     if rank != 0:
         return
     shape = get_shape(args.config)
-    from threadpoolctl import threadpool_info
+    from threadpoolctl import threadpool_info, threadpool_limits
 
     from oracle import moe as om
+    # torchrun sets OMP_NUM_THREADS=1 for every rank; rank 0 alone runs the oracle,
+    # so give its BLAS all of the host cores
+    threadpool_limits(limits=os.cpu_count() or 1)
     w = synth.moe_weights(shape, seed=args.seed)
     lay = om.layer_from_synth(w, shape.top_k)
     del w
