@@ -466,12 +466,21 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   // wasted MMA rows; measured 0.88 -> 0.99 of HBM for Scout decode GEMM1).
   const long avg_rows = (long)T * k * (allreduce ? 1 : ctx->ep) / E;
   const int routed_cg = ctx->gemm_cg ? ctx->gemm_cg : (avg_rows < 256 ? 1 : 2);
+  // decode (single-CTA tiles, weight streaming): pick the tile width with the smaller
+  // last-wave waste from the expected tile count (MMA width is not the bound there)
+  auto pick_bn = [&](int N, bool swiglu) {
+    if (routed_cg != 1 || ctx->gemm_cg) return 0;
+    const long mt = ctx->e_loc * ((avg_rows + 127) / 128), slots = ctx->gemm_ctas;
+    auto cost = [&](int b) { const long nt = swiglu ? N / (b / 2) : N / b; return ((mt * nt + slots - 1) / slots) * b; };
+    return cost(128) * 100 < cost(256) * 95 ? 128 : 0;
+  };
   GemmLaunch g1{};
   g1.A = recv; g1.a_rows = recv_rows; g1.B0 = w->w1; g1.B1 = w->w2; g1.b_rows = (long)ctx->e_loc * c.ffn;
   g1.b_group_rows = c.ffn; g1.K = d; g1.N = c.ffn; g1.G = ctx->e_loc; g1.counts = recv_counts; g1.m_total = 0;
   g1.out = ctx->h; g1.ldo = c.ffn; g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas; g1.cta_group = routed_cg;
   g1.a_idx = a_idx;
   g1.row_base = row_base;
+  g1.bn = pick_bn(c.ffn, true);
   (void)G_loc;
   PH_BEGIN(PH_GEMM1);
   CK(launch_grouped_gemm(g1, s));
@@ -481,6 +490,7 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   g2.b_group_rows = d; g2.K = c.ffn; g2.N = d; g2.G = ctx->e_loc; g2.counts = recv_counts; g2.m_total = 0;
   g2.out = ctx->y; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = routed_cg;
   g2.row_base = row_base;
+  g2.bn = pick_bn(d, false);
   if (ctx->ep > 1 && !allreduce) fsc_transport_scatter_target(ctx, &g2.ret, g2.peer_out);  // P:100 Combine, fused
   if (fused_out && ctx->ep == 1) {   // P:100 "sum the routed experts", fused into the down GEMM
     g2.comb_out = fused_out; g2.comb_resid = fused_resid; g2.src_row = ctx->src_row; g2.pos = ctx->pos;

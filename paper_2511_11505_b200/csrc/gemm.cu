@@ -655,6 +655,7 @@ cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s) {
   if (L.G < 1 || L.G > kMaxGroups || L.K % BK || L.K <= 0) return cudaErrorInvalidValue;
   int bn = gemm_pick_bn(L.epi, L.N);
   if (!bn) return cudaErrorInvalidValue;
+  if (L.bn == 128 && bn == 256 && (L.epi == EPI_SWIGLU ? L.N % 64 == 0 : L.N % 128 == 0)) bn = 128;
   if (L.a_rows == 0) return cudaSuccess;
 #define FSC_GEMM_CASE(BNV, EV)                                  \
   if (bn == BNV && L.epi == EV) {                               \

@@ -65,6 +65,7 @@ struct GemmLaunch {
   void* peer_out[8] = {};
   const int* a_idx = nullptr;         // A gather map (see GemmParams); A then has a_rows source rows
   const int* row_base = nullptr;      // device row offset of group 0 (see GemmParams)
+  int bn = 0;                         // tile width override (0 = auto); must suit N and the epilogue
   float* comb_out = nullptr;          // fused unpermute (see GemmParams)
   const float* comb_resid = nullptr;
   const int* src_row = nullptr;
