@@ -666,24 +666,38 @@ __global__ void __launch_bounds__(256) router_finish_kernel(RouterLaunch L, int 
   const long t0 = (long)blockIdx.x * L.rpb;
   const int rows = (int)min((long)L.rpb, (long)L.T - t0);
   for (int e = tid; e < EP; e += NT) s_wsq[e] = e < L.E ? L.w_sq[e] : 0.f;
-  if (tid < rows) {
-    double ssp = 0.0;
-    for (int sp = 0; sp < nsplit; ++sp) ssp += L.part_sq[(long)sp * L.T + t0 + tid];
+  if (tid < rows) {                       // all split partials in flight, summed in split order
+    double q[kMaxSplit];
+#pragma unroll
+    for (int sp = 0; sp < kMaxSplit; ++sp) q[sp] = sp < nsplit ? L.part_sq[(long)sp * L.T + t0 + tid] : 0.0;
+    double ssp = q[0];
+#pragma unroll
+    for (int sp = 1; sp < kMaxSplit; ++sp)
+      if (sp < nsplit) ssp += q[sp];
     s_r[tid] = (float)(1.0 / sqrt(ssp / (double)L.d + (double)L.eps));
     s_xn[tid] = (float)sqrt(ssp) * 1.0001f;
   }
   __syncthreads();
-  for (int i = tid; i < rows * EP; i += NT) {
-    const int tt = i / EP, e = i % EP;
-    const float* pp = L.part + (t0 + tt) * EP + e;
-    float v[kMaxSplit];
+  for (int i0 = tid; i0 < rows * EP; i0 += 4 * NT) {   // 4 items x nsplit partials in flight per thread
+    float v[4][kMaxSplit];
 #pragma unroll
-    for (int sp = 0; sp < kMaxSplit; ++sp) v[sp] = sp < nsplit ? pp[(long)sp * L.T * EP] : 0.f;
-    float sacc = v[0];
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * NT;
+      const float* pp = L.part + (t0 + i / EP) * EP + i % EP;
 #pragma unroll
-    for (int sp = 1; sp < kMaxSplit; ++sp)
-      if (sp < nsplit) sacc += v[sp];
-    lg[tt * LGS + e] = sacc * s_r[tt];
+      for (int sp = 0; sp < kMaxSplit; ++sp)
+        v[u][sp] = (i < rows * EP && sp < nsplit) ? pp[(long)sp * L.T * EP] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * NT;
+      if (i >= rows * EP) break;
+      float sacc = v[u][0];
+#pragma unroll
+      for (int sp = 1; sp < kMaxSplit; ++sp)
+        if (sp < nsplit) sacc += v[u][sp];
+      lg[(i / EP) * LGS + i % EP] = sacc * s_r[i / EP];
+    }
   }
   __syncthreads();
   router_select_and_xn<EW>(L, lg, s_r, s_xn, s_wsq, rs, t0, rows, chain);
