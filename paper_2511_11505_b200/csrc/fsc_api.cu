@@ -367,8 +367,11 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
   CK(launch_router(rl, s));
   PH_END(PH_ROUTER);
   const bool early_shared = shared_out && (ctx->ep == 1 || ctx->ep_mode == FSC_EP_ALLREDUCE);
-  cudaStream_t ps = early_shared ? ctx->aux : s;   // stream of the permutation work
-  if (early_shared) {
+  // FarSkip at EP = 1: the local permutation (maps + permute) stands in for the dispatch
+  // and runs on the comm stream, overlapping the caller's attention part (b) (P:198 steps 4-5)
+  const bool ep1_async = ctx->ep == 1 && overlap && !early_shared && !ctx->gather_a;
+  cudaStream_t ps = early_shared ? ctx->aux : (ep1_async ? ctx->comm : s);   // stream of the permutation work
+  if (early_shared || ep1_async) {
     CK(cudaEventRecord(ctx->ev_c, s));
     CK(cudaStreamWaitEvent(ps, ctx->ev_c, 0));
   }
@@ -426,6 +429,7 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     PH_BEGIN_ON(PH_DISPATCH, ps);
     CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, ps));
     PH_END_ON(PH_DISPATCH, ps);
+    if (ep1_async) CK(cudaEventRecord(ctx->ev_b, ps));
     if (early_shared) {
       CK(cudaEventRecord(ctx->ev_d, ps));
       int rc = moe_shared(ctx, w, T, shared_resid, shared_out, dbg, s);   // beside the permutation
@@ -448,18 +452,19 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     recv_rows = ctx->recv_rows_cap;
     recv_counts = ctx->recv_counts;
   }
+  if (cb) cb(user, 0, s);  // P:198 step 5: attention part (b) while dispatch is in flight
+  if ((ctx->ep > 1 || ep1_async) && overlap) {  // step 6: sync Dispatch (the compute stream stalls only if late)
+    PH_BEGIN(PH_DISPATCH_STALL);
+    CK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
+    PH_END(PH_DISPATCH_STALL);
+  }
   if (dbg) {
     if (dbg->topk_idx) CK(cudaMemcpyAsync(dbg->topk_idx, ctx->topk_idx, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
     if (dbg->topk_w) CK(cudaMemcpyAsync(dbg->topk_w, ctx->topk_w, sizeof(float) * T * k, cudaMemcpyDeviceToDevice, s));
     if (dbg->counts) CK(cudaMemcpyAsync(dbg->counts, ctx->counts, sizeof(int) * E, cudaMemcpyDeviceToDevice, s));
     if (dbg->pos) CK(cudaMemcpyAsync(dbg->pos, ctx->pos, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
   }
-  if (cb) cb(user, 0, s);  // P:198 step 5: attention part (b) while dispatch is in flight
-  if (ctx->ep > 1 && overlap) {  // step 6: sync Dispatch (the compute stream stalls only if it is late)
-    PH_BEGIN(PH_DISPATCH_STALL);
-    CK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
-    PH_END(PH_DISPATCH_STALL);
-  }
+
   // Routed experts (P:198 step 6): GEMM1 + SwiGLU, GEMM2 (+ fused Combine for EP > 1).
   // cta_group auto: M = 256 CTA-pair tiles when the experts get >= 256 rows on average
   // (prefill), single-CTA M = 128 tiles below that (decode: weight streaming, fewer
