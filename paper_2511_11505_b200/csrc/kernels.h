@@ -42,6 +42,7 @@ struct GemmParams {
   const float* topk_w;         // [T, k]
   int* comb_cnt;               // [T, n_cb] zero between calls (the last arrival resets)
   int top_k, n_cb;
+  int stage_rows;              // bf16 epilogue: 1 = staged row-contiguous stores, 0 = direct
 };
 
 struct GemmLaunch {

@@ -80,3 +80,4 @@ cublas("DS gemm2 (dense equiv)", 49152, 2048, 1408)
 cublas("DS shared1", 8192, 5632, 2048)
 cublas("DS shared2", 8192, 2048, 2816)
 cublas("square 8192^3", 8192, 8192, 8192, iters=5)
+bench("qwen3 gemm2 down (EP1)", 0, 1024, 128, 2048, 768, cg=2)
