@@ -299,3 +299,48 @@ def test_error_paths_are_status_codes_not_crashes():
     torch.cuda.synchronize()
     assert torch.isfinite(out).all()
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["dsv2lite", "qwen3", "scout"])
+def test_bench_launch_configuration_graph_replay(name):
+    """Exactly what bench.py times: the full BASELINE-size layer captured as CUDA graphs
+    with the GEMM1 timing event nodes (fsc_set_timing_mask) and replayed back to back
+    with an L2 flush between steps. Every replay equals the eager run bit for bit, and
+    sampled tokens match the fp64 oracle."""
+    shape = synth.CONFIGS[name]
+    T = shape.tokens
+    ctx = make_ctx(shape, T)
+    w = synth.moe_weights(shape, seed=3)
+    wd = moe_weights_dev(w)
+    x = synth.tokens(shape, seed=3, T=T)
+    xin = dev_f32(x)
+    eager = torch.empty_like(xin)
+    ctx.moe_forward_blocking(wd, xin, eager)
+    torch.cuda.synchronize()
+    outs = [torch.empty_like(xin) for _ in range(2)]
+    ctx.set_timing_mask(["gemm1"])
+    graphs = []
+    for o in outs:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            ctx.moe_forward_blocking(wd, xin, o)
+        graphs.append(g)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    for i in range(4):
+        flush.fill_(float(i))
+        graphs[i % 2].replay()
+    torch.cuda.synchronize()
+    log = ctx.timing_log(64)
+    ctx.set_timing(False)
+    assert log and all(n == "gemm1" and ms > 0 for n, ms in log)
+    for o in outs:
+        assert torch.equal(o, eager)
+    sample = np.array([0, 1, T // 2, T - 1])
+    lay = om.layer_from_synth(w, shape.top_k)
+    idx = torch.empty(T, shape.top_k, dtype=torch.int32, device="cuda")
+    from paper_2511_11505_b200 import MoeDebug
+    ctx.moe_forward_blocking(wd, xin, torch.empty_like(xin), MoeDebug(topk_idx=idx))
+    r, _ = om.adopt_router(lay, x[sample], idx.cpu().numpy()[sample])
+    sh, ro, _ = om.moe_block(x[sample], lay, router=r)
+    assert rel_l2(outs[0].cpu().numpy()[sample], (x[sample].astype(np.float64) + sh) + ro) < TOL
+    ctx.close()
