@@ -184,6 +184,13 @@ FSC_API int fsc_set_ep_mode(fsc_ctx* ctx, int mode);
  * oracle's moe_block_ep_fp8. d % 128 == 0. Call before fsc_bootstrap_export. */
 FSC_API int fsc_set_dispatch_fp8(fsc_ctx* ctx, int on);
 
+/* Debug finiteness check (the error class of SPEC S:29): when on, every
+ * fsc_moe_forward_blocking, fsc_moe_wait (and so every layer of
+ * fsc_layer_stack_forward) counts the non-finite values of its fp32 output on the
+ * device, SYNCHRONISES the stream and returns FSC_ERR_NONFINITE (not sticky) if
+ * there is any. Not allowed under stream capture (FSC_ERR_STATE). Default off. */
+FSC_API int fsc_set_debug_checks(fsc_ctx* ctx, int on);
+
 /* Per-phase CUDA-event timing of the MoE calls (bench / profiling). When enabled,
  * events are recorded on the call's stream around every phase; fsc_get_timings
  * waits for the last call's events and writes n <= 9 durations in ms (-1 = phase
@@ -220,8 +227,9 @@ FSC_API int fsc_moe_forward_blocking_host(fsc_ctx* ctx, const fsc_moe_weights* w
  * x_in_host (pinned) on an internal copy stream, the forward on `stream` and the
  * D2H copy into out_host (pinned) on a second copy stream, ordered by events on
  * two internal staging slots, and returns at once. Step i's compute therefore
- * overlaps step i+1's upload and step i-1's download. Host buffers must stay
- * untouched until fsc_host_flush returns (or two calls later). */
+ * overlaps step i+1's upload and step i-1's download. The host buffers of call i
+ * may be reused once call i+2 has returned (call i+2 waits on the host for call i's
+ * download before it enqueues anything) or after fsc_host_flush. */
 FSC_API int fsc_moe_forward_host_async(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in_host,
                                        float* out_host, void* stream);
 /* Wait until every fsc_moe_forward_host_async output has reached host memory. */
@@ -238,7 +246,11 @@ FSC_API int fsc_moe_forward_farskip(fsc_ctx* ctx, const fsc_moe_weights* w, int 
 
 /* Complete a FarSkip handle: waits (in stream order) for its combine and writes
  *   full_out = partial_in + routed-exp-out_k   (= mlp-in_{k+1} = o_k)
- * full_out may alias partial_in. FSC_ERR_STATE if h was already waited. */
+ * full_out may alias partial_in. FSC_ERR_STATE if h was already waited.
+ * Stream requirement: call fsc_moe_wait on the SAME stream as the
+ * fsc_moe_forward_farskip that made h, and issue the next fsc_moe_forward_farskip
+ * on that stream too (or order the streams with events yourself): the next call
+ * reuses the receive / combine buffers that this wait reads (write-after-read). */
 FSC_API int fsc_moe_wait(fsc_ctx* ctx, fsc_handle h, const float* partial_in, float* full_out, void* stream);
 
 /* ---------------------------------------------------------------- stack */

@@ -12,7 +12,8 @@ heads and rotary position embedding (C-amb-18):
            g = h // (Hq / Hkv)
   out    = concat_h(o_h) W_o^T
 Parity of this filler against the paper is unpinned beyond the textbook
-special cases in tests/test_oracle_attention.py (T=1, zero weights, causality).
+special cases in tests/test_oracle_stack.py (T=1, zero weights, causality,
+sequence packing, RoPE invariants).
 """
 from __future__ import annotations
 

@@ -398,24 +398,6 @@ def adopt_router(layer: EpLayer, x: np.ndarray, gpu_idx: np.ndarray, margin: flo
     return r, excl
 
 
-# ---------------------------------------------------------------------------
-# Sub-block outputs in the two wirings (C-amb-12 summation order)
-# ---------------------------------------------------------------------------
-
-def moe_sublayer_blocking(x_in, layer: EpLayer):
-    """Regular MoE sub-block: out = (x_in + shared) + routed (Eq. 6, C-amb-12)."""
-    sh, ro, r = moe_block(x_in, layer)
-    return (np.asarray(x_in, np.float64) + sh) + ro, sh, ro, r
-
-
-def moe_sublayer_farskip(x_in, partial_in, layer: EpLayer):
-    """FarSkip MoE sub-block: partial = partial_in + shared
-    (= attn-in_{k+1}); full = partial + routed (= mlp-in_{k+1} = o_k)."""
-    sh, ro, r = moe_block(x_in, layer)
-    partial = np.asarray(partial_in, np.float64) + sh
-    return partial, partial + ro, sh, ro, r
-
-
 def layer_from_synth(w, top_k: int) -> EpLayer:
     """Widen a synth.MoeWeights (bf16 bits) to fp64 exactly."""
     def wid(b):

@@ -73,6 +73,7 @@ _SIGS = {
     "fsc_set_router_int8": (_I, [_P, _I]),
     "fsc_set_ep_mode": (_I, [_P, _I]),
     "fsc_set_dispatch_fp8": (_I, [_P, _I]),
+    "fsc_set_debug_checks": (_I, [_P, _I]),
     "fsc_set_timing": (_I, [_P, _I]),
     "fsc_set_timing_mask": (_I, [_P, ctypes.c_uint]),
     "fsc_get_timings": (_I, [_P, ctypes.POINTER(ctypes.c_float), _I]),
@@ -266,6 +267,10 @@ class Context:
         """Blocking EP = 1: gate-weighted unpermute fused into the down GEMM epilogue
         (True / False; None = auto: top-1 routing only)."""
         self._ck(self.lib.fsc_set_fused_unpermute(self.h, -1 if on is None else int(on)))
+
+    def set_debug_checks(self, on: bool):
+        """Finiteness check of every output (synchronises; FSC_ERR_NONFINITE on failure)."""
+        self._ck(self.lib.fsc_set_debug_checks(self.h, int(on)))
 
     def set_gemm_ctas(self, n: int):
         self._ck(self.lib.fsc_set_gemm_ctas(self.h, n))

@@ -269,13 +269,8 @@ static cudaError_t launch_fa_t(const uint16_t* qkv, uint16_t* out, int T, int Hq
                                cudaStream_t s) {
   constexpr int LD = HD + 8;
   const size_t smem = (size_t)(FA_BM + 4 * FA_BN) * LD * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(flash_attn_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (cudaError_t e = ensure_smem_attr(flash_attn_fwd_kernel<HD>, (int)smem, attr)) return e;
   dim3 grid((T + FA_BM - 1) / FA_BM, Hq);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
   ++g_launches;

@@ -6,11 +6,28 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #define FSC_DEVINL __device__ __forceinline__
 
 namespace fsc {
 
 constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device). The
+// attribute belongs to the device context, so a context on a second GPU in the same
+// process sets it again; `flag` (one static per call site) keeps one bit per device.
+template <typename K>
+inline cudaError_t ensure_smem_attr(K kern, int bytes, std::atomic<unsigned long long>& flag) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (flag.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) flag.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // ------------------------------------------------------------------ bf16
 FSC_DEVINL uint32_t pack_bf16x2(float lo, float hi) {

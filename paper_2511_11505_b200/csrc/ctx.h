@@ -32,6 +32,8 @@ struct fsc_ctx {
   int router_i8 = 0;           // exact int8 tensor-core router (fsc_set_router_int8)
   int gather_a = 0;            // EP = 1: GEMM1 gathers A through src_row (fused permute)
   int sticky = 0;
+  int debug_checks = 0;        // fsc_set_debug_checks: finiteness check of every output (syncs)
+  int* nf_count = nullptr;     // [1] device counter of non-finite output values
   char err[512] = {0};
 
   // per-call workspace (device), sized for cfg at fsc_init
@@ -107,6 +109,10 @@ struct fsc_ctx {
 };
 
 void fsc_set_error(fsc_ctx* c, const char* fmt, ...);
+// argument checks of one MoE call (weights, T, activation pointers, alignment); no enqueue
+int fsc_validate_moe(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, const void* out);
+// debug finiteness check of an fp32 [n] output (fsc_set_debug_checks): synchronises s
+int fsc_check_finite(fsc_ctx* ctx, const float* out, long n, cudaStream_t s, const char* what);
 
 // transport (EP > 1). All return fsc_status.
 size_t fsc_transport_blob_size();

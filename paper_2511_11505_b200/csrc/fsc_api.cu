@@ -144,6 +144,7 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(dalloc(&ctx->tmp, T * d));
   CK(dalloc(&ctx->io_in, T * d));
   CK(dalloc(&ctx->io_out, T * d));
+  CK(dalloc(&ctx->nf_count, 1));
   CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, -5));
   CK(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
@@ -173,7 +174,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->i8_x, ctx->i8_w, ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2]};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->i8_x, ctx->i8_w, ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2], ctx->nf_count};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -251,6 +252,26 @@ extern "C" int fsc_timing_log(fsc_ctx* ctx, int* phase, float* ms, int cap) {
   return n;
 }
 
+extern "C" int fsc_set_debug_checks(fsc_ctx* ctx, int on) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  ctx->debug_checks = on ? 1 : 0;
+  return FSC_OK;
+}
+
+int fsc_check_finite(fsc_ctx* ctx, const float* out, long n, cudaStream_t s, const char* what) {
+  if (!ctx->debug_checks || n == 0) return FSC_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(s, &cs));
+  REQUIRE(cs == cudaStreamCaptureStatusNone, FSC_ERR_STATE, "debug checks synchronise: not under stream capture");
+  CK(cudaMemsetAsync(ctx->nf_count, 0, sizeof(int), s));
+  CK(launch_count_nonfinite(out, n, ctx->nf_count, s));
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, ctx->nf_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  REQUIRE(bad == 0, FSC_ERR_NONFINITE, "%s: %d non-finite values (debug check)", what, bad);
+  return FSC_OK;
+}
+
 extern "C" int fsc_set_gemm_cta_group(fsc_ctx* ctx, int cg) {
   if (!ctx) return FSC_ERR_SHAPE;
   REQUIRE(cg == 0 || cg == 1 || cg == 2, FSC_ERR_CONFIG, "cta_group must be 0 (auto), 1 or 2");
@@ -326,7 +347,7 @@ extern "C" int fsc_set_gemm_ctas(fsc_ctx* ctx, int n) {
 
 // ---------------------------------------------------------------------------- MoE pieces
 
-static int validate_call(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, const void* out) {
+int fsc_validate_moe(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, const void* out) {
   if (!ctx) return FSC_ERR_SHAPE;
   if (ctx->sticky) return ctx->sticky;
   REQUIRE(w && w->gamma && w->w_router && w->w1 && w->w2 && w->w3, FSC_ERR_SHAPE, "null weight pointer");
@@ -338,6 +359,9 @@ static int validate_call(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const fl
               aligned16(w->gamma) && aligned16(w->w_router),
           FSC_ERR_SHAPE, "pointers must be 16-byte aligned");
   return FSC_OK;
+}
+static int validate_call(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, const void* out) {
+  return fsc_validate_moe(ctx, w, T, x_in, out);
 }
 
 // Forward declarations (shared expert used by the blocking overlap below)
@@ -605,8 +629,18 @@ static int moe_finish(fsc_ctx* ctx, int T, const float* resid, float* out, const
 
 // ---------------------------------------------------------------------------- MoE entry points
 
+static int moe_blocking_impl(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, float* out,
+                             const fsc_moe_debug* dbg, void* stream);
+
 extern "C" int fsc_moe_forward_blocking(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, float* out,
                                         const fsc_moe_debug* dbg, void* stream) {
+  int rc = moe_blocking_impl(ctx, w, T, x_in, out, dbg, stream);
+  if (rc) return rc;
+  return fsc_check_finite(ctx, out, (long)T * ctx->cfg.d, static_cast<cudaStream_t>(stream), "fsc_moe_forward_blocking");
+}
+
+static int moe_blocking_impl(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, float* out,
+                             const fsc_moe_debug* dbg, void* stream) {
   int rc = validate_call(ctx, w, T, x_in, out);
   if (rc) return rc;
   REQUIRE(!ctx->pending, FSC_ERR_STATE, "a FarSkip handle is outstanding");
@@ -677,6 +711,9 @@ extern "C" int fsc_moe_forward_host_async(fsc_ctx* ctx, const fsc_moe_weights* w
   }
   const int slot = ctx->io_slot;
   ctx->io_slot ^= 1;
+  // the slot's previous call (two calls ago) must have finished its D2H into the caller's
+  // out_host before this call returns, so that "two calls later" the host buffers are free
+  CK(cudaEventSynchronize(ctx->ev_out[slot]));
   const size_t bytes = sizeof(float) * (size_t)T * ctx->cfg.d;
   CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_cdone[slot], 0));      // slot's previous compute read its input
   CK(cudaMemcpyAsync(ctx->io_slot_in[slot], x_in_host, bytes, cudaMemcpyHostToDevice, ctx->h2d));
@@ -735,7 +772,9 @@ extern "C" int fsc_moe_wait(fsc_ctx* ctx, fsc_handle h, const float* partial_in,
   ctx->pending = 0;
   fsc_moe_debug dbg{};
   dbg.routed_out = h->dbg_routed;
-  return moe_finish(ctx, h->T, partial_in, full_out, dbg.routed_out ? &dbg : nullptr, s);
+  int rc = moe_finish(ctx, h->T, partial_in, full_out, dbg.routed_out ? &dbg : nullptr, s);
+  if (rc) return rc;
+  return fsc_check_finite(ctx, full_out, (long)h->T * ctx->cfg.d, s, "fsc_moe_wait");
 }
 
 // ---------------------------------------------------------------------------- op-level entry points

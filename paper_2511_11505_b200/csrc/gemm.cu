@@ -635,12 +635,8 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   if (!make_map(&mb0, L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
   if (!make_map(&mb1, L.B1 ? L.B1 : L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
   auto kern = grouped_gemm_kernel<BN, EPI, CG>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<unsigned long long> attr_set{0};
+  if (cudaError_t e = ensure_smem_attr(kern, C::SMEM, attr_set)) return e;
   GemmParams p;
   p.counts = L.counts;
   p.G = L.G;

@@ -149,5 +149,7 @@ cudaError_t launch_flash_attn(const uint16_t* qkv, uint16_t* out, int T, int Hq,
 
 // elementwise helpers
 cudaError_t launch_copy_f32(const float* src, float* dst, long n, cudaStream_t s);
+// debug: *bad += number of non-finite values of x [n] (n % 4 == 0)
+cudaError_t launch_count_nonfinite(const float* x, long n, int* bad, cudaStream_t s);
 
 }  // namespace fsc

@@ -271,4 +271,26 @@ cudaError_t launch_copy_f32(const float* src, float* dst, long n, cudaStream_t s
   return cudaGetLastError();
 }
 
+// Debug finiteness check (FSC_ERR_NONFINITE, fsc_set_debug_checks): count the
+// non-finite fp32 values of x [n] into *bad.
+__global__ void __launch_bounds__(256) nonfinite_kernel(const float4* __restrict__ x, long n4, int* bad) {
+  int c = 0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+    const float4 v = x[i];
+    c += !isfinite(v.x) + !isfinite(v.y) + !isfinite(v.z) + !isfinite(v.w);
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(bad, c);
+}
+
+cudaError_t launch_count_nonfinite(const float* x, long n, int* bad, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  long blocks = (n / 4 + 255) / 256;
+  if (blocks > kNumSMs * 4) blocks = kNumSMs * 4;
+  if (blocks < 1) blocks = 1;
+  ++g_launches;
+  nonfinite_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(x), n / 4, bad);
+  return cudaGetLastError();
+}
+
 }  // namespace fsc

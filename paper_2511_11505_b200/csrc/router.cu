@@ -1083,12 +1083,8 @@ static cudaError_t launch_router_i8(const RouterLaunch& L, cudaStream_t s) {
   CUtensorMap ma, mb;
   if (!i8_make_map(&ma, L.i8_x, (long)I8_NP * L.T, L.d, I8_BM)) return cudaErrorInvalidValue;
   if (!i8_make_map(&mb, L.i8_w, (long)I8_NP * I8_EP, L.d, I8_EP)) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(router_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (cudaError_t e = ensure_smem_attr(router_i8_kernel, I8_SMEM, attr)) return e;
   const int nblk = (L.T + I8_BM - 1) / I8_BM;
   int nsplit = kNumSMs / nblk;                                 // fill the SMs: split d across CTAs
   if (nsplit > I8_MAX_SPLIT) nsplit = I8_MAX_SPLIT;
@@ -1126,12 +1122,8 @@ static cudaError_t launch_router_t(const RouterLaunch& L, cudaStream_t s) {
   if (nsplit > 1 && (long)nsplit * L.T > kRouterSplitRows) return cudaErrorInvalidValue;
   router_prescale_kernel<<<EP, 256, 0, s>>>(L.w_router, L.gamma, L.w_scaled, L.w_sq, L.E, L.d, EP);
   const size_t smem = (size_t)(NS * (TB * LDS + DC * EP) + 2 * TB + EP) * 4 + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(router_kernel<EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (cudaError_t e = ensure_smem_attr(router_kernel<EW>, (int)smem, attr)) return e;
   router_kernel<EW><<<dim3(grid, nsplit), 256, smem, s>>>(LL);
   g_launches += 2;
   if (nsplit > 1) {   // 8 tokens per finish CTA: more CTAs in flight for the latency-bound epilogue

@@ -168,6 +168,13 @@ int copy_f32(fsc_ctx* ctx, float* dst, const float* src, long n, cudaStream_t s)
 
 }  // namespace
 
+static int stack_body(fsc_ctx* ctx, const fsc_attn_weights* attn, const fsc_moe_weights* moe, int L, int T,
+                      int seq_len, const int* modes, int schedule, const float* o0, float* oL,
+                      const fsc_act_cache* cache, cudaStream_t s, fsc_handle* h_out);
+
+// Everything is validated before the first enqueue (fsc.h contract). If an enqueue
+// fails half way (a CUDA error, sticky), the pending FarSkip handle is completed into
+// scratch so that the context (and, at EP > 1, the peers) is not left waiting.
 extern "C" int fsc_layer_stack_forward(fsc_ctx* ctx, const fsc_attn_weights* attn, const fsc_moe_weights* moe, int L,
                                        int T, int seq_len, const int* modes, int schedule, const float* o0, float* oL,
                                        const fsc_act_cache* cache, void* stream) {
@@ -190,9 +197,26 @@ extern "C" int fsc_layer_stack_forward(fsc_ctx* ctx, const fsc_attn_weights* att
     SREQ(((a.n_heads + 2 * a.n_kv_heads) * a.head_dim) % 64 == 0 && (a.n_heads * a.head_dim) % 64 == 0,
          FSC_ERR_CONFIG, "stack: projection widths must be multiples of 64");
   }
+  for (int k = 0; k < L; ++k) {
+    SRC(fsc_validate_moe(ctx, &moe[k], T, o0, oL));
+    SREQ(((reinterpret_cast<uintptr_t>(attn[k].w_qkv) | reinterpret_cast<uintptr_t>(attn[k].w_o) |
+           reinterpret_cast<uintptr_t>(attn[k].gamma)) & 15) == 0,
+         FSC_ERR_SHAPE, "stack: attention weights of layer %d must be 16-byte aligned", k);
+  }
   SCK(cudaSetDevice(ctx->device));
   SRC(ensure_workspace(ctx, attn, L));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  fsc_handle h = nullptr;
+  const int rc = stack_body(ctx, attn, moe, L, T, seq_len, modes, schedule, o0, oL, cache, s, &h);
+  if (rc && ctx->pending && h) fsc_moe_wait(ctx, h, ctx->rbuf[0], ctx->rbuf[1], s);   // best effort
+  ctx->no_overlap = 0;
+  ctx->attn_pending = 0;
+  return rc;
+}
+
+static int stack_body(fsc_ctx* ctx, const fsc_attn_weights* attn, const fsc_moe_weights* moe, int L, int T,
+                      int seq_len, const int* modes, int schedule, const float* o0, float* oL,
+                      const fsc_act_cache* cache, cudaStream_t s, fsc_handle* h_out) {
   const int d = ctx->cfg.d;
   const long n = (long)T * d;
   const bool ov = schedule == FSC_OVERLAPPED;
@@ -200,7 +224,7 @@ extern "C" int fsc_layer_stack_forward(fsc_ctx* ctx, const fsc_attn_weights* att
   float* bufM = ctx->rbuf[1];   // mlp-in of the current layer (M_k)
   float* bufP = ctx->rbuf[2];   // partial of the current layer (A_{k+1} in progress)
   SRC(copy_f32(ctx, bufA, o0, n, s));
-  fsc_handle h = nullptr;       // pending routed output: o_{k-1} = bufA + routed_{k-1}
+  fsc_handle& h = *h_out;       // pending routed output: o_{k-1} = bufA + routed_{k-1}
   ctx->no_overlap = ov ? 0 : 1;
   int prev_k = -1;
   for (int k = 0; k < L; ++k) {
@@ -261,7 +285,7 @@ extern "C" int fsc_layer_stack_forward(fsc_ctx* ctx, const fsc_attn_weights* att
   // final o_L = A_{L+1} + routed_L: the last combine has nothing to overlap
   SRC(attn_finish(ctx, bufA, s));
   SRC(fsc_moe_wait(ctx, h, bufA, oL, s));
+  h = nullptr;
   if (cache) SRC(copy_f32(ctx, cache[L - 1].o, oL, n, s));
-  ctx->no_overlap = 0;
   return FSC_OK;
 }

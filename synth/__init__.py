@@ -97,7 +97,7 @@ def decode_shape(base: str, tokens: int) -> MoeShape:
 
 _KIND = {"x": 1, "gamma": 2, "w_router": 3, "w1": 4, "w2": 5, "w3": 6,
          "ws1": 7, "ws2": 8, "ws3": 9, "attn_gamma": 10, "w_qkv": 11, "w_o": 12,
-         "router_bias": 13}
+         "skew_mean": 13}
 
 
 def _rng(seed: int, layer: int, kind: str, sub: int = 0) -> np.random.Generator:
@@ -109,11 +109,26 @@ def _normal(seed, layer, kind, sub, shape, std) -> np.ndarray:
     return (g.standard_normal(shape, dtype=np.float32) * np.float32(std)).astype(np.float32)
 
 
+SKEW_DEFAULT = 0.15   # the skewed-load variant's max/mean expert load ~1.5-2x
+
+
 def tokens(shape: MoeShape, seed: int = 0, rank: int = 0, T: Optional[int] = None,
-           layer: int = 0) -> np.ndarray:
-    """x ~ N(0,1) fp32 [T, d] for one rank."""
+           layer: int = 0, skew: float = 0.0) -> np.ndarray:
+    """x ~ N(0,1) fp32 [T, d] for one rank.
+
+    skew > 0 is the skewed-load variant (reading C-amb-21):
+    every token gets the same mean vector m ~ N(0, skew^2) (one draw per (seed, layer),
+    shared by all ranks), x = z + m. The router stays the paper's pure linear map
+    G(A) = s(A W_R^T); the shift adds to expert e's logit the offset
+    r (m . gamma W_R[e]), ~N(0, skew^2) relative to the token part, so the same
+    experts are hot on every rank. Measured max/mean expert load (4096 tokens):
+    skew 0.15 (SKEW_DEFAULT) 1.9x DS-V2-Lite, 1.9x Qwen3, 1.65x Scout; skew 0.5:
+    5-6x (stress)."""
     T = shape.tokens if T is None else T
-    return _normal(seed, layer, "x", rank, (T, shape.d), 1.0)
+    x = _normal(seed, layer, "x", rank, (T, shape.d), 1.0)
+    if skew:
+        x = (x + _normal(seed, layer, "skew_mean", 0, (shape.d,), skew)).astype(np.float32)
+    return x
 
 
 @dataclasses.dataclass
@@ -175,14 +190,3 @@ def attn_weights(shape: MoeShape, seed: int = 0, layer: int = 0, zero_o: bool = 
     if zero_o:
         w_o[:] = 0
     return AttnWeights(gamma, w_qkv, w_o, hq, hkv, hd)
-
-
-def router_bias(shape: MoeShape, seed: int = 0, layer: int = 0, std: float = 0.5) -> np.ndarray:
-    """Skewed-load variant: b_e ~ N(0, std) added to W_R rows' effect.
-
-    Realised as an input transform: the GPU and the oracle both see a modified
-    x-independent logit offset folded into an extra constant feature is not part
-    of the paper; instead we scale W_R rows, which keeps the router a pure
-    linear map G(A) = s(A W_R^T)."""
-    g = _rng(seed, layer, "router_bias", 0)
-    return np.exp(g.standard_normal(shape.n_experts) * std).astype(np.float32)

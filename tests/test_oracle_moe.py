@@ -323,3 +323,33 @@ def test_fp8_dispatch_block_matches_exact_block_within_fp8_error():
         np.testing.assert_array_equal(sh0, sh1)                          # shared expert: local, unquantised
         err = np.linalg.norm(ro1 - ro0) / np.linalg.norm(ro0)
         assert 1e-3 < err < 8e-2                                         # FP8-level, not exact, not broken
+
+
+def _bf16_brute_nearest_even(x32):
+    """Nearest bf16 by brute force: the two bf16 neighbours of each fp32 value (bit
+    truncation and the next bf16 away from zero), the closer one in fp64, exact ties
+    to the even bf16 mantissa (IEEE round-to-nearest-even)."""
+    u = np.asarray(x32, np.float32).view(np.uint32)
+    lo = (u & 0xFFFF0000).astype(np.uint32)
+    hi = (lo + 0x10000).astype(np.uint32)
+    f = lambda b: b.view(np.float32).astype(np.float64)  # noqa: E731
+    x, a, b = np.asarray(x32, np.float32).astype(np.float64), f(lo), f(hi)
+    da, db = np.abs(x - a), np.abs(x - b)
+    even_lo = ((lo >> 16) & 1) == 0
+    pick_lo = (da < db) | ((da == db) & even_lo)
+    return np.where(pick_lo, a, b)
+
+
+def test_bf16_rne_exact_ties_and_brute_force():
+    """bf16_rne (the kernels' cvt.rn.bf16.f32) against the format: exact halfway
+    cases go to the even mantissa, and random values to the nearest bf16."""
+    ulp = 2.0 ** -7                                                   # bf16 spacing in [1, 2)
+    ties = np.array([1 + ulp / 2, 1 + 3 * ulp / 2, 2 - ulp / 2, 1.5 + ulp / 2], np.float32)
+    want = [1.0, 1 + 2 * ulp, 2.0, 1.5]                               # halfway -> even mantissa
+    got = om.bf16_rne(ties)
+    assert got.tolist() == want
+    np.testing.assert_array_equal(om.bf16_rne(-ties), -got)            # sign symmetric
+    assert om.bf16_rne(np.float32(1 + ulp / 2 + 2 ** -20)) == 1 + ulp  # just above the tie: up
+    v = (rng(9).standard_normal(20000) * np.exp(rng(10).uniform(-30, 30, 20000))).astype(np.float32)
+    v[:200] = ((v[:200].view(np.uint32) & 0xFFFF0000) | 0x8000).view(np.float32)   # 200 exact ties
+    np.testing.assert_array_equal(om.bf16_rne(v), _bf16_brute_nearest_even(v))
