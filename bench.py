@@ -216,6 +216,12 @@ def run_gpu(args):
                   shared_ffn=shape.shared_ffn, max_tokens=T, rank=erank, ep_size=ep, device=local)
     if args.cta_group:
         ctx.set_gemm_cta_group(args.cta_group)
+    from paper_2511_11505_b200 import (FSC_BLOCKING_REGULAR_PLUS, FSC_BLOCKING_SERIAL, FSC_COMBINE_FUSED,
+                                       FSC_COMBINE_STREAM)
+    ctx.set_combine_mode(FSC_COMBINE_FUSED if args.combine == "fused" else FSC_COMBINE_STREAM)
+    ctx.set_blocking_mode(FSC_BLOCKING_SERIAL if args.blocking == "serial" else FSC_BLOCKING_REGULAR_PLUS)
+    if args.comm_ctas:
+        ctx.set_comm_ctas(args.comm_ctas)
     if ep > 1:
         if args.dispatch_fp8 and not allreduce:
             ctx.set_dispatch_fp8(True)
@@ -416,14 +422,17 @@ def run_gpu(args):
     if allreduce:
         a2a_bytes = 2.0 * (ep - 1) / ep * T * shape.d * 4     # fp32 reduce-scatter + all-gather per rank
     w_bytes = 2.0 * 3 * shape.d * (e_loc * shape.ffn + shape.shared_ffn)
-    layer_roof_ms = max(exp_flop / (peaks["bf16_tflops"] * 1e12), a2a_bytes / 770e9,
+    layer_roof_ms = max(exp_flop / (peaks["bf16_tflops"] * 1e12), a2a_bytes / (NVLINK_GBS * 1e9),
                         w_bytes / (peaks["hbm_gbs"] * 1e9)) * 1e3
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if allreduce else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": dict(workload_config(shape, ep, world, "blocking"),
+        "config": dict(workload_config(shape, ep, world, "blocking (serial, Eq. 6)" if args.blocking == "serial" else
+                                       "blocking (Regular+: shared expert beside the in-flight combine, P:103)"),
+                       combine=("fused into the down GEMM epilogue" if args.combine == "fused" else
+                                "comm-stream push after the down GEMM") if ep > 1 else None,
                        **({"ep_mode": "allreduce (replicated tokens, P:215-217)", "global_tokens": T}
                           if allreduce else {"ep_mode": "all-to-all (dispatch / combine)",
                                              "dispatch_payload": "fp8 e4m3 + per-128-col scales"
@@ -432,8 +441,8 @@ def run_gpu(args):
         "layer_roofline": {"expert_flop": exp_flop, "t_roof_ms": layer_roof_ms,
                            "a2a_bytes": a2a_bytes, "frac": layer_roof_ms / ms_per_step,
                            "weight_bytes": w_bytes,
-                           "note": "max(expert FLOPs / bf16 burst peak, a2a bytes / 770 GB/s measured NVLink "
-                                   "peer bandwidth, expert weight bytes / HBM); a2a = 0 at EP=1"},
+                           "note": "max(expert FLOPs / bf16 burst peak, a2a bytes leaving the rank / 900 GB/s "
+                                   "NVLink 5 per direction (spec), expert weight bytes / HBM); a2a = 0 at EP=1"},
         "phase_ms": phase_ms, "phase_timing": phase_src,
         "exposed_a2a_us_per_layer": (stack or {}).get("exposed_a2a_us_per_layer",
                                                        {"farskip": None, "blocking": None}),
@@ -460,65 +469,140 @@ def run_gpu(args):
 
 
 # ----------------------------------------------------------------------------- stack (FarSkip vs blocking)
+NVLINK_GBS = 900.0          # NVLink 5 per direction per GPU (spec; not measurable on the one-GPU dev box)
+COMPUTE_PHASES = {"router", "perm_maps", "gemm1", "gemm2", "shared1", "shared2", "unpermute", "attn_a", "attn_b"}
+COMM_PHASES = {"dispatch", "combine", "dispatch_stall", "combine_wait"}
+
+
+def _union(iv):
+    out = []
+    for a, b in sorted(iv):
+        if out and a <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
+def exposed_from_timeline(tl):
+    """Exposed communication (C-amb-14) from fsc_timeline's [(phase, stream, t0_ms, dur_ms)]:
+    the measure of the union of communication intervals (dispatch and combine kernels on
+    any stream, plus the compute stream's waits for peers: dispatch stall, combine wait)
+    not covered by the union of compute-phase intervals on this GPU. Returns
+    (exposed_ms, communication_union_ms)."""
+    comp = _union([(t0, t0 + du) for ph, _, t0, du in tl if ph in COMPUTE_PHASES])
+    comm = _union([(t0, t0 + du) for ph, _, t0, du in tl if ph in COMM_PHASES and du > 0])
+    comm_ms = sum(b - a for a, b in comm)
+    cov = sum(max(0.0, min(b, e) - max(a, s)) for a, b in comm for s, e in comp)
+    return comm_ms - cov, comm_ms
+
+
+def attention_flop(shape, T):
+    """FLOPs of the attention filler per layer (causal GQA, packed sequences): part (a)
+    = QKV projection, part (b) = core (QK^T and PV over the causal half) + o-projection."""
+    hq, hkv, hd, d, sl = shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.d, shape.seq_len
+    a = 2.0 * T * d * (hq + 2 * hkv) * hd
+    b = 2.0 * 2.0 * T * (sl + 1) / 2.0 * hq * hd + 2.0 * T * hq * hd * d
+    return a, b
+
+
 def stack_measure(ctx, shape, wd, x, L, steps, world, dev, rank, seed):
-    """L-layer Hybrid (FarSkip-wired) stack with the attention filler, timed in the
-    BLOCKING and OVERLAPPED schedules (same kernels, same numbers). Exposed
-    all-to-all per layer = compute-stream time spent in communication:
-    blocking: dispatch (counts exchange + dispatch copy + wait) + combine wait;
-    FarSkip: dispatch stall of the compute stream + combine wait. The MoE weights
-    of layer 0 are reused for every layer (timing only)."""
+    """L-layer stack with the attention filler in four schedules (same kernels, same
+    numbers): FarSkip = Hybrid wiring + OVERLAPPED; Regular = Eq. 6 wiring run
+    BLOCKING (serialised; the headline baseline, C-amb-16); Regular+ = Eq. 6
+    wiring, OVERLAPPED (the shared expert beside the in-flight combine); and each again
+    with the zero-byte all-to-all (fsc_set_a2a_zero_bytes) for the cross-check
+    exposed ~= t_layer - t_layer(zero-byte). Per-phase intervals come from the library's
+    CUDA-event timeline (fsc_timeline); exposed = communication not covered by compute.
+    The MoE weights of layer 0 are reused for every layer (timing only)."""
     import torch
     import torch.distributed as dist
 
-    from paper_2511_11505_b200 import FSC_BLOCKING, FSC_HYBRID, FSC_OVERLAPPED
+    from paper_2511_11505_b200 import FSC_BLOCKING, FSC_HYBRID, FSC_OVERLAPPED, FSC_REGULAR
     from tests.gpu_util import attn_weights_dev
     aw = attn_weights_dev(synth.attn_weights(shape, seed=seed), dev)
     o0 = x
     oL = torch.empty_like(x)
-    res = {}
     stream = torch.cuda.current_stream(dev)
-    for name, sched in (("blocking", FSC_BLOCKING), ("farskip", FSC_OVERLAPPED)):
-        def run():
-            ctx.layer_stack_forward([aw] * L, [wd] * L, shape.tokens, shape.seq_len, [FSC_HYBRID] * L, sched, o0, oL,
-                                    stream=stream.cuda_stream)
-        for _ in range(2):
-            run()
-        torch.cuda.synchronize(dev)
+    T = shape.tokens
+    schedules = (("farskip", [FSC_HYBRID] * L, FSC_OVERLAPPED), ("regular", [FSC_REGULAR] * L, FSC_BLOCKING),
+                 ("regular_plus", [FSC_REGULAR] * L, FSC_OVERLAPPED))
+    res = {}
+    for zb in (False, True):
         if world > 1:
-            dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(steps):
-            run()
-        b.record(stream)
-        torch.cuda.synchronize(dev)
-        t = a.elapsed_time(b) / steps
-        ctx.set_timing(True)
-        for _ in range(steps):
-            run()
-        log = ctx.timing_log(4096)
-        ctx.set_timing(False)
-        comm = {"dispatch": 0.0, "dispatch_stall": 0.0, "combine_wait": 0.0}
-        for ph, ms in log:
-            if ph in comm:
-                comm[ph] += ms
-        exposed = (comm["dispatch"] if name == "blocking" else comm["dispatch_stall"]) + comm["combine_wait"]
-        vals = allreduce_max([t, exposed / steps / L], dev)
-        res[name] = {"ms_per_stack": float(vals[0]), "ms_per_layer": float(vals[0]) / L,
-                     "exposed_comm_us_per_layer": float(vals[1]) * 1e3,
-                     "phase_ms_per_layer": {k: v / steps / L for k, v in comm.items()}}
-    if ctx.lib is not None and getattr(ctx, "cfg", None) is not None and world == 1:
-        # EP=1: the "dispatch" phase is a local permute; there is no all-to-all to expose
-        for r in res.values():
-            r["exposed_comm_us_per_layer"] = 0.0
-    blk, fs = res["blocking"]["exposed_comm_us_per_layer"], res["farskip"]["exposed_comm_us_per_layer"]
-    return {"layers": L, "modes": "hybrid", "attention": f"GQA {shape.n_heads}/{shape.n_kv_heads}x{shape.head_dim},"
-                                                         f" seq {shape.seq_len}",
-            "blocking": res["blocking"], "farskip": res["farskip"],
-            "speedup_farskip_vs_blocking": res["blocking"]["ms_per_stack"] / res["farskip"]["ms_per_stack"],
-            "exposed_a2a_us_per_layer": {"farskip": fs if world > 1 else None, "blocking": blk if world > 1 else None,
-                                         "farskip_frac_of_blocking": (fs / blk) if (world > 1 and blk > 0) else None,
-                                         "note": None if world > 1 else "EP=1: no all-to-all on one GPU"}}
+            ctx.set_a2a_zero_bytes(zb)
+        elif zb:
+            break
+        for name, modes, sched in schedules:
+            def run():
+                ctx.layer_stack_forward([aw] * L, [wd] * L, T, shape.seq_len, modes, sched, o0, oL,
+                                        stream=stream.cuda_stream)
+            for _ in range(2):
+                run()
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(steps):
+                run()
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            t = a.elapsed_time(b) / steps
+            key = name + ("_zero_bytes" if zb else "")
+            if zb:
+                res[key] = {"ms_per_layer": allreduce_max([t], dev)[0] / L}
+                continue
+            ctx.set_timing(True)
+            exp, comm, ph = 0.0, 0.0, {}
+            for _ in range(steps):
+                run()
+                tl = ctx.timeline()
+                e, c = exposed_from_timeline(tl)
+                exp += e
+                comm += c
+                for p, _, _, du in tl:
+                    ph[p] = ph.get(p, 0.0) + du
+            ctx.set_timing(False)
+            n = steps * L
+            vals = allreduce_max([t, exp / n, comm / n], dev)
+            res[key] = {"ms_per_stack": vals[0], "ms_per_layer": vals[0] / L,
+                        "exposed_comm_us_per_layer": vals[1] * 1e3, "comm_us_per_layer": vals[2] * 1e3,
+                        "phase_ms_per_layer": {k: v / n for k, v in sorted(ph.items())}}
+    if world > 1:
+        ctx.set_a2a_zero_bytes(False)
+    fa, fb = attention_flop(shape, T)
+    fs = res["farskip"]["phase_ms_per_layer"]
+    attn = {"flop_part_a": fa, "flop_part_b": fb,
+            "tflops_part_a": fa / (fs["attn_a"] * 1e-3) / 1e12 if fs.get("attn_a") else None,
+            "tflops_part_b": fb / (fs["attn_b"] * 1e-3) / 1e12 if fs.get("attn_b") else None,
+            "note": "attention filler (QKV / core+o-proj) TFLOP/s inside the FarSkip stack; the core is mma.sync "
+                    "(not the hot path)"}
+    # Eq. 9 (P:199-205): overlappable compute (attention + shared expert) minus the
+    # communication it must hide, per layer, from the serialised (Regular) run's phase times
+    rp = res["regular"]["phase_ms_per_layer"]
+    overlappable = sum(rp.get(k, 0.0) for k in ("attn_a", "attn_b", "shared1", "shared2"))
+    comm = sum(rp.get(k, 0.0) for k in ("dispatch", "combine"))
+    eq9 = {"overlappable_us": overlappable * 1e3, "comm_us": comm * 1e3, "slack_us": (overlappable - comm) * 1e3}
+    out = {"layers": L, "attention": f"GQA {shape.n_heads}/{shape.n_kv_heads}x{shape.head_dim}, seq {shape.seq_len}",
+           **res, "attention_throughput": attn, "eq9": eq9,
+           "speedup_farskip_vs_regular": res["regular"]["ms_per_stack"] / res["farskip"]["ms_per_stack"],
+           "speedup_farskip_vs_regular_plus": res["regular_plus"]["ms_per_stack"] / res["farskip"]["ms_per_stack"]}
+    if world > 1:
+        fs_e, blk_e = res["farskip"]["exposed_comm_us_per_layer"], res["regular"]["exposed_comm_us_per_layer"]
+        zb = {n: (res[n]["ms_per_layer"] - res[n + "_zero_bytes"]["ms_per_layer"]) * 1e3 for n, _, _ in schedules}
+        out["exposed_a2a_us_per_layer"] = {
+            "farskip": fs_e, "blocking": blk_e, "regular_plus": res["regular_plus"]["exposed_comm_us_per_layer"],
+            "blocking_comm_us": res["regular"]["comm_us_per_layer"],
+            "farskip_frac_of_blocking": fs_e / res["regular"]["comm_us_per_layer"]
+            if res["regular"]["comm_us_per_layer"] > 0 else None,
+            "zero_byte_crosscheck_us": zb,
+            "method": "fsc_timeline CUDA-event intervals: dispatch/combine time not covered by any compute phase; "
+                      "cross-check = t_layer - t_layer(zero-byte all-to-all)"}
+    else:
+        out["exposed_a2a_us_per_layer"] = {"farskip": None, "blocking": None, "farskip_frac_of_blocking": None,
+                                           "note": "EP=1: no all-to-all on one GPU"}
+    return out
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -578,6 +662,11 @@ def main():
                     help="N > 1: all-to-all dispatch/combine (training path) or the all-reduce inference variant")
     ap.add_argument("--dispatch-fp8", action="store_true", help="N > 1 all-to-all: FP8 e4m3 dispatch payload")
     ap.add_argument("--cta-group", type=int, default=0, choices=[0, 1, 2], help="GEMM tcgen05 cta_group (0 = auto)")
+    ap.add_argument("--combine", default="stream", choices=["stream", "fused"],
+                    help="N > 1: combine pushed on the comm stream after the down GEMM, or fused into its epilogue")
+    ap.add_argument("--blocking", default="regular+", choices=["regular+", "serial"],
+                    help="N > 1 headline layer: shared expert beside the in-flight combine, or fully serialised")
+    ap.add_argument("--comm-ctas", type=int, default=0, help="CTAs of the dispatch / combine kernels (0 = library default)")
     ap.add_argument("--no-live-timing", action="store_true", help="no CUDA events inside the timed graphs")
     ap.add_argument("--stack-layers", type=int, default=4, help="0 disables the FarSkip-vs-blocking stack timing")
     args = ap.parse_args()

@@ -68,6 +68,21 @@ enum { FSC_BLOCKING = 0, FSC_OVERLAPPED = 1 };
  * computes only its local experts' contributions and the partial outputs are
  * all-reduced (reduce-scatter + all-gather over peer memory, rank-order sums). */
 enum { FSC_EP_ALLTOALL = 0, FSC_EP_ALLREDUCE = 1 };
+/* Combine data path at EP > 1 (PAPER.md:100, P:198 step 7): FSC_COMBINE_STREAM (default)
+ * = the down GEMM stores its rows locally and a push kernel on the communication stream
+ * sends them back to their source ranks, overlapping the shared expert (step 8) and, in
+ * the FarSkip stack, the next layer's attention part (a); FSC_COMBINE_FUSED = the down
+ * GEMM's epilogue stores every row straight into its source rank's buffer (no local
+ * round trip, but the transfer is serialised with the GEMM). Bitwise the same results. */
+enum { FSC_COMBINE_STREAM = 0, FSC_COMBINE_FUSED = 1 };
+/* fsc_moe_forward_blocking at EP > 1: FSC_BLOCKING_REGULAR_PLUS (default) = the
+ * shared expert runs while the combine is in flight ("(c) may be partially overlapped if a
+ * shared expert is present"); FSC_BLOCKING_SERIAL = the combine is waited first (the plain
+ * Eq. 6 serialised run, DESIGN C-amb-16). Bitwise the same results. */
+enum { FSC_BLOCKING_REGULAR_PLUS = 0, FSC_BLOCKING_SERIAL = 1 };
+/* Phases of fsc_set_spin_schedule (the SPEC S:437 duration names). */
+enum { FSC_SPIN_GATE = 0, FSC_SPIN_DISPATCH, FSC_SPIN_QKV, FSC_SPIN_CORE, FSC_SPIN_ROUTED, FSC_SPIN_COMBINE,
+       FSC_SPIN_SHARED, FSC_SPIN_N };
 
 /* MoE layer shape. d % 64 == 0, ffn % 64 == 0, shared_ffn % 64 == 0 (0 = no shared
  * expert; n shared experts = one SwiGLU of concatenated width, C-amb-7),
@@ -107,7 +122,13 @@ typedef struct {
  *   pos int32 [T,k] (row of copy (t,j) in this rank's expert-sorted send buffer),
  *   logits fp32 [T,E] (fp32 router logits before near-tie refinement),
  *   shared_out fp32 [T,d], routed_out fp32 [T,d] (computed separately),
- *   n_refined int32 [1] device counter of tokens re-selected in fp64 (accumulates). */
+ *   n_refined int32 [1] device counter of tokens re-selected in fp64 (accumulates).
+ * EP > 1 all-to-all only (the exchange of P:97-100 as this rank saw it):
+ *   ep_counts int32 [P,E]: row s = copies per global expert sent by rank s (all-gathered),
+ *   recv_counts int32 [E_loc]: rows received per local expert,
+ *   recv_src int32 [P * max_tokens * min(k, E_loc)]: for received row r (expert-major, then
+ *     source rank, then token, C-amb-11) (source rank << 24) | row in the source's
+ *     expert-sorted send order; rows past sum(recv_counts) are unspecified. */
 typedef struct {
   int* topk_idx;
   float* topk_w;
@@ -117,6 +138,9 @@ typedef struct {
   float* shared_out;
   float* routed_out;
   int* n_refined;
+  int* ep_counts;
+  int* recv_counts;
+  int* recv_src;
 } fsc_moe_debug;
 
 /* Caller hook invoked by fsc_moe_forward_farskip while a collective is in flight:
@@ -184,6 +208,29 @@ FSC_API int fsc_set_ep_mode(fsc_ctx* ctx, int mode);
  * oracle's moe_block_ep_fp8. d % 128 == 0. Call before fsc_bootstrap_export. */
 FSC_API int fsc_set_dispatch_fp8(fsc_ctx* ctx, int on);
 
+/* Combine data path (FSC_COMBINE_STREAM default / FSC_COMBINE_FUSED, see above). */
+FSC_API int fsc_set_combine_mode(fsc_ctx* ctx, int mode);
+/* Schedule of fsc_moe_forward_blocking at EP > 1 (FSC_BLOCKING_REGULAR_PLUS default / SERIAL). */
+FSC_API int fsc_set_blocking_mode(fsc_ctx* ctx, int mode);
+/* CTAs of the dispatch and combine kernels (default 64: a fraction of the 148 SMs, so that
+ * the overlapped compute keeps most of them). 1 <= n <= 592. */
+FSC_API int fsc_set_comm_ctas(fsc_ctx* ctx, int n);
+/* Measurement instrument ("zero-byte all-to-all"): on != 0 keeps the counts
+ * exchange, the flags and every kernel launch of the all-to-all but moves no payload rows
+ * (the expert GEMMs run on whatever the receive buffer holds; results are garbage). The
+ * exposed all-to-all time of a schedule is t_layer(real) - t_layer(zero-byte). */
+FSC_API int fsc_set_a2a_zero_bytes(fsc_ctx* ctx, int on);
+/* Test instrument for the stream wiring (the SPEC S:437 golden replay):
+ * with unit_ns != NULL ([FSC_SPIN_N] nanoseconds), every phase of the MoE calls and of
+ * fsc_layer_stack_forward launches ONE single-thread spin kernel of that duration instead
+ * of its real kernels, on the same stream and behind the same events (gate = router +
+ * maps, dispatch, qkv = attention part (a), core = part (b), routed = both expert GEMMs,
+ * combine, shared). Nothing is computed. NULL restores the real kernels. */
+FSC_API int fsc_set_spin_schedule(fsc_ctx* ctx, const long long* unit_ns);
+/* Test instrument: a spin kernel of a pseudo-random duration in [0, max_ns] (xorshift32 from
+ * seed) before every compute and communication stage; the results must not change. 0 = off. */
+FSC_API int fsc_set_delay_fuzz(fsc_ctx* ctx, unsigned seed, long long max_ns);
+
 /* Debug finiteness check (the error class of SPEC S:29): when on, every
  * fsc_moe_forward_blocking, fsc_moe_wait (and so every layer of
  * fsc_layer_stack_forward) counts the non-finite values of its fp32 output on the
@@ -207,6 +254,14 @@ FSC_API int fsc_get_timings(fsc_ctx* ctx, float* ms, int n);
  * 9 = dispatch stall of the compute stream, 10 = combine wait); waits for the
  * events, writes up to cap (phase, ms) pairs, returns the count and clears the log. */
 FSC_API int fsc_timing_log(fsc_ctx* ctx, int* phase, float* ms, int cap);
+/* Timeline of every logged phase instance (same ids, plus 11 = attention part (a): norm +
+ * QKV + RoPE, 12 = attention part (b): core + o-projection, both from
+ * fsc_layer_stack_forward): phase, stream (0 = the caller's compute stream, 1 = the
+ * communication stream, 2 = the auxiliary compute stream), start offset from the first
+ * logged instance and duration, in ms (CUDA events on the phase's stream). Waits for the
+ * events, returns the count and clears the log; FSC_ERR_STATE if instances were dropped
+ * (more than 4096 between two reads, or more than cap). Any output may be NULL. */
+FSC_API int fsc_timeline(fsc_ctx* ctx, int* phase, int* stream, float* t0_ms, float* dur_ms, int cap);
 /* Cumulative number of CUDA kernels launched by libfsc in this process. */
 FSC_API long fsc_launch_count(void);
 
@@ -252,6 +307,43 @@ FSC_API int fsc_moe_forward_farskip(fsc_ctx* ctx, const fsc_moe_weights* w, int 
  * on that stream too (or order the streams with events yourself): the next call
  * reuses the receive / combine buffers that this wait reads (write-after-read). */
 FSC_API int fsc_moe_wait(fsc_ctx* ctx, fsc_handle h, const float* partial_in, float* full_out, void* stream);
+
+/* ---------------------------------------------------------------- backward */
+
+/* Gradients of one MoE sub-block, all fp32, caller-owned device buffers (any NULL except dx
+ * = not wanted; written, not accumulated):
+ *   dx        [T, d]        dL/dx_in (this rank's tokens)
+ *   dgamma    [d]           RMSNorm weight (this rank's tokens)
+ *   dw_router [E, d]        router W_R (this rank's tokens)
+ *   dw1, dw2  [E_loc, c, d], dw3 [E_loc, d, c]   this rank's experts, from every rank's tokens
+ *   dws1, dws2 [c_s, d], dws3 [d, c_s]           shared expert (this rank's tokens)
+ * The data-parallel reduction of the replicated weights' gradients (gamma, W_R, shared) over
+ * the EP ranks is the caller's. */
+typedef struct {
+  float* dx;
+  float* dgamma;
+  float* dw_router;
+  float* dw1;
+  float* dw2;
+  float* dw3;
+  float* dws1;
+  float* dws2;
+  float* dws3;
+} fsc_moe_grads;
+
+/* Backward of out = x_in + shared(xn) + routed(xn) (the sub-block of Eq. 6 / A5; the
+ * far-skip connections are identities, so the FarSkip wiring routes the same gradients,
+ * P:207-211) given grad_out = dL/dout fp32 [T, d]. Recomputes the forward's routing and
+ * expert inputs from x_in (activation recomputation), then, in this stream order:
+ * gradient Dispatch (G rows + gates to the experts' owners) on the communication stream
+ * while the shared expert's backward runs; routed dgrad (dh = G W3, SwiGLU backward on the
+ * recomputed u, v, dX = [dU | dV] [W1 ; W2]); gradient Combine of dX and the gate gradients
+ * on the communication stream while the routed weight gradients run (the explicit order that
+ * replaces the paper's autograd re-prioritisation); then the router and RMSNorm backward per
+ * token. All-to-all EP mode (or EP = 1) only. Allocates its workspace on the first call.
+ * Errors as the forward (FSC_ERR_CONFIG in the all-reduce EP mode). */
+FSC_API int fsc_moe_backward(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in,
+                             const float* grad_out, const fsc_moe_grads* grads, void* stream);
 
 /* ---------------------------------------------------------------- stack */
 
@@ -313,6 +405,27 @@ FSC_API int fsc_op_grouped_gemm_gather(fsc_ctx* ctx, int epi, const void* A, lon
 /* K5: out fp32 [T,d] = resid + sum_j w[t,j] y[pos[t,j]] (resid may be NULL -> 0). */
 FSC_API int fsc_op_unpermute(fsc_ctx* ctx, const void* y, const int* pos, const float* w, const float* resid, float* out,
                      int T, int k, int d, void* stream);
+
+/* K4 backward, dgrad (MN-major B): per group g, out[rows of g] = A[rows of g] B_g with
+ * B_g = rows [g * b_group_rows, +K) of B0 read as [K, N] (row-major, N contiguous); with
+ * kb_split > 0 the K rows are [B0 rows (kb_split * 64) ; B1 rows (K - kb_split * 64)].
+ * epi 0: bf16 out [M, N]; epi 2: fp32 out = resid + A B (resid may be NULL). */
+FSC_API int fsc_op_gemm_dgrad(fsc_ctx* ctx, int epi, const void* A, long a_rows, const void* B0, const void* B1,
+                              long b_group_rows, int G, const int* counts, int m_total, int N, int K, int kb_split,
+                              void* out, const float* resid, void* stream);
+/* K4 backward, SwiGLU backward with recomputation: u = A W1_g^T, v = A W2_g^T (B0 = W1,
+ * B1 = W2 as [G*N, K]); dh bf16 [M, N]; row_gate fp32 [M] or NULL (1): h = u SiLU(v),
+ * du = g dh SiLU(v), dv = g dh u SiLU'(v) -> duv bf16 [M, 2N] = [du | dv], hg bf16 [M, N] = g h,
+ * dg_part fp32 [M, dg_ld] (NULL: skipped) = per-tile partial sums of h * dh (2 per N tile). */
+FSC_API int fsc_op_gemm_swiglu_bwd(fsc_ctx* ctx, const void* A, long a_rows, const void* B0, const void* B1, int G,
+                                   const int* counts, int m_total, int N, int K, const void* dh,
+                                   const float* row_gate, void* duv, void* hg, float* dg_part, int dg_ld,
+                                   void* stream);
+/* K4 backward, wgrad: out[g][i][j] (+)= sum over group g's rows m of A[m, a_col0 + i] B[m, b_col0 + j]
+ * (A [a_rows, lda], B [a_rows, ldb] bf16; out fp32 [G, N1, N2]; N2 % 64 == 0). */
+FSC_API int fsc_op_gemm_wgrad(fsc_ctx* ctx, const int* counts, int G, int m_total, int N1, int N2, const void* A,
+                              long a_rows, long lda, int a_col0, const void* B, long ldb, int b_col0, float* out,
+                              int accumulate, void* stream);
 
 #ifdef __cplusplus
 }

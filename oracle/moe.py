@@ -296,16 +296,19 @@ def shared_expert(xn: np.ndarray, layer: EpLayer) -> np.ndarray:
     return swiglu(xn, layer.ws1, layer.ws2, layer.ws3)
 
 
-def moe_block_ep(x_per_rank: Sequence[np.ndarray], layer: EpLayer, n_ranks: int):
+def moe_block_ep(x_per_rank: Sequence[np.ndarray], layer: EpLayer, n_ranks: int,
+                 routers: Optional[Sequence[RouterOutput]] = None):
     """MoE block forward with EP over n_ranks simulated ranks.
 
     Per rank s: xn = rmsnorm(x_s); router; dispatch; experts; combine.
     Returns [(shared_out_s, routed_out_s, RouterOutput_s)] for every rank s,
-    shared and routed SEPARATELY."""
+    shared and routed SEPARATELY. ``routers[s]`` (optional) fixes rank
+    s's selection (the near-tie adoption rule R-1)."""
     if len(x_per_rank) != n_ranks:
         raise ValueError("one token block per rank")
     xns = [rmsnorm(x, layer.gamma) for x in x_per_rank]
-    routers = [route(xn, layer.w_router, layer.top_k) for xn in xns]
+    if routers is None:
+        routers = [route(xn, layer.w_router, layer.top_k) for xn in xns]
     recv, rc, dst_rank, dst_row, _ = dispatch_sim(xns, [r.idx for r in routers],
                                                    layer.n_experts, n_ranks)
     ys = [experts_on_rank(recv[p], rc[p], layer, p, n_ranks) for p in range(n_ranks)]

@@ -18,6 +18,9 @@ FSC_OK, FSC_ERR_CONFIG, FSC_ERR_SHAPE, FSC_ERR_CUDA, FSC_ERR_COMM, FSC_ERR_NONFI
 FSC_REGULAR, FSC_HYBRID = 0, 1
 FSC_BLOCKING, FSC_OVERLAPPED = 0, 1
 FSC_EP_ALLTOALL, FSC_EP_ALLREDUCE = 0, 1
+FSC_COMBINE_STREAM, FSC_COMBINE_FUSED = 0, 1
+FSC_BLOCKING_REGULAR_PLUS, FSC_BLOCKING_SERIAL = 0, 1
+SPIN_PHASES = ("gate", "dispatch", "qkv", "core", "routed", "combine", "shared")   # FSC_SPIN_* order
 EPI_BF16, EPI_SWIGLU, EPI_RESID_F32 = 0, 1, 2
 
 _STATUS = {FSC_ERR_CONFIG: "CONFIG", FSC_ERR_SHAPE: "SHAPE", FSC_ERR_CUDA: "CUDA", FSC_ERR_COMM: "COMM",
@@ -41,7 +44,12 @@ class MoeWeightsC(ctypes.Structure):
 
 class MoeDebugC(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("topk_idx", "topk_w", "counts", "pos", "logits", "shared_out",
-                                               "routed_out", "n_refined")]
+                                               "routed_out", "n_refined", "ep_counts", "recv_counts", "recv_src")]
+
+
+class MoeGradsC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("dx", "dgamma", "dw_router", "dw1", "dw2", "dw3", "dws1", "dws2",
+                                               "dws3")]
 
 
 class AttnWeightsC(ctypes.Structure):
@@ -74,6 +82,13 @@ _SIGS = {
     "fsc_set_ep_mode": (_I, [_P, _I]),
     "fsc_set_dispatch_fp8": (_I, [_P, _I]),
     "fsc_set_debug_checks": (_I, [_P, _I]),
+    "fsc_set_combine_mode": (_I, [_P, _I]),
+    "fsc_set_blocking_mode": (_I, [_P, _I]),
+    "fsc_set_comm_ctas": (_I, [_P, _I]),
+    "fsc_set_a2a_zero_bytes": (_I, [_P, _I]),
+    "fsc_set_spin_schedule": (_I, [_P, _P]),
+    "fsc_set_delay_fuzz": (_I, [_P, ctypes.c_uint, ctypes.c_longlong]),
+    "fsc_timeline": (_I, [_P, _P, _P, _P, _P, _I]),
     "fsc_set_timing": (_I, [_P, _I]),
     "fsc_set_timing_mask": (_I, [_P, ctypes.c_uint]),
     "fsc_get_timings": (_I, [_P, ctypes.POINTER(ctypes.c_float), _I]),
@@ -94,6 +109,10 @@ _SIGS = {
     "fsc_op_grouped_gemm": (_I, [_P, _I, _P, _L, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "fsc_op_grouped_gemm_gather": (_I, [_P, _I, _P, _L, _P, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "fsc_op_unpermute": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),
+    "fsc_moe_backward": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, ctypes.POINTER(MoeGradsC), _P]),
+    "fsc_op_gemm_dgrad": (_I, [_P, _I, _P, _L, _P, _P, _L, _I, _P, _I, _I, _I, _I, _P, _P, _P]),
+    "fsc_op_gemm_swiglu_bwd": (_I, [_P, _P, _L, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P]),
+    "fsc_op_gemm_wgrad": (_I, [_P, _P, _I, _I, _I, _I, _P, _L, _L, _I, _P, _L, _I, _P, _I, _P]),
 }
 
 _lib = None
@@ -211,7 +230,8 @@ class Context:
         self._ck(self.lib.fsc_bootstrap_import(self.h, buf))
 
     PHASES = ("router", "perm_maps", "dispatch", "gemm1", "gemm2", "combine", "shared1", "shared2", "unpermute",
-              "dispatch_stall", "combine_wait")
+              "dispatch_stall", "combine_wait", "attn_a", "attn_b")
+    STREAMS = ("compute", "comm", "aux")
 
     def set_timing(self, enable: bool):
         self._ck(self.lib.fsc_set_timing(self.h, int(enable)))
@@ -239,6 +259,43 @@ class Context:
         if n < 0:
             self._ck(n)
         return [(self.PHASES[ph[i]], ms[i]) for i in range(n)]
+
+    def timeline(self, cap: int = 4096):
+        """[(phase, stream, t0_ms, dur_ms)] of every logged phase instance (fsc_timeline)."""
+        ph = (ctypes.c_int * cap)()
+        st = (ctypes.c_int * cap)()
+        t0 = (ctypes.c_float * cap)()
+        du = (ctypes.c_float * cap)()
+        n = self.lib.fsc_timeline(self.h, ph, st, t0, du, cap)
+        if n < 0:
+            self._ck(n)
+        return [(self.PHASES[ph[i]], self.STREAMS[st[i]], t0[i], du[i]) for i in range(n)]
+
+    def set_combine_mode(self, mode: int):
+        """FSC_COMBINE_STREAM (comm-stream push after the down GEMM) or FSC_COMBINE_FUSED."""
+        self._ck(self.lib.fsc_set_combine_mode(self.h, mode))
+
+    def set_blocking_mode(self, mode: int):
+        """FSC_BLOCKING_REGULAR_PLUS or FSC_BLOCKING_SERIAL (fsc_moe_forward_blocking at EP > 1)."""
+        self._ck(self.lib.fsc_set_blocking_mode(self.h, mode))
+
+    def set_comm_ctas(self, n: int):
+        self._ck(self.lib.fsc_set_comm_ctas(self.h, n))
+
+    def set_a2a_zero_bytes(self, on: bool):
+        """Measurement instrument: all-to-all without payload rows (flags and counts only)."""
+        self._ck(self.lib.fsc_set_a2a_zero_bytes(self.h, int(on)))
+
+    def set_spin_schedule(self, unit_ns):
+        """{phase: ns} over SPIN_PHASES (spin kernels instead of the real work), or None."""
+        if unit_ns is None:
+            self._ck(self.lib.fsc_set_spin_schedule(self.h, None))
+            return
+        arr = (ctypes.c_longlong * len(SPIN_PHASES))(*[int(unit_ns[p]) for p in SPIN_PHASES])
+        self._ck(self.lib.fsc_set_spin_schedule(self.h, arr))
+
+    def set_delay_fuzz(self, seed: int, max_ns: int):
+        self._ck(self.lib.fsc_set_delay_fuzz(self.h, seed, max_ns))
 
     def launch_count(self) -> int:
         return int(self.lib.fsc_launch_count())
@@ -324,6 +381,33 @@ class Context:
             cc = (ActCacheC * L)(*[ActCacheC(**{k: ptr(v) for k, v in c.items()}) for c in cache])
         self._ck(self.lib.fsc_layer_stack_forward(self.h, aw, mw, L, T, seq_len, md, schedule, ptr(o0), ptr(oL), cc,
                                                   stream if stream is not None else cur_stream()))
+
+    # -- backward
+    def moe_backward(self, w: MoeWeights, x_in, grad_out, grads: dict, stream=None):
+        """grads: {"dx": ..., optional "dgamma", "dw_router", "dw1", "dw2", "dw3", "dws1", "dws2", "dws3"}
+        (fp32 device tensors, written)."""
+        T = x_in.shape[0]
+        g = MoeGradsC(**{k: ptr(v) for k, v in grads.items()})
+        self._ck(self.lib.fsc_moe_backward(self.h, ctypes.byref(w.c), T, ptr(x_in), ptr(grad_out), ctypes.byref(g),
+                                           stream if stream is not None else cur_stream()))
+
+    def op_gemm_dgrad(self, epi, A, B0, B1, b_group_rows, G, counts, m_total, N, K, kb_split, out, resid=None,
+                      stream=None):
+        self._ck(self.lib.fsc_op_gemm_dgrad(self.h, epi, ptr(A), A.shape[0], ptr(B0), ptr(B1), b_group_rows, G,
+                                            ptr(counts), m_total, N, K, kb_split, ptr(out), ptr(resid),
+                                            stream if stream is not None else cur_stream()))
+
+    def op_gemm_swiglu_bwd(self, A, B0, B1, G, counts, m_total, N, K, dh, row_gate, duv, hg, dg_part=None,
+                           dg_ld=0, stream=None):
+        self._ck(self.lib.fsc_op_gemm_swiglu_bwd(self.h, ptr(A), A.shape[0], ptr(B0), ptr(B1), G, ptr(counts),
+                                                 m_total, N, K, ptr(dh), ptr(row_gate), ptr(duv), ptr(hg),
+                                                 ptr(dg_part), dg_ld, stream if stream is not None else cur_stream()))
+
+    def op_gemm_wgrad(self, counts, G, m_total, N1, N2, A, lda, a_col0, B, ldb, b_col0, out, accumulate=False,
+                      stream=None):
+        self._ck(self.lib.fsc_op_gemm_wgrad(self.h, ptr(counts), G, m_total, N1, N2, ptr(A), A.shape[0], lda, a_col0,
+                                            ptr(B), ldb, b_col0, ptr(out), int(accumulate),
+                                            stream if stream is not None else cur_stream()))
 
     # -- op level
     def op_router(self, x, gamma, w_router, k, xn, topk_idx, topk_w, logits=None, n_refined=None, stream=None):

@@ -113,6 +113,21 @@ FSC_DEVINL uint64_t umma_desc_sw128(uint32_t smem_addr) {
   d |= (uint64_t)2 << 61;                              // SWIZZLE_128B   [61,64)
   return d;
 }
+// MN-major operand, 128B swizzle (canonical ((64 elems, n), (8 rows, k)) layout): the
+// tile is a row of TMA boxes {64 MN-elements x 64 K-rows}; K-rows are 128-byte lines,
+// 8-row swizzle atoms are SBO = 1024 B apart along K, consecutive 64-element MN blocks
+// are LBO = lbo_bytes apart (one box). One K=16 MMA step spans two atoms (2048 B).
+FSC_DEVINL uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);        // start address  [0,14)
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;   // LBO: next 64 MN elements
+  d |= (uint64_t)(1024 >> 4) << 32;                    // SBO: next 8 K rows
+  d |= (uint64_t)1 << 46;                              // version = 1
+  d |= (uint64_t)2 << 61;                              // SWIZZLE_128B
+  return d;
+}
+// Instruction-descriptor "major" bits: A MN-major (bit 15), B MN-major (bit 16).
+constexpr uint32_t kIdescAMN = 1u << 15, kIdescBMN = 1u << 16;
 // Instruction descriptor, kind::f16: D=F32, A=B=BF16, both K-major, M x N.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4)                       // c_format F32

@@ -16,8 +16,10 @@ struct fsc_peer_state;  // transport.cu
 
 // phases timed with CUDA events when timing is enabled (fsc_get_timings order)
 enum { PH_ROUTER = 0, PH_PERM, PH_DISPATCH, PH_GEMM1, PH_GEMM2, PH_COMBINE, PH_SHARED1, PH_SHARED2, PH_UNPERMUTE,
-       PH_DISPATCH_STALL, PH_COMBINE_WAIT, PH_N };
-constexpr int kLogEvents = 2048;
+       PH_DISPATCH_STALL, PH_COMBINE_WAIT, PH_ATTN_A, PH_ATTN_B, PH_N };
+constexpr int kLogEvents = 8192;   // 4096 phase instances between two fsc_timeline reads
+// spin-schedule phases (fsc_set_spin_schedule; SPEC S:437 duration names)
+enum { SP_GATE = 0, SP_DISPATCH, SP_QKV, SP_CORE, SP_ROUTED, SP_COMBINE, SP_SHARED, SP_N };
 
 struct fsc_ctx {
   int rank = 0, ep = 1, device = 0;
@@ -31,6 +33,15 @@ struct fsc_ctx {
   int ep_mode = 0;             // FSC_EP_ALLTOALL (dispatch / combine) or FSC_EP_ALLREDUCE (replicated tokens)
   int router_i8 = 0;           // exact int8 tensor-core router (fsc_set_router_int8)
   int gather_a = 0;            // EP = 1: GEMM1 gathers A through src_row (fused permute)
+  int combine_mode = 0;        // FSC_COMBINE_STREAM (comm-stream push after GEMM2) or FSC_COMBINE_FUSED
+  int blocking_mode = 0;       // fsc_moe_forward_blocking: FSC_BLOCKING_REGULAR_PLUS or FSC_BLOCKING_SERIAL
+  int a2a_zero_bytes = 0;      // test instrument: all-to-all flags / counts only, no payload rows
+  int comm_ctas = 64;          // CTAs of the dispatch / combine kernels (a fraction of the SMs)
+  long long spin_ns[SP_N] = {};   // fsc_set_spin_schedule: one spin kernel per phase instead of the real work
+  int spin = 0;
+  unsigned fuzz_seed = 0;      // fsc_set_delay_fuzz: random spin delays before every stage
+  long long fuzz_max_ns = 0;
+  int comb_async = 0;          // the last MoE call's combine runs on the comm stream (ev_comb)
   int sticky = 0;
   int debug_checks = 0;        // fsc_set_debug_checks: finiteness check of every output (syncs)
   int* nf_count = nullptr;     // [1] device counter of non-finite output values
@@ -84,6 +95,7 @@ struct fsc_ctx {
   int io_slot = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_d = nullptr;
   cudaEvent_t ev_t1 = nullptr, ev_t2 = nullptr;   // TP attention all-reduce (stack)
+  cudaEvent_t ev_g2 = nullptr, ev_comb = nullptr; // GEMM2 done (compute) -> combine done (comm)
   int attn_pending = 0;        // 1: attention all-reduce in line, 2: on the comm stream
   float* attn_cache = nullptr;
   int attn_T = 0;
@@ -104,11 +116,29 @@ struct fsc_ctx {
   // timing log: every phase instance since the last reset (bench: per-layer exposure)
   cudaEvent_t log_ev[kLogEvents] = {};
   int log_phase[kLogEvents / 2] = {};
+  int log_stream[kLogEvents / 2] = {};   // 0 = caller's (compute) stream, 1 = comm, 2 = aux
   int log_n = 0;
+  long log_dropped = 0;                  // phase instances not logged (log full): reported as an error
   fsc_handle_s handle{};
+  // backward workspace (moe_bwd.cu), allocated on the first fsc_moe_backward call
+  uint16_t* b_gb = nullptr;     // bf16 [T, d]              G
+  uint16_t* b_duv = nullptr;    // bf16 [rows, 2 max(c, c_s)] [dU | dV]
+  uint16_t* b_hg = nullptr;     // bf16 [rows, max(c, c_s)] g * h
+  float* b_dgpart = nullptr;    // fp32 [rows, b_dg_ld]     gate-gradient partials
+  int b_dg_ld = 0;
+  float* b_dlrow = nullptr;     // fp32 [T * k]             logit gradients per send row
+  float* b_rtok = nullptr;      // fp32 [T]                 RMS factors
+  uint16_t* b_gr = nullptr;     // EP = 1: bf16 [T * k, d]  gradient rows (expert-sorted)
+  float* b_gate = nullptr;      // EP = 1: fp32 [T * k]     their gates
 };
 
 void fsc_set_error(fsc_ctx* c, const char* fmt, ...);
+// phase timing (CUDA events on the phase's stream, logged for fsc_timeline)
+cudaError_t fsc_phase_begin(fsc_ctx* ctx, int i, cudaStream_t st);
+cudaError_t fsc_phase_end(fsc_ctx* ctx, int i, cudaStream_t st);
+// test instruments: spin kernel for spin-schedule phase sp; random delay (delay fuzz)
+cudaError_t fsc_spin(fsc_ctx* ctx, int sp, cudaStream_t st);
+cudaError_t fsc_fuzz(fsc_ctx* ctx, cudaStream_t st);
 // argument checks of one MoE call (weights, T, activation pointers, alignment); no enqueue
 int fsc_validate_moe(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, const void* out);
 // debug finiteness check of an fp32 [n] output (fsc_set_debug_checks): synchronises s
@@ -124,6 +154,13 @@ int fsc_transport_dispatch(fsc_ctx* ctx, int T, cudaStream_t s);
 int fsc_transport_dispatch_wait(fsc_ctx* ctx, cudaStream_t s);
 int fsc_transport_combine(fsc_ctx* ctx, int T, cudaStream_t s);
 int fsc_transport_combine_wait(fsc_ctx* ctx, cudaStream_t s);
+int fsc_transport_combine_push(fsc_ctx* ctx, const uint16_t* y, cudaStream_t s);
+void fsc_transport_debug(fsc_ctx* ctx, const int** cnt, const int** ret);
+void fsc_transport_bwd_ptrs(fsc_ctx* ctx, uint16_t** gr, float** gate, float** dgs);
+int fsc_transport_dispatch_grad(fsc_ctx* ctx, int T, const float* G, cudaStream_t s);
+int fsc_transport_combine_grad(fsc_ctx* ctx, const uint16_t* y, const float* dg_part, int dg_n, int dg_ld,
+                               cudaStream_t s);
+int fsc_transport_combine_grad_wait(fsc_ctx* ctx, cudaStream_t s);
 void fsc_transport_scatter_target(fsc_ctx* ctx, const int** ret, void** peer_out);
 // EP all-reduce channels: 0 = MoE routed sum, 1 = TP attention o-projection (stack)
 float* fsc_transport_ar_partial(fsc_ctx* ctx, int ch = 0);

@@ -56,23 +56,49 @@ static cudaError_t ph_record(cudaEvent_t ev, cudaStream_t st) {
   return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
                                              : cudaEventRecord(ev, st);
 }
-#define PH_REC(ev, st) CK(ph_record(ev, st))
-#define PH_BEGIN_ON(i, st)                                                         \
-  if (ctx->timing && ((ctx->timing_mask >> (i)) & 1u)) {                                                               \
-    PH_REC(ctx->ph_ev[i][0], st);                                                  \
-    if (ctx->log_n < kLogEvents / 2) PH_REC(ctx->log_ev[2 * ctx->log_n], st);      \
+
+static bool ph_on(const fsc_ctx* ctx, int i) { return ctx->timing && ((ctx->timing_mask >> i) & 1u); }
+
+cudaError_t fsc_phase_begin(fsc_ctx* ctx, int i, cudaStream_t st) {
+  if (!ph_on(ctx, i)) return cudaSuccess;
+  cudaError_t e = ph_record(ctx->ph_ev[i][0], st);
+  if (e == cudaSuccess && ctx->log_n < kLogEvents / 2) e = ph_record(ctx->log_ev[2 * ctx->log_n], st);
+  return e;
+}
+
+cudaError_t fsc_phase_end(fsc_ctx* ctx, int i, cudaStream_t st) {
+  if (!ph_on(ctx, i)) return cudaSuccess;
+  cudaError_t e = ph_record(ctx->ph_ev[i][1], st);
+  ctx->ph_used[i] = 1;
+  if (ctx->log_n < kLogEvents / 2) {
+    if (e == cudaSuccess) e = ph_record(ctx->log_ev[2 * ctx->log_n + 1], st);
+    ctx->log_phase[ctx->log_n] = i;
+    ctx->log_stream[ctx->log_n] = st == ctx->comm ? 1 : (st == ctx->aux ? 2 : 0);
+    ++ctx->log_n;
+  } else {
+    ++ctx->log_dropped;
   }
-#define PH_END_ON(i, st)                                                           \
-  if (ctx->timing && ((ctx->timing_mask >> (i)) & 1u)) {                                                               \
-    PH_REC(ctx->ph_ev[i][1], st);                                                  \
-    ctx->ph_used[i] = 1;                                                           \
-    if (ctx->log_n < kLogEvents / 2) {                                             \
-      PH_REC(ctx->log_ev[2 * ctx->log_n + 1], st);                                 \
-      ctx->log_phase[ctx->log_n++] = i;                                            \
-    }                                                                              \
-  }
+  return e;
+}
+#define PH_BEGIN_ON(i, st) CK(fsc_phase_begin(ctx, i, st))
+#define PH_END_ON(i, st) CK(fsc_phase_end(ctx, i, st))
 #define PH_BEGIN(i) PH_BEGIN_ON(i, s)
 #define PH_END(i) PH_END_ON(i, s)
+
+// Test instruments (fsc_set_spin_schedule / fsc_set_delay_fuzz): one spin kernel of the
+// phase's duration instead of its real kernels; a random delay in front of a stage.
+cudaError_t fsc_spin(fsc_ctx* ctx, int sp, cudaStream_t st) { return launch_spin(ctx->spin_ns[sp], st); }
+
+cudaError_t fsc_fuzz(fsc_ctx* ctx, cudaStream_t st) {
+  if (ctx->fuzz_max_ns <= 0) return cudaSuccess;
+  unsigned x = ctx->fuzz_seed ? ctx->fuzz_seed : 0x9E3779B9u;   // xorshift32
+  x ^= x << 13;
+  x ^= x >> 17;
+  x ^= x << 5;
+  ctx->fuzz_seed = x;
+  return launch_spin((long long)(x % 1000u) * ctx->fuzz_max_ns / 1000, st);
+}
+#define FUZZ(st) CK(fsc_fuzz(ctx, st))
 
 constexpr int TB_DEFAULT = 32;   // RouterLaunch::rpb (set by launch_router)
 
@@ -152,6 +178,8 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(cudaEventCreateWithFlags(&ctx->ev_d, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_t1, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_t2, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_g2, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_comb, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
   rc = fsc_transport_init(ctx);
   if (rc) return rc;
@@ -174,7 +202,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->i8_x, ctx->i8_w, ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2], ctx->nf_count};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->i8_x, ctx->i8_w, ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2], ctx->nf_count, ctx->b_gb, ctx->b_duv, ctx->b_hg, ctx->b_dgpart, ctx->b_dlrow, ctx->b_rtok, ctx->b_gr, ctx->b_gate};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -184,6 +212,8 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   if (ctx->ev_d) cudaEventDestroy(ctx->ev_d);
   if (ctx->ev_t1) cudaEventDestroy(ctx->ev_t1);
   if (ctx->ev_t2) cudaEventDestroy(ctx->ev_t2);
+  if (ctx->ev_g2) cudaEventDestroy(ctx->ev_g2);
+  if (ctx->ev_comb) cudaEventDestroy(ctx->ev_comb);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
@@ -241,15 +271,79 @@ extern "C" int fsc_get_timings(fsc_ctx* ctx, float* ms, int n) {
 extern "C" long fsc_launch_count(void) { return fsc::g_launches; }
 
 extern "C" int fsc_timing_log(fsc_ctx* ctx, int* phase, float* ms, int cap) {
+  return fsc_timeline(ctx, phase, nullptr, nullptr, ms, cap);
+}
+
+extern "C" int fsc_timeline(fsc_ctx* ctx, int* phase, int* stream, float* t0_ms, float* dur_ms, int cap) {
   if (!ctx) return FSC_ERR_SHAPE;
+  const long dropped = ctx->log_dropped;
   const int n = ctx->log_n < cap ? ctx->log_n : cap;
+  const long lost = dropped + (ctx->log_n - n);
+  ctx->log_dropped = 0;
+  if (n > 0) CK(cudaEventSynchronize(ctx->log_ev[2 * (n - 1) + 1]));
   for (int i = 0; i < n; ++i) {
     CK(cudaEventSynchronize(ctx->log_ev[2 * i + 1]));
     if (phase) phase[i] = ctx->log_phase[i];
-    if (ms) CK(cudaEventElapsedTime(&ms[i], ctx->log_ev[2 * i], ctx->log_ev[2 * i + 1]));
+    if (stream) stream[i] = ctx->log_stream[i];
+    if (t0_ms) CK(cudaEventElapsedTime(&t0_ms[i], ctx->log_ev[0], ctx->log_ev[2 * i]));
+    if (dur_ms) CK(cudaEventElapsedTime(&dur_ms[i], ctx->log_ev[2 * i], ctx->log_ev[2 * i + 1]));
   }
   ctx->log_n = 0;
+  REQUIRE(lost == 0, FSC_ERR_STATE, "timing log overflow: %ld phase instances were not logged", lost);
   return n;
+}
+
+extern "C" int fsc_set_combine_mode(fsc_ctx* ctx, int mode) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(mode == FSC_COMBINE_STREAM || mode == FSC_COMBINE_FUSED, FSC_ERR_CONFIG, "unknown combine mode %d", mode);
+  REQUIRE(!ctx->pending, FSC_ERR_STATE, "a FarSkip handle is outstanding");
+  ctx->combine_mode = mode;
+  return FSC_OK;
+}
+
+extern "C" int fsc_set_blocking_mode(fsc_ctx* ctx, int mode) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(mode == FSC_BLOCKING_REGULAR_PLUS || mode == FSC_BLOCKING_SERIAL, FSC_ERR_CONFIG,
+          "unknown blocking mode %d", mode);
+  ctx->blocking_mode = mode;
+  return FSC_OK;
+}
+
+extern "C" int fsc_set_a2a_zero_bytes(fsc_ctx* ctx, int on) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(!ctx->pending, FSC_ERR_STATE, "a FarSkip handle is outstanding");
+  ctx->a2a_zero_bytes = on ? 1 : 0;
+  return FSC_OK;
+}
+
+extern "C" int fsc_set_comm_ctas(fsc_ctx* ctx, int n) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(n >= 1 && n <= 4 * kNumSMs, FSC_ERR_CONFIG, "comm ctas %d outside [1,592]", n);
+  ctx->comm_ctas = n;
+  return FSC_OK;
+}
+
+extern "C" int fsc_set_spin_schedule(fsc_ctx* ctx, const long long* unit_ns) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(!ctx->pending, FSC_ERR_STATE, "a FarSkip handle is outstanding");
+  if (!unit_ns) {
+    ctx->spin = 0;
+    return FSC_OK;
+  }
+  for (int i = 0; i < SP_N; ++i) {
+    REQUIRE(unit_ns[i] >= 0 && unit_ns[i] <= 10000000000ll, FSC_ERR_CONFIG, "spin duration %d out of range", i);
+    ctx->spin_ns[i] = unit_ns[i];
+  }
+  ctx->spin = 1;
+  return FSC_OK;
+}
+
+extern "C" int fsc_set_delay_fuzz(fsc_ctx* ctx, unsigned seed, long long max_ns) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(max_ns >= 0 && max_ns <= 1000000000ll, FSC_ERR_CONFIG, "fuzz delay out of range");
+  ctx->fuzz_seed = seed;
+  ctx->fuzz_max_ns = max_ns;
+  return FSC_OK;
 }
 
 extern "C" int fsc_set_debug_checks(fsc_ctx* ctx, int on) {
@@ -368,63 +462,84 @@ static int validate_call(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const fl
 static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* resid, float* out,
                       const fsc_moe_debug* dbg, cudaStream_t s);
 
-// Steps 3-4 of P:198 (gate + dispatch start) and 6 (routed experts). On return
-// the routed expert outputs y are complete in this rank's receive layout and,
-// for EP > 1, already pushed back toward their source ranks (combine started).
-// shared_resid != nullptr (blocking schedule, EP = 1): the shared expert
-// (out = shared_resid + shared) runs on the compute stream right after the router
-// while the permutation maps and the permute run beside it on the aux stream.
+// Steps 3-4 of P:198 (gate + dispatch start), 6 (routed experts) and 7 (combine start).
+// async_dispatch: the counts exchange and dispatch run on the comm stream while the
+// caller's phase-0 callback (attention part (b)) runs on the compute stream (FarSkip).
+// serial: the combine is waited before returning (plain blocking, P:103 bubble (c));
+// otherwise it stays in flight on the comm stream (ctx->comb_async) and fsc_moe_wait /
+// moe_finish waits for it.
+// shared_resid != nullptr (blocking schedule): the shared expert out = shared_resid +
+// shared runs here too - at EP = 1 right after the router, beside the permutation maps
+// and the permute on the aux stream; at EP > 1 after the combine started (Regular+) or,
+// serial, after it landed.
 // fused_out != nullptr (blocking, EP = 1): GEMM2's epilogue also performs the
 // gate-weighted unpermute, fused_out = fused_resid + routed (bitwise the unpermute kernel).
 static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in,
                                  const fsc_moe_debug* dbg, cudaStream_t s, fsc_overlap_cb cb, void* user,
-                                 bool overlap, const float* shared_resid = nullptr, float* shared_out = nullptr,
-                                 float* fused_out = nullptr, const float* fused_resid = nullptr) {
+                                 bool async_dispatch, bool serial, const float* shared_resid = nullptr,
+                                 float* shared_out = nullptr, float* fused_out = nullptr,
+                                 const float* fused_resid = nullptr) {
   const fsc_moe_config& c = ctx->cfg;
   const int d = c.d, E = c.n_experts, k = c.top_k;
-  RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
-                  dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr,
-                  ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, TB_DEFAULT,
-                  ctx->router_i8 ? ctx->i8_x : nullptr, ctx->i8_w,
-                  ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt};
+  const bool spin = ctx->spin != 0;
+  ctx->comb_async = 0;
+  // ---- gate (P:198 step 3): RMSNorm + router + top-k (+ permutation maps below)
+  FUZZ(s);
   PH_BEGIN(PH_ROUTER);
-  CK(launch_router(rl, s));
+  if (spin) {
+    CK(fsc_spin(ctx, SP_GATE, s));
+  } else {
+    RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
+                    dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr,
+                    ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, TB_DEFAULT,
+                    ctx->router_i8 ? ctx->i8_x : nullptr, ctx->i8_w,
+                    ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt};
+    CK(launch_router(rl, s));
+  }
   PH_END(PH_ROUTER);
-  const bool early_shared = shared_out && (ctx->ep == 1 || ctx->ep_mode == FSC_EP_ALLREDUCE);
-  // FarSkip at EP = 1: the local permutation (maps + permute) stands in for the dispatch
-  // and runs on the comm stream, overlapping the caller's attention part (b) (P:198 steps 4-5)
-  const bool ep1_async = ctx->ep == 1 && overlap && !early_shared && !ctx->gather_a;
+  const bool allreduce = ctx->ep > 1 && ctx->ep_mode == FSC_EP_ALLREDUCE;
+  const bool early_shared = shared_out && (ctx->ep == 1 || allreduce) && !spin;
+  // EP = 1 FarSkip: the local permutation (maps + permute) stands in for the dispatch and
+  // runs on the comm stream, overlapping the caller's attention part (b) (P:198 steps 4-5)
+  const bool ep1_async = ctx->ep == 1 && async_dispatch && !early_shared && !ctx->gather_a;
   cudaStream_t ps = early_shared ? ctx->aux : (ep1_async ? ctx->comm : s);   // stream of the permutation work
   if (early_shared || ep1_async) {
     CK(cudaEventRecord(ctx->ev_c, s));
     CK(cudaStreamWaitEvent(ps, ctx->ev_c, 0));
   }
-  PermLaunch pl{ctx->topk_idx, T, k, E, ctx->hist, ctx->base, ctx->counts, ctx->offsets, ctx->pos, ctx->src_row};
-  PH_BEGIN_ON(PH_PERM, ps);
-  CK(launch_perm_maps(pl, ps));
-  PH_END_ON(PH_PERM, ps);
-  // Dispatch: permute into the expert-sorted order and, for EP > 1,
-  // straight into the owning ranks' receive buffers. In the FarSkip schedule the
-  // counts exchange and dispatch run on the comm stream (P:198 step 4) while the
-  // caller's attention part (b) runs on the compute stream (step 5).
+  if (!spin) {
+    PermLaunch pl{ctx->topk_idx, T, k, E, ctx->hist, ctx->base, ctx->counts, ctx->offsets, ctx->pos, ctx->src_row};
+    PH_BEGIN_ON(PH_PERM, ps);
+    CK(launch_perm_maps(pl, ps));
+    PH_END_ON(PH_PERM, ps);
+  }
+  // ---- dispatch (P:97-100, P:198 step 4): permute into the expert-sorted order and,
+  // for EP > 1, straight into the owning ranks' receive buffers
   const int R = T * k;
   const uint16_t* recv = ctx->xs;
   long recv_rows = R;
   const int* recv_counts = ctx->counts;
-  cudaStream_t cs = overlap ? ctx->comm : s;
+  cudaStream_t cs = async_dispatch ? ctx->comm : s;
   const int* a_idx = nullptr;
-  const bool allreduce = ctx->ep > 1 && ctx->ep_mode == FSC_EP_ALLREDUCE;
   const int* row_base = nullptr;
-  int G_loc = ctx->e_loc;
-  if (allreduce) {
+  bool dispatch_on_comm = false;
+  if (spin) {
+    if (cs != s) {
+      CK(cudaEventRecord(ctx->ev_a, s));
+      CK(cudaStreamWaitEvent(cs, ctx->ev_a, 0));
+    }
+    PH_BEGIN_ON(PH_DISPATCH, cs);
+    CK(fsc_spin(ctx, SP_DISPATCH, cs));
+    PH_END_ON(PH_DISPATCH, cs);
+    if (cs != s) CK(cudaEventRecord(ctx->ev_b, cs));
+    dispatch_on_comm = cs != s;
+  } else if (allreduce) {
     // replicated tokens, local experts only. Their rows are the contiguous
     // range [offsets[e0], offsets[e0 + E_loc]) of the global expert-sorted order.
     const int e0 = ctx->rank * ctx->e_loc;
     PH_BEGIN_ON(PH_DISPATCH, ps);
     CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, ps, ctx->offsets + e0, ctx->e_loc));
     PH_END_ON(PH_DISPATCH, ps);
-    recv = ctx->xs;
-    recv_rows = R;
     recv_counts = ctx->counts + e0;
     row_base = ctx->offsets + e0;
     if (early_shared) {
@@ -450,10 +565,14 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     }
   } else if (ctx->ep == 1) {
     // EP = 1: explicit permute into the expert-sorted send buffer (full-bandwidth SM copy)
+    if (ep1_async) FUZZ(ps);
     PH_BEGIN_ON(PH_DISPATCH, ps);
     CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, ps));
     PH_END_ON(PH_DISPATCH, ps);
-    if (ep1_async) CK(cudaEventRecord(ctx->ev_b, ps));
+    if (ep1_async) {
+      CK(cudaEventRecord(ctx->ev_b, ps));
+      dispatch_on_comm = true;
+    }
     if (early_shared) {
       CK(cudaEventRecord(ctx->ev_d, ps));
       int rc = moe_shared(ctx, w, T, shared_resid, shared_out, dbg, s);   // beside the permutation
@@ -461,9 +580,10 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
       CK(cudaStreamWaitEvent(s, ctx->ev_d, 0));
     }
   } else {
-    if (overlap) {
+    if (cs != s) {
       CK(cudaEventRecord(ctx->ev_a, s));
       CK(cudaStreamWaitEvent(cs, ctx->ev_a, 0));
+      FUZZ(cs);
     }
     PH_BEGIN_ON(PH_DISPATCH, cs);
     int rc = fsc_transport_dispatch(ctx, T, cs);
@@ -471,64 +591,86 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     rc = fsc_transport_dispatch_wait(ctx, cs);
     if (rc) return rc;
     PH_END_ON(PH_DISPATCH, cs);
-    if (overlap) CK(cudaEventRecord(ctx->ev_b, cs));
+    if (cs != s) {
+      CK(cudaEventRecord(ctx->ev_b, cs));
+      dispatch_on_comm = true;
+    }
     recv = ctx->xr;
     recv_rows = ctx->recv_rows_cap;
     recv_counts = ctx->recv_counts;
   }
   if (cb) cb(user, 0, s);  // P:198 step 5: attention part (b) while dispatch is in flight
-  if ((ctx->ep > 1 || ep1_async) && overlap) {  // step 6: sync Dispatch (the compute stream stalls only if late)
+  if (dispatch_on_comm) {  // step 6: sync Dispatch (the compute stream stalls only if late)
     PH_BEGIN(PH_DISPATCH_STALL);
     CK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     PH_END(PH_DISPATCH_STALL);
   }
-  if (dbg) {
+  if (dbg && !spin) {
     if (dbg->topk_idx) CK(cudaMemcpyAsync(dbg->topk_idx, ctx->topk_idx, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
     if (dbg->topk_w) CK(cudaMemcpyAsync(dbg->topk_w, ctx->topk_w, sizeof(float) * T * k, cudaMemcpyDeviceToDevice, s));
     if (dbg->counts) CK(cudaMemcpyAsync(dbg->counts, ctx->counts, sizeof(int) * E, cudaMemcpyDeviceToDevice, s));
     if (dbg->pos) CK(cudaMemcpyAsync(dbg->pos, ctx->pos, sizeof(int) * T * k, cudaMemcpyDeviceToDevice, s));
+    if (ctx->ep > 1 && !allreduce) {   // the exchanged counts matrix and the receive map (after the dispatch)
+      const int *cnt = nullptr, *ret = nullptr;
+      fsc_transport_debug(ctx, &cnt, &ret);
+      if (dbg->ep_counts)
+        CK(cudaMemcpyAsync(dbg->ep_counts, cnt, sizeof(int) * ctx->ep * E, cudaMemcpyDeviceToDevice, s));
+      if (dbg->recv_counts)
+        CK(cudaMemcpyAsync(dbg->recv_counts, ctx->recv_counts, sizeof(int) * ctx->e_loc, cudaMemcpyDeviceToDevice, s));
+      if (dbg->recv_src)
+        CK(cudaMemcpyAsync(dbg->recv_src, ret, sizeof(int) * ctx->max_recv, cudaMemcpyDeviceToDevice, s));
+    }
   }
 
-  // Routed experts (P:198 step 6): GEMM1 + SwiGLU, GEMM2 (+ fused Combine for EP > 1).
+  // ---- routed experts (P:198 step 6): GEMM1 + SwiGLU, GEMM2.
   // cta_group auto: M = 256 CTA-pair tiles when the experts get >= 256 rows on average
   // (prefill), single-CTA M = 128 tiles below that (decode: weight streaming, fewer
   // wasted MMA rows; measured 0.88 -> 0.99 of HBM for Scout decode GEMM1).
-  const long avg_rows = (long)T * k * (allreduce ? 1 : ctx->ep) / E;
-  const int routed_cg = ctx->gemm_cg ? ctx->gemm_cg : (avg_rows < 256 ? 1 : 2);
-  // decode (single-CTA tiles, weight streaming): pick the tile width with the smaller
-  // last-wave waste from the expected tile count (MMA width is not the bound there)
-  auto pick_bn = [&](int N, bool swiglu) {
-    if (routed_cg != 1 || ctx->gemm_cg) return 0;
-    const long mt = ctx->e_loc * ((avg_rows + 127) / 128), slots = ctx->gemm_ctas;
-    auto cost = [&](int b) { const long nt = swiglu ? N / (b / 2) : N / b; return ((mt * nt + slots - 1) / slots) * b; };
-    return cost(128) * 100 < cost(256) * 95 ? 128 : 0;
-  };
-  GemmLaunch g1{};
-  g1.A = recv; g1.a_rows = recv_rows; g1.B0 = w->w1; g1.B1 = w->w2; g1.b_rows = (long)ctx->e_loc * c.ffn;
-  g1.b_group_rows = c.ffn; g1.K = d; g1.N = c.ffn; g1.G = ctx->e_loc; g1.counts = recv_counts; g1.m_total = 0;
-  g1.out = ctx->h; g1.ldo = c.ffn; g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas; g1.cta_group = routed_cg;
-  g1.a_idx = a_idx;
-  g1.row_base = row_base;
-  g1.bn = pick_bn(c.ffn, true);
-  (void)G_loc;
-  PH_BEGIN(PH_GEMM1);
-  CK(launch_grouped_gemm(g1, s));
-  PH_END(PH_GEMM1);
-  GemmLaunch g2{};
-  g2.A = ctx->h; g2.a_rows = a_idx ? (long)R : recv_rows; g2.B0 = w->w3; g2.B1 = nullptr; g2.b_rows = (long)ctx->e_loc * d;
-  g2.b_group_rows = d; g2.K = c.ffn; g2.N = d; g2.G = ctx->e_loc; g2.counts = recv_counts; g2.m_total = 0;
-  g2.out = ctx->y; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = routed_cg;
-  g2.row_base = row_base;
-  g2.bn = pick_bn(d, false);
-  if (ctx->ep > 1 && !allreduce) fsc_transport_scatter_target(ctx, &g2.ret, g2.peer_out);  // P:100 Combine, fused
-  if (fused_out && ctx->ep == 1) {   // P:100 "sum the routed experts", fused into the down GEMM
-    g2.comb_out = fused_out; g2.comb_resid = fused_resid; g2.src_row = ctx->src_row; g2.pos = ctx->pos;
-    g2.topk_w = ctx->topk_w; g2.comb_cnt = ctx->comb_cnt; g2.top_k = k;
+  const bool fused_combine = ctx->ep > 1 && !allreduce && ctx->combine_mode == FSC_COMBINE_FUSED &&
+                             !ctx->a2a_zero_bytes;
+  FUZZ(s);
+  if (spin) {
+    PH_BEGIN(PH_GEMM1);
+    CK(fsc_spin(ctx, SP_ROUTED, s));
+    PH_END(PH_GEMM1);
+  } else {
+    const long avg_rows = (long)T * k * (allreduce ? 1 : ctx->ep) / E;
+    const int routed_cg = ctx->gemm_cg ? ctx->gemm_cg : (avg_rows < 256 ? 1 : 2);
+    // decode (single-CTA tiles, weight streaming): pick the tile width with the smaller
+    // last-wave waste from the expected tile count (MMA width is not the bound there)
+    auto pick_bn = [&](int N, bool swiglu) {
+      if (routed_cg != 1 || ctx->gemm_cg) return 0;
+      const long mt = ctx->e_loc * ((avg_rows + 127) / 128), slots = ctx->gemm_ctas;
+      auto cost = [&](int b) { const long nt = swiglu ? N / (b / 2) : N / b; return ((mt * nt + slots - 1) / slots) * b; };
+      return cost(128) * 100 < cost(256) * 95 ? 128 : 0;
+    };
+    GemmLaunch g1{};
+    g1.A = recv; g1.a_rows = recv_rows; g1.B0 = w->w1; g1.B1 = w->w2; g1.b_rows = (long)ctx->e_loc * c.ffn;
+    g1.b_group_rows = c.ffn; g1.K = d; g1.N = c.ffn; g1.G = ctx->e_loc; g1.counts = recv_counts; g1.m_total = 0;
+    g1.out = ctx->h; g1.ldo = c.ffn; g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas; g1.cta_group = routed_cg;
+    g1.a_idx = a_idx;
+    g1.row_base = row_base;
+    g1.bn = pick_bn(c.ffn, true);
+    PH_BEGIN(PH_GEMM1);
+    CK(launch_grouped_gemm(g1, s));
+    PH_END(PH_GEMM1);
+    GemmLaunch g2{};
+    g2.A = ctx->h; g2.a_rows = a_idx ? (long)R : recv_rows; g2.B0 = w->w3; g2.B1 = nullptr; g2.b_rows = (long)ctx->e_loc * d;
+    g2.b_group_rows = d; g2.K = c.ffn; g2.N = d; g2.G = ctx->e_loc; g2.counts = recv_counts; g2.m_total = 0;
+    g2.out = ctx->y; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = routed_cg;
+    g2.row_base = row_base;
+    g2.bn = pick_bn(d, false);
+    if (fused_combine) fsc_transport_scatter_target(ctx, &g2.ret, g2.peer_out);  // P:100 Combine, fused
+    if (fused_out && ctx->ep == 1) {   // P:100 "sum the routed experts", fused into the down GEMM
+      g2.comb_out = fused_out; g2.comb_resid = fused_resid; g2.src_row = ctx->src_row; g2.pos = ctx->pos;
+      g2.topk_w = ctx->topk_w; g2.comb_cnt = ctx->comb_cnt; g2.top_k = k;
+    }
+    PH_BEGIN(PH_GEMM2);
+    CK(launch_grouped_gemm(g2, s));
+    PH_END(PH_GEMM2);
   }
-  PH_BEGIN(PH_GEMM2);
-  CK(launch_grouped_gemm(g2, s));
-  PH_END(PH_GEMM2);
-  if (allreduce) {
+  // ---- combine (P:100, P:198 step 7)
+  if (allreduce && !spin) {
     // local partial of the routed sum (fp32, slot order) into the peer-visible buffer,
     // then the all-reduce on the comm stream (FarSkip) or in line (blocking)
     const int e0 = ctx->rank * ctx->e_loc;
@@ -536,7 +678,7 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     CK(launch_unpermute_local(ctx->y, ctx->pos, ctx->topk_w, ctx->topk_idx, e0, e0 + ctx->e_loc,
                               fsc_transport_ar_partial(ctx), T, k, d, s));
     PH_END(PH_UNPERMUTE);
-    if (overlap) {
+    if (async_dispatch) {
       CK(cudaEventRecord(ctx->ev_a, s));
       CK(cudaStreamWaitEvent(cs, ctx->ev_a, 0));
     }
@@ -544,12 +686,43 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     int rc = fsc_transport_ar_start(ctx, T, cs);
     if (rc) return rc;
     PH_END_ON(PH_COMBINE, cs);
-    if (overlap) CK(cudaEventRecord(ctx->ev_b, cs));
-  } else if (ctx->ep > 1) {
+    if (async_dispatch) CK(cudaEventRecord(ctx->ev_b, cs));
+  } else if (fused_combine && !spin) {
     PH_BEGIN(PH_COMBINE);
-    int rc = fsc_transport_combine(ctx, T, s);  // P:198 step 7: Combine completes asynchronously
+    int rc = fsc_transport_combine(ctx, T, s);  // rows already stored by GEMM2: raise the flags
     if (rc) return rc;
     PH_END(PH_COMBINE);
+    if (serial) {
+      PH_BEGIN(PH_COMBINE_WAIT);
+      rc = fsc_transport_combine_wait(ctx, s);
+      if (rc) return rc;
+      PH_END(PH_COMBINE_WAIT);
+    }
+  } else if (ctx->ep > 1 || spin) {
+    // decoupled combine on the comm stream: overlaps the shared expert (step 8) and,
+    // in the FarSkip stack, the next layer's attention part (a)
+    CK(cudaEventRecord(ctx->ev_g2, s));
+    CK(cudaStreamWaitEvent(ctx->comm, ctx->ev_g2, 0));
+    FUZZ(ctx->comm);
+    PH_BEGIN_ON(PH_COMBINE, ctx->comm);
+    if (spin) {
+      CK(fsc_spin(ctx, SP_COMBINE, ctx->comm));
+    } else {
+      int rc = fsc_transport_combine_push(ctx, ctx->y, ctx->comm);
+      if (rc) return rc;
+    }
+    PH_END_ON(PH_COMBINE, ctx->comm);
+    CK(cudaEventRecord(ctx->ev_comb, ctx->comm));
+    ctx->comb_async = 1;
+    if (serial) {   // plain blocking: the compute stream waits for the combine (P:103 bubble (c))
+      PH_BEGIN(PH_COMBINE_WAIT);
+      CK(cudaStreamWaitEvent(s, ctx->ev_comb, 0));
+      if (ctx->ep > 1 && !spin) {
+        int rc = fsc_transport_combine_wait(ctx, s);
+        if (rc) return rc;
+      }
+      PH_END(PH_COMBINE_WAIT);
+    }
   }
   if (shared_out && !early_shared) {
     int rc = moe_shared(ctx, w, T, shared_resid, shared_out, dbg, s);
@@ -563,6 +736,13 @@ static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float
                       const fsc_moe_debug* dbg, cudaStream_t s) {
   const fsc_moe_config& c = ctx->cfg;
   const int d = c.d;
+  FUZZ(s);
+  if (ctx->spin) {
+    PH_BEGIN(PH_SHARED1);
+    CK(fsc_spin(ctx, SP_SHARED, s));
+    PH_END(PH_SHARED1);
+    return FSC_OK;
+  }
   if (c.shared_ffn == 0) {
     if (dbg && dbg->shared_out) CK(cudaMemsetAsync(dbg->shared_out, 0, sizeof(float) * T * (long)d, s));
     if (resid != out) {   // (never on the blocking / FarSkip paths: they pass resid == out or skip the call)
@@ -610,13 +790,18 @@ static int moe_finish(fsc_ctx* ctx, int T, const float* resid, float* out, const
     }
     return FSC_OK;
   }
-  if (ctx->ep > 1) {
+  if (ctx->ep > 1 || ctx->comb_async) {
     PH_BEGIN(PH_COMBINE_WAIT);
-    int rc = fsc_transport_combine_wait(ctx, s);
-    if (rc) return rc;
+    if (ctx->comb_async) CK(cudaStreamWaitEvent(s, ctx->ev_comb, 0));   // my own push is done (buffer reuse)
+    if (ctx->ep > 1 && !ctx->spin) {
+      int rc = fsc_transport_combine_wait(ctx, s);                        // every source's rows landed
+      if (rc) return rc;
+    }
     PH_END(PH_COMBINE_WAIT);
+    ctx->comb_async = 0;
     ysrc = ctx->ys;
   }
+  if (ctx->spin) return FSC_OK;
   if (!fused) {   // (fused: done by GEMM2's epilogue)
     PH_BEGIN(PH_UNPERMUTE);
     CK(launch_unpermute(ysrc, ctx->pos, ctx->topk_w, resid, out, T, c.top_k, c.d, s));
@@ -653,16 +838,19 @@ static int moe_blocking_impl(fsc_ctx* ctx, const fsc_moe_weights* w, int T, cons
   // fused unpermute: auto (-1) = top-1 routing only (measured: at k = 6 / 8 the per-tile
   // counter + cooperative finish costs the down GEMM more than the separate kernel)
   const int fu = ctx->fuse_unpermute < 0 ? (ctx->cfg.top_k == 1) : ctx->fuse_unpermute;
-  const bool fuse = ctx->ep == 1 && fu && ctx->cfg.top_k <= 8;   // (the epilogue holds <= 8 slots)
+  const bool fuse = ctx->ep == 1 && fu && ctx->cfg.top_k <= 8 && !ctx->spin;   // (the epilogue holds <= 8 slots)
+  // FSC_BLOCKING_SERIAL: the combine is waited before the shared expert (P:103 bubbles
+  // (b) and (c)); FSC_BLOCKING_REGULAR_PLUS: the shared expert runs while it is in flight
+  const bool serial = ctx->blocking_mode == FSC_BLOCKING_SERIAL;
   if (ctx->cfg.shared_ffn == 0) {   // no shared expert: out = x_in + routed, straight from x_in
-    rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false, nullptr, nullptr,
+    rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false, serial, nullptr, nullptr,
                                fuse ? out : nullptr, x_in);
     if (rc) return rc;
     rc = moe_shared(ctx, w, T, x_in, const_cast<float*>(x_in), dbg, s);   // debug shared_out = 0 only
     if (rc) return rc;
     return moe_finish(ctx, T, x_in, out, dbg, s, fuse);
   }
-  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false, x_in, ctx->tmp,
+  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, nullptr, nullptr, false, serial, x_in, ctx->tmp,
                              fuse ? out : nullptr, ctx->tmp);
   if (rc) return rc;
   return moe_finish(ctx, T, ctx->tmp, out, dbg, s, fuse);
@@ -746,7 +934,10 @@ extern "C" int fsc_moe_forward_farskip(fsc_ctx* ctx, const fsc_moe_weights* w, i
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
-  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, cb, user, !ctx->no_overlap);
+  // no_overlap (set by the stack): 1 = BLOCKING schedule (dispatch in line, combine waited
+  // before the shared expert); 2 = Regular layer of an OVERLAPPED stack (dispatch in line,
+  // shared expert beside the in-flight combine: Regular+); 0 = FarSkip
+  rc = moe_route_and_experts(ctx, w, T, x_in, dbg, s, cb, user, ctx->no_overlap == 0, ctx->no_overlap == 1);
   if (rc) return rc;
   if (cb) cb(user, 1, s);  // combine in flight
   // P:198 step 8 and C-amb-12: attn-in_{k+1} = (mlp-in_k + attn-out_k) + shared-out_k

@@ -226,7 +226,7 @@ FSC_DEVINL void fused_unpermute(const GemmParams& p, long tok, int c0, int lane)
 // leader (cta_group::2); each CTA stages its 128 rows of A and half of the B
 // columns, so per-SM smem traffic per MAC drops by a third and the pipeline is
 // 1.5x deeper at the same shared-memory footprint.
-template <int BN, int EPI, int CG>
+template <int BN, int EPI, int CG, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                         const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmA32,
@@ -304,7 +304,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // segments (4 lanes per row) instead of 32 rows x 16 B per store instruction. A/B in
   // one run: down GEMM 200.7 -> 194.6 us (DS, K = 1408), 357 -> 307 us (Qwen3, K = 768)
   const bool stage_rows = p.stage_rows != 0;
-  const int n_tiles = (EPI == EPI_SWIGLU) ? p.N / C::HALF : p.N / BN;
+  constexpr bool SWI = EPI == EPI_SWIGLU || EPI == EPI_SWIGLU_BWD;   // [U | G] accumulator halves
+  const int n_tiles = SWI ? p.N / C::HALF : p.N / BN;
   const int total = s_tile_off[G] * n_tiles;
   const int kblocks = p.K / BK;
   const int t_first = blockIdx.x / CG, t_step = gridDim.x / CG;
@@ -383,14 +384,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap* mb0 = &tmB0;
         const CUtensorMap* mb1 = &tmB0;
         if (CG == 2) {
-          if (EPI == EPI_SWIGLU) {           // CTA0: U columns from W1, CTA1: G columns from W2
+          if (SWI) {                         // CTA0: U columns from W1, CTA1: G columns from W2
             brow0 = ti.g * p.b_group_rows + ti.nb * C::HALF;
             mb0 = rank ? &tmB1 : &tmB0;
           } else {
             brow0 = ti.g * p.b_group_rows + ti.nb * BN + (int)rank * C::HALF;
           }
         } else {
-          if (EPI == EPI_SWIGLU) {
+          if (SWI) {
             brow0 = ti.g * p.b_group_rows + ti.nb * C::HALF;
             brow1 = brow0;
             mb1 = &tmB1;
@@ -410,7 +411,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* b = sB + stage * C::B_BYTES;
-          if (CG == 2) {
+          if (BMN) {
+            // MN-major B: this CTA's B_ROWS output columns x BK k-rows as boxes of
+            // {64 columns, 64 k-rows} (128-byte k-rows, 8 KB per box)
+            const bool hi = p.kb_split > 0 && kb >= p.kb_split;
+            const CUtensorMap* mk = hi ? &tmB1 : &tmB0;
+            const int krow = ti.g * p.b_group_rows + (hi ? kb - p.kb_split : kb) * BK;
+            const int ncol = ti.nb * BN + (CG == 2 ? (int)rank * C::HALF : 0);
+            if (CG == 2) {
+              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::B_BYTES + a_bytes);
+              if (mybox) tma_load_2d_2sm(sA + stage * C::A_BYTES, ma, &full[stage], kb * BK, arow, kEvictNormal);
+#pragma unroll
+              for (int i = 0; i < C::B_ROWS / 64; ++i)
+                tma_load_2d_2sm(b + i * 64 * BK * 2, mk, &full[stage], ncol + 64 * i, krow, kEvictLast);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], C::B_BYTES + a_bytes);
+              if (mybox) tma_load_2d(sA + stage * C::A_BYTES, ma, &full[stage], kb * BK, arow, kEvictNormal);
+#pragma unroll
+              for (int i = 0; i < C::B_ROWS / 64; ++i)
+                tma_load_2d(b + i * 64 * BK * 2, mk, &full[stage], ncol + 64 * i, krow, kEvictLast);
+            }
+          } else if (CG == 2) {
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::B_BYTES + a_bytes);
             if (mybox) tma_load_2d_2sm(sA + stage * C::A_BYTES, ma, &full[stage], kb * BK, arow, kEvictNormal);
             tma_load_2d_2sm(b, mb0, &full[stage], kb * BK, brow0, kEvictLast);
@@ -427,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader CTA only)
     if (leader && elect_one()) {
-      const uint32_t idesc = idesc_bf16_f32(C::TILE_M, BN);
+      const uint32_t idesc = idesc_bf16_f32(C::TILE_M, BN) | (BMN ? kIdescBMN : 0u);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -444,12 +465,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t bdesc = BMN ? umma_desc_sw128_mn(b_addr + k * 2048, 64 * BK * 2)
+                                       : umma_desc_sw128(b_addr + k * 32);
             if (CG == 2)
-              umma_bf16_ss_2sm(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
-                               (kb | k) != 0);
+              umma_bf16_ss_2sm(d_tmem, umma_desc_sw128(a_addr + k * 32), bdesc, idesc, (kb | k) != 0);
             else
-              umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
-                           (kb | k) != 0);
+              umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), bdesc, idesc, (kb | k) != 0);
           }
           if (CG == 2) umma_commit_2sm(&empty[stage]);
           else umma_commit(&empty[stage]);
@@ -503,6 +524,57 @@ __global__ void __launch_bounds__(kThreads, 1)
               st_global_v4(out + c + 8 * i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
           }
         }
+      } else if (EPI == EPI_SWIGLU_BWD) {
+        // backward of h = u SiLU(v) with the recomputed u, v (see GemmParams)
+        const long col0 = (long)ti.nb * C::HALF;
+        __nv_bfloat16* o_du = reinterpret_cast<__nv_bfloat16*>(p.out) + grow * p.ldo + col0;
+        __nv_bfloat16* o_dv = o_du + p.N;
+        __nv_bfloat16* o_h = reinterpret_cast<__nv_bfloat16*>(p.out2) + grow * (long)p.N + col0;
+        const uint16_t* i_dh = p.dh + grow * (long)p.N + col0;
+        const float gr = (valid && p.row_gate) ? __ldg(p.row_gate + grow) : 1.f;
+        float dgp = 0.f;
+#pragma unroll 1
+        for (int c = half * (C::HALF / 2); c < (half + 1) * (C::HALF / 2); c += 32) {
+          uint32_t u[32], gv[32];
+          tmem_ld32(tb + c, u);
+          tmem_ld32(tb + C::HALF + c, gv);
+          uint4 dq[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dq[i] = valid ? __ldg(reinterpret_cast<const uint4*>(i_dh + c) + i) : make_uint4(0u, 0u, 0u, 0u);
+          tmem_ld_wait();
+          const uint32_t* dw = reinterpret_cast<const uint32_t*>(dq);
+          uint32_t pu[16], pv[16], ph[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float hh[2], du[2], dv[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const float uu = __uint_as_float(u[2 * i + e]), vv = __uint_as_float(gv[2 * i + e]);
+              const float dhu = e ? bf16hi(dw[i]) : bf16lo(dw[i]);
+              const float sg = __fdividef(1.0f, 1.0f + __expf(-vv));     // logistic(v)
+              const float sv = vv * sg;                                   // SiLU(v)
+              const float dsv = sg * (1.0f + vv * (1.0f - sg));           // SiLU'(v)
+              hh[e] = uu * sv;
+              const float dh = gr * dhu;
+              du[e] = dh * sv;
+              dv[e] = dh * uu * dsv;
+              dgp = fmaf(hh[e], dhu, dgp);
+            }
+            pu[i] = pack_bf16x2(du[0], du[1]);
+            pv[i] = pack_bf16x2(dv[0], dv[1]);
+            ph[i] = pack_bf16x2(gr * hh[0], gr * hh[1]);
+          }
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              st_global_v4(o_du + c + 8 * i, make_uint4(pu[4 * i], pu[4 * i + 1], pu[4 * i + 2], pu[4 * i + 3]));
+              st_global_v4(o_dv + c + 8 * i, make_uint4(pv[4 * i], pv[4 * i + 1], pv[4 * i + 2], pv[4 * i + 3]));
+              st_global_v4(o_h + c + 8 * i, make_uint4(ph[4 * i], ph[4 * i + 1], ph[4 * i + 2], ph[4 * i + 3]));
+            }
+          }
+        }
+        if (p.dg_part && valid) p.dg_part[grow * p.dg_ld + ti.nb * 2 + half] = dgp;
       } else if (EPI == EPI_BF16) {
         __nv_bfloat16* out;
         if (p.ret) {     // fused combine: write the row straight into its source rank's buffer
@@ -610,12 +682,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 2-D bf16 row-major [rows, cols] map with a {64 cols x box_rows} box, 128B swizzle.
-static bool make_map(CUtensorMap* m, const void* base, long rows, long cols, int box_rows) {
+// 2-D bf16 row-major [rows, cols] map (row stride ld elements, default cols) with a
+// {64 cols x box_rows} box, 128B swizzle.
+static bool make_map(CUtensorMap* m, const void* base, long rows, long cols, int box_rows, long ld = 0) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld ? ld : cols) * 2};
   cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
@@ -624,17 +697,23 @@ static bool make_map(CUtensorMap* m, const void* base, long rows, long cols, int
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int EPI, int CG>
+template <int BN, int EPI, int CG, bool BMN = false>
 static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   using C = Cfg<BN, CG, EPI>;
   CUtensorMap ma, mb0, mb1, ma32, ma64;
   long a_rows = L.a_rows > 0 ? L.a_rows : 1;
-  if (!make_map(&ma, L.A, a_rows, L.K, L.a_idx ? 1 : BM)) return cudaErrorInvalidValue;   // gather4: {64, 1} box
-  if (!make_map(&ma32, L.A, a_rows, L.K, 32)) return cudaErrorInvalidValue;               // ragged group ends
-  if (!make_map(&ma64, L.A, a_rows, L.K, 64)) return cudaErrorInvalidValue;
-  if (!make_map(&mb0, L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
-  if (!make_map(&mb1, L.B1 ? L.B1 : L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
-  auto kern = grouped_gemm_kernel<BN, EPI, CG>;
+  const long lda = L.lda ? L.lda : L.K;
+  if (!make_map(&ma, L.A, a_rows, L.K, L.a_idx ? 1 : BM, lda)) return cudaErrorInvalidValue;   // gather4: {64, 1} box
+  if (!make_map(&ma32, L.A, a_rows, L.K, 32, lda)) return cudaErrorInvalidValue;               // ragged group ends
+  if (!make_map(&ma64, L.A, a_rows, L.K, 64, lda)) return cudaErrorInvalidValue;
+  if (BMN) {   // B = [K rows, N cols] per group: boxes of {64 columns, 64 k-rows}
+    if (!make_map(&mb0, L.B0, L.b_rows, L.N, 64)) return cudaErrorInvalidValue;
+    if (!make_map(&mb1, L.B1 ? L.B1 : L.B0, L.b_rows, L.N, 64)) return cudaErrorInvalidValue;
+  } else {
+    if (!make_map(&mb0, L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
+    if (!make_map(&mb1, L.B1 ? L.B1 : L.B0, L.b_rows, L.K, C::HALF)) return cudaErrorInvalidValue;
+  }
+  auto kern = grouped_gemm_kernel<BN, EPI, CG, BMN>;
   static std::atomic<unsigned long long> attr_set{0};
   if (cudaError_t e = ensure_smem_attr(kern, C::SMEM, attr_set)) return e;
   GemmParams p;
@@ -660,6 +739,12 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   p.comb_cnt = L.comb_cnt;
   p.top_k = L.top_k;
   p.n_cb = L.N / (BN / 2);
+  p.kb_split = L.kb_split;
+  p.dh = L.dh;
+  p.row_gate = L.row_gate;
+  p.out2 = L.out2;
+  p.dg_part = L.dg_part;
+  p.dg_ld = L.dg_ld;
   // FSC_GEMM_STAGE_ROWS = 0 / 1 overrides the K-based choice (A/B measurements)
   static const int stage_env = getenv("FSC_GEMM_STAGE_ROWS") ? atoi(getenv("FSC_GEMM_STAGE_ROWS")) : -1;
   p.stage_rows = stage_env >= 0 ? stage_env : (L.epi == EPI_BF16 ? 1 : 0);
@@ -683,7 +768,7 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
 }
 
 int gemm_pick_bn(int epi, int N) {
-  if (epi == EPI_SWIGLU) return (N % 128 == 0) ? 256 : (N % 64 == 0 ? 128 : 0);
+  if (epi == EPI_SWIGLU || epi == EPI_SWIGLU_BWD) return (N % 128 == 0) ? 256 : (N % 64 == 0 ? 128 : 0);
   return (N % 256 == 0) ? 256 : (N % 128 == 0 ? 128 : (N % 64 == 0 ? 64 : 0));
 }
 
@@ -693,13 +778,28 @@ cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s) {
   if (!bn) return cudaErrorInvalidValue;
   if (L.bn == 128 && bn == 256 && (L.epi == EPI_SWIGLU ? L.N % 64 == 0 : L.N % 128 == 0)) bn = 128;
   if (L.a_rows == 0) return cudaSuccess;
-#define FSC_GEMM_CASE(BNV, EV)                                  \
-  if (bn == BNV && L.epi == EV) {                               \
-    if (L.cta_group == 1) return launch_t<BNV, EV, 1>(L, s);    \
-    return launch_t<BNV, EV, 2>(L, s);                          \
+  if (L.b_mn && L.epi != EPI_BF16 && L.epi != EPI_RESID_F32) return cudaErrorInvalidValue;
+  // MN-major B is loaded as 64-column boxes: a CTA of a pair holds BN / 2 columns, so BN = 64
+  // runs single-CTA tiles
+  const int cgsel = (L.b_mn && bn == 64) ? 1 : L.cta_group;
+#define FSC_GEMM_CASE(BNV, EV)                                          \
+  if (bn == BNV && L.epi == EV) {                                       \
+    if (L.b_mn) {                                                       \
+      if (cgsel == 1) return launch_t<BNV, EV, 1, true>(L, s);          \
+      return launch_t<BNV, EV, 2, true>(L, s);                          \
+    }                                                                   \
+    if (cgsel == 1) return launch_t<BNV, EV, 1>(L, s);                  \
+    return launch_t<BNV, EV, 2>(L, s);                                  \
   }
-  FSC_GEMM_CASE(256, EPI_SWIGLU)
-  FSC_GEMM_CASE(128, EPI_SWIGLU)
+#define FSC_GEMM_CASE_K(BNV, EV)                                        \
+  if (bn == BNV && L.epi == EV) {                                       \
+    if (L.cta_group == 1) return launch_t<BNV, EV, 1>(L, s);            \
+    return launch_t<BNV, EV, 2>(L, s);                                  \
+  }
+  FSC_GEMM_CASE_K(256, EPI_SWIGLU)
+  FSC_GEMM_CASE_K(128, EPI_SWIGLU)
+  FSC_GEMM_CASE_K(256, EPI_SWIGLU_BWD)
+  FSC_GEMM_CASE_K(128, EPI_SWIGLU_BWD)
   FSC_GEMM_CASE(256, EPI_BF16)
   FSC_GEMM_CASE(128, EPI_BF16)
   FSC_GEMM_CASE(64, EPI_BF16)
@@ -707,6 +807,7 @@ cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s) {
   FSC_GEMM_CASE(128, EPI_RESID_F32)
   FSC_GEMM_CASE(64, EPI_RESID_F32)
 #undef FSC_GEMM_CASE
+#undef FSC_GEMM_CASE_K
   return cudaErrorInvalidValue;
 }
 

@@ -8,7 +8,7 @@ namespace fsc {
 // number of kernels this process has launched through libfsc (evidence for bench's gpu_launches)
 extern long g_launches;
 
-enum { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_RESID_F32 = 2 };
+enum { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_RESID_F32 = 2, EPI_SWIGLU_BWD = 3 };
 
 struct GemmParams {
   const int* counts;  // [G] rows per group (device) or nullptr -> one group of m_total rows
@@ -43,11 +43,25 @@ struct GemmParams {
   int* comb_cnt;               // [T, n_cb] zero between calls (the last arrival resets)
   int top_k, n_cb;
   int stage_rows;              // bf16 epilogue: 1 = staged row-contiguous stores, 0 = direct
+  // MN-major B (dgrad GEMMs, template BMN): B is [K rows, N cols] per group, group g's K rows
+  // start at g * b_group_rows; kb_split > 0: k-blocks >= kb_split read tmB1 (rows restart at
+  // 0), i.e. the K dimension is [B0 rows ; B1 rows] (dX = [dU | dV] [W1 ; W2])
+  int kb_split;
+  // EPI_SWIGLU_BWD (recomputed u = A W1^T, v = A W2^T; N = c): with dh_u = dh [M, N] bf16 and
+  // the row gate g (row_gate, nullptr = 1): h = u SiLU(v), dh = g dh_u, du = dh SiLU(v),
+  // dv = dh u SiLU'(v); out (ldo = 2N) = [du | dv] bf16, out2 [M, N] = g h bf16,
+  // dg_part[row * dg_ld + tile * 2 + half] = partial sum_cols h dh_u (fp32, per warp half)
+  const uint16_t* dh;
+  const float* row_gate;
+  void* out2;
+  float* dg_part;
+  int dg_ld;
 };
 
 struct GemmLaunch {
-  const void* A;      // bf16 [a_rows, K]
+  const void* A;      // bf16 [a_rows, K] (row stride lda, 0 = K)
   long a_rows;
+  long lda = 0;
   const void* B0;     // bf16 [b_rows, K]  (W1 for SwiGLU, else the only B)
   const void* B1;     // bf16 [b_rows, K]  (W2 for SwiGLU) or nullptr
   long b_rows;
@@ -74,9 +88,35 @@ struct GemmLaunch {
   const float* topk_w = nullptr;
   int* comb_cnt = nullptr;
   int top_k = 0;
+  bool b_mn = false;                  // B MN-major [K rows, N cols] per group (dgrad)
+  int kb_split = 0;                   // see GemmParams
+  const uint16_t* dh = nullptr;       // EPI_SWIGLU_BWD inputs / outputs (see GemmParams)
+  const float* row_gate = nullptr;
+  void* out2 = nullptr;
+  float* dg_part = nullptr;
+  int dg_ld = 0;
 };
 
 cudaError_t launch_grouped_gemm(const GemmLaunch& L, cudaStream_t s);
+
+// K4 backward, weight gradients (gemm_wgrad.cu): per group g (rows [row_off[g], +M_g) of
+// A and B, M_g from counts or m_total, offset by *row_base):
+//   out[g][i][j] (+)= sum_m A[m, a_col0 + i] * B[m, b_col0 + j],  i < N1, j < N2  (fp32)
+struct WgradParams {
+  const int* counts;   // [G] device, or nullptr -> one group of m_total rows
+  int G, m_total;
+  const int* row_base; // device int or nullptr
+  int N1, N2;          // N2 % 64 == 0
+  const uint16_t* A;   // bf16 row-major, row stride lda
+  long lda;
+  int a_col0;
+  const uint16_t* B;
+  long ldb;
+  int b_col0;
+  float* out;          // fp32 [G, N1, N2]
+  int accumulate;      // 1: out += (gradient accumulation)
+};
+cudaError_t launch_wgrad_gemm(const WgradParams& p, long a_rows, long b_rows, int ctas, cudaStream_t s);
 int gemm_pick_bn(int epi, int N);
 
 // K1: RMSNorm + fp32 router logits + top-k + renormalised gates (+ fp64 near-tie refinement)
@@ -149,6 +189,8 @@ cudaError_t launch_flash_attn(const uint16_t* qkv, uint16_t* out, int T, int Hq,
 
 // elementwise helpers
 cudaError_t launch_copy_f32(const float* src, float* dst, long n, cudaStream_t s);
+// test instrument: one thread spinning for ns nanoseconds of %globaltimer (ns <= 0: no launch)
+cudaError_t launch_spin(long long ns, cudaStream_t s);
 // debug: *bad += number of non-finite values of x [n] (n % 4 == 0)
 cudaError_t launch_count_nonfinite(const float* x, long n, int* bad, cudaStream_t s);
 

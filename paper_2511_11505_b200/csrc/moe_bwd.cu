@@ -1,0 +1,473 @@
+// fsc_moe_backward: gradients of one MoE sub-block (the backward of
+// PAPER.md:73-76 and P:92-103, overlapped as P:207-211 describes) on sm_100a.
+//
+// Forward being differentiated (oracle/moe_backward.py; readings C-amb-2,4,5,7):
+//   r_t = (mean x_t^2 + eps)^-1/2, xn = gamma x r; l = xn W_R^T; S_t = top-k, g = softmax_S(l);
+//   y_e(a) = (a W1_e^T * SiLU(a W2_e^T)) W3_e^T; out = x + shared(xn) + sum_j g_tj y_{e_j}(xn_t)
+//
+// Schedule on this rank (compute stream s, high-priority comm stream):
+//   s    : router + permutation maps (recomputed: the selection is piecewise constant), G -> bf16
+//   comm : Dispatch of the xn rows (recompute) and of the gradient rows G[t] + gates g_tj to the
+//          experts' owners (the gradient of the Combine)
+//   s    : shared-expert backward (dgrad + wgrad) while those fly
+//   s    : routed dgrad: dh_u = G_r W3 (MN-major B), SwiGLU backward on the recomputed
+//          u, v (fused epilogue: du, dv, g h, dg partials), dX = [dU | dV] [W1 ; W2]
+//   comm : dX rows + gate gradients back to their sources (the gradient of the Dispatch)
+//   s    : routed wgrads dW3 = G_r^T (g h), dW1 = dU^T X, dW2 = dV^T X while that flies -
+//          the explicit stream order that replaces the paper's autograd sequence-number hijack
+//   s    : per token: router backward (softmax over the selected logits), sum of the dX
+//          copies, RMSNorm backward; dgamma column sums; dW_R per expert.
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "ctx.h"
+#include "kernels.h"
+
+using namespace fsc;
+
+#define BCK(call)                                                                                 \
+  do {                                                                                            \
+    cudaError_t e__ = (call);                                                                     \
+    if (e__ != cudaSuccess) {                                                                     \
+      fsc_set_error(ctx, "backward %s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e__)); \
+      ctx->sticky = FSC_ERR_CUDA;                                                                 \
+      return FSC_ERR_CUDA;                                                                        \
+    }                                                                                             \
+  } while (0)
+#define BREQ(cond, code, ...)          \
+  do {                                 \
+    if (!(cond)) {                     \
+      fsc_set_error(ctx, __VA_ARGS__); \
+      return code;                     \
+    }                                  \
+  } while (0)
+#define BRC(expr)          \
+  do {                     \
+    int r__ = (expr);      \
+    if (r__) return r__;   \
+  } while (0)
+
+namespace {
+
+// G fp32 [T, d] -> bf16 (the GEMM operand of the shared expert's dgrad / wgrad)
+__global__ void __launch_bounds__(256) f32_to_bf16_kernel(const float4* __restrict__ x, uint2* __restrict__ y, long n4) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(x + i);
+    y[i] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+  }
+}
+
+// EP = 1 gradient "dispatch": row pos[t,j] of the expert-sorted layout gets bf16(G[t]) and
+// its gate g_tj (the receive layout is the send layout). One warp per copy.
+__global__ void __launch_bounds__(256) permute_grad_kernel(const float* __restrict__ G, const int* __restrict__ pos,
+                                                           const float* __restrict__ topk_w, long n_copies, int k,
+                                                           int d, uint4* __restrict__ gr, float* __restrict__ gate) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dv = d / 8;
+  for (long c = (long)blockIdx.x * 8 + w; c < n_copies; c += (long)gridDim.x * 8) {
+    const long t = c / k;
+    const int q = __ldg(pos + c);
+    const float4* a = reinterpret_cast<const float4*>(G + t * d);
+    for (int i = lane; i < dv; i += 32) {
+      const float4 lo = __ldg(a + 2 * i), hi = __ldg(a + 2 * i + 1);
+      gr[(long)q * dv + i] = make_uint4(pack_bf16x2(lo.x, lo.y), pack_bf16x2(lo.z, lo.w), pack_bf16x2(hi.x, hi.y),
+                                        pack_bf16x2(hi.z, hi.w));
+    }
+    if (lane == 0) gate[q] = __ldg(topk_w + c);
+  }
+}
+
+// Per token t (one CTA of 256 threads):
+//   dg_j   = gate gradient of copy j (dgs[pos] at EP > 1, sum of dg_part[pos] at EP = 1)
+//   dl_j   = g_j (dg_j - sum_i g_i dg_i)                (softmax over the selected logits)
+//   dxn    = dxn_shared[t] + sum_j dX[pos[t,j]] + sum_j dl_j W_R[e_j]
+//   r      = (mean x^2 + eps)^-1/2;  q = dxn gamma;  dx = G + r q - x r^3 (q . x) / d
+//   zg[t]  = dxn x r  (dgamma summands, summed over tokens by colsum_kernel)
+//   dl_row[pos[t,j]] = dl_j, r_tok[t] = r   (for dW_R)
+template <int K_MAX>
+__global__ void __launch_bounds__(256) token_bwd_kernel(const float* __restrict__ x, const float* __restrict__ G,
+                                                        const float* __restrict__ gamma, const float* __restrict__ w_router,
+                                                        const int* __restrict__ idx, const int* __restrict__ pos,
+                                                        const float* __restrict__ topk_w, const uint16_t* __restrict__ dxr,
+                                                        const float* __restrict__ dgs, const float* __restrict__ dg_part,
+                                                        int dg_n, int dg_ld, float* dxn_zg, float* __restrict__ dx,
+                                                        float* __restrict__ dl_row, float* __restrict__ r_tok, int T,
+                                                        int d, int k, float eps) {
+  __shared__ float s_red[8][2];
+  __shared__ float s_dl[K_MAX];
+  __shared__ int s_e[K_MAX], s_q[K_MAX];
+  __shared__ float s_r, s_qx;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (long t = blockIdx.x; t < T; t += gridDim.x) {
+    const float* xt = x + t * d;
+    if (tid < k) {
+      const int q = __ldg(pos + t * k + tid);
+      s_q[tid] = q;
+      s_e[tid] = __ldg(idx + t * k + tid);
+      float g = 0.f;
+      if (dgs) {
+        g = __ldcg(dgs + q);
+      } else {
+        for (int i = 0; i < dg_n; ++i) g += __ldg(dg_part + (long)q * dg_ld + i);
+      }
+      s_dl[tid] = g;   // dg_j for now
+    }
+    // sum x^2 (r) in fp32, fixed reduction order
+    float ss = 0.f;
+    for (int i = tid; i < d; i += 256) ss = fmaf(xt[i], xt[i], ss);
+    __syncthreads();
+    if (tid == 0) {
+      float gd = 0.f;
+      for (int j = 0; j < k; ++j) gd = fmaf(__ldg(topk_w + t * k + j), s_dl[j], gd);
+      for (int j = 0; j < k; ++j) {
+        const float g = __ldg(topk_w + t * k + j);
+        s_dl[j] = g * (s_dl[j] - gd);
+      }
+    }
+    // block reduction of ss
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) s_red[w][0] = ss;
+    __syncthreads();
+    if (tid == 0) {
+      float a = 0.f;
+      for (int i = 0; i < 8; ++i) a += s_red[i][0];
+      s_r = rsqrtf(a / (float)d + eps);
+    }
+    __syncthreads();
+    const float r = s_r;
+    // dxn (kept in registers per thread: d / 256 <= 32 columns), q . x
+    float qx = 0.f;
+    float dxn_v[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int i = tid + 256 * u;
+      dxn_v[u] = 0.f;
+      if (i < d) {
+        float v = dxn_zg[t * d + i];   // shared-expert part (fp32)
+        for (int j = 0; j < k; ++j) {
+          const uint16_t b = __ldcg(dxr + (long)s_q[j] * d + i);
+          v += __uint_as_float((uint32_t)b << 16);
+          v = fmaf(s_dl[j], __ldg(w_router + (long)s_e[j] * d + i), v);
+        }
+        dxn_v[u] = v;
+        qx = fmaf(v * __ldg(gamma + i), xt[i], qx);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) qx += __shfl_xor_sync(0xffffffffu, qx, o);
+    if (lane == 0) s_red[w][1] = qx;
+    __syncthreads();
+    if (tid == 0) {
+      float a = 0.f;
+      for (int i = 0; i < 8; ++i) a += s_red[i][1];
+      s_qx = a;
+    }
+    __syncthreads();
+    const float c3 = r * r * r * s_qx / (float)d;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int i = tid + 256 * u;
+      if (i < d) {
+        const float xv = xt[i];
+        const float qv = dxn_v[u] * __ldg(gamma + i);
+        dx[t * d + i] = __ldg(G + t * d + i) + r * qv - xv * c3;
+        dxn_zg[t * d + i] = dxn_v[u] * xv * r;
+      }
+    }
+    if (tid < k) dl_row[s_q[tid]] = s_dl[tid];
+    if (tid == 0) r_tok[t] = r;
+    __syncthreads();
+  }
+}
+
+// dgamma[i] = sum_t zg[t, i] (token order; 256 columns per CTA, 4 row phases summed in order)
+__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ zg, float* __restrict__ out, int T, int d) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= d) return;
+  float a = 0.f;
+  for (int t = 0; t < T; ++t) a += zg[(long)t * d + i];
+  out[i] = a;
+}
+
+// dW_R[e, i] = sum over the copies q of expert e (send order) of dl_row[q] * xn32[src_row[q], i],
+// xn32 = x r gamma in fp32
+__global__ void __launch_bounds__(256) dwr_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
+                                                  const float* __restrict__ r_tok, const int* __restrict__ offsets,
+                                                  const int* __restrict__ src_row, const float* __restrict__ dl_row,
+                                                  float* __restrict__ dwr, int d) {
+  const int e = blockIdx.y;
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= d) return;
+  const int q0 = offsets[e], q1 = offsets[e + 1];
+  float a = 0.f;
+  for (int q = q0; q < q1; ++q) {
+    const int t = __ldg(src_row + q);
+    a = fmaf(__ldg(dl_row + q), x[(long)t * d + i] * __ldg(r_tok + t), a);
+  }
+  dwr[(long)e * d + i] = a * __ldg(gamma + i);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------- host
+
+namespace {
+
+template <typename T>
+cudaError_t balloc(T** p, size_t n) {
+  return cudaMalloc(reinterpret_cast<void**>(p), (n ? n : 1) * sizeof(T));
+}
+
+// backward workspace, allocated on the first fsc_moe_backward call
+int ensure_bwd_workspace(fsc_ctx* ctx) {
+  if (ctx->b_duv) return FSC_OK;
+  const fsc_moe_config& c = ctx->cfg;
+  const long T = c.max_tokens, d = c.d, k = c.top_k;
+  const long rows = std::max(ctx->max_recv, std::max(T * k, T));
+  const long cmax = std::max(c.ffn, c.shared_ffn);
+  BCK(balloc(&ctx->b_gb, T * d));
+  BCK(balloc(&ctx->b_duv, rows * 2 * cmax));
+  BCK(balloc(&ctx->b_hg, rows * cmax));
+  ctx->b_dg_ld = 2 * (c.ffn / 64) + 2;
+  BCK(balloc(&ctx->b_dgpart, rows * ctx->b_dg_ld));
+  BCK(balloc(&ctx->b_dlrow, T * k));
+  BCK(balloc(&ctx->b_rtok, T));
+  if (ctx->ep == 1) {
+    BCK(balloc(&ctx->b_gr, T * k * d));
+    BCK(balloc(&ctx->b_gate, T * k));
+  }
+  return FSC_OK;
+}
+
+int launch_wgrad(fsc_ctx* ctx, const int* counts, int G, int m_total, int N1, int N2, const uint16_t* A, long lda,
+                 int a_col0, const uint16_t* B, long ldb, float* out, long rows, cudaStream_t s) {
+  if (!out) return FSC_OK;
+  WgradParams p{};
+  p.counts = counts; p.G = G; p.m_total = m_total; p.row_base = nullptr; p.N1 = N1; p.N2 = N2;
+  p.A = A; p.lda = lda; p.a_col0 = a_col0; p.B = B; p.ldb = ldb; p.b_col0 = 0; p.out = out; p.accumulate = 0;
+  BCK(launch_wgrad_gemm(p, rows, rows, ctx->gemm_ctas, s));
+  return FSC_OK;
+}
+
+}  // namespace
+
+extern "C" int fsc_moe_backward(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in,
+                                const float* grad_out, const fsc_moe_grads* gr, void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  BRC(fsc_validate_moe(ctx, w, T, x_in, grad_out));
+  BREQ(gr && gr->dx, FSC_ERR_SHAPE, "backward: dx is required");
+  BREQ(!ctx->pending, FSC_ERR_STATE, "backward: a FarSkip handle is outstanding");
+  BREQ(ctx->ep == 1 || ctx->ep_mode == FSC_EP_ALLTOALL, FSC_ERR_CONFIG,
+       "backward: the all-reduce inference variant has no backward");
+  BREQ(!ctx->spin, FSC_ERR_STATE, "backward: spin schedule active");
+  BREQ(!ctx->a2a_zero_bytes, FSC_ERR_STATE, "backward: zero-byte instrument active");
+  const fsc_moe_config& c = ctx->cfg;
+  const int d = c.d, E = c.n_experts, k = c.top_k, cf = c.ffn, cs = c.shared_ffn;
+  BREQ(cf % 64 == 0 && cs % 64 == 0, FSC_ERR_CONFIG, "backward: ffn widths must be multiples of 64");
+  BCK(cudaSetDevice(ctx->device));
+  if (T == 0) return FSC_OK;
+  BRC(ensure_bwd_workspace(ctx));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long R = (long)T * k;
+  memset(ctx->ph_used, 0, sizeof(ctx->ph_used));
+
+  // ---- recompute the selection (router + maps) and G in bf16
+  BCK(fsc_phase_begin(ctx, PH_ROUTER, s));
+  RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
+                  nullptr, nullptr, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, 32,
+                  nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  BCK(launch_router(rl, s));
+  PermLaunch pl{ctx->topk_idx, T, k, E, ctx->hist, ctx->base, ctx->counts, ctx->offsets, ctx->pos, ctx->src_row};
+  BCK(launch_perm_maps(pl, s));
+  BCK(fsc_phase_end(ctx, PH_ROUTER, s));
+  {
+    const long n4 = (long)T * d / 4;
+    ++g_launches;
+    f32_to_bf16_kernel<<<(int)std::min<long>((n4 + 255) / 256, 4 * kNumSMs), 256, 0, s>>>(
+        reinterpret_cast<const float4*>(grad_out), reinterpret_cast<uint2*>(ctx->b_gb), n4);
+    BCK(cudaGetLastError());
+  }
+  // ---- comm stream: Dispatch of the xn rows (recompute) and of the gradient rows
+  BCK(cudaEventRecord(ctx->ev_a, s));
+  BCK(cudaStreamWaitEvent(ctx->comm, ctx->ev_a, 0));
+  const uint16_t* xrows;      // expert input rows (receive layout)
+  const int* rcounts;         // rows per local expert
+  long rows_cap;
+  uint16_t* g_rows;
+  float* g_gate;
+  float* dgs = nullptr;
+  BCK(fsc_phase_begin(ctx, PH_DISPATCH, ctx->comm));
+  if (ctx->ep == 1) {
+    BCK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, (int)R, d, ctx->comm));
+    g_rows = ctx->b_gr;
+    g_gate = ctx->b_gate;
+    ++g_launches;
+    permute_grad_kernel<<<(int)std::min<long>((R + 7) / 8, 4 * kNumSMs), 256, 0, ctx->comm>>>(
+        grad_out, ctx->pos, ctx->topk_w, R, k, d, reinterpret_cast<uint4*>(g_rows), g_gate);
+    BCK(cudaGetLastError());
+    xrows = ctx->xs;
+    rcounts = ctx->counts;
+    rows_cap = R;
+  } else {
+    BRC(fsc_transport_dispatch(ctx, T, ctx->comm));
+    BRC(fsc_transport_dispatch_wait(ctx, ctx->comm));
+    BRC(fsc_transport_dispatch_grad(ctx, T, grad_out, ctx->comm));
+    fsc_transport_bwd_ptrs(ctx, &g_rows, &g_gate, &dgs);
+    xrows = ctx->xr;
+    rcounts = ctx->recv_counts;
+    rows_cap = ctx->recv_rows_cap;
+  }
+  BCK(fsc_phase_end(ctx, PH_DISPATCH, ctx->comm));
+  BCK(cudaEventRecord(ctx->ev_b, ctx->comm));
+
+  // ---- shared expert backward (beside the dispatches): dxn = shared part, dWs
+  const int cg = ctx->gemm_cg ? ctx->gemm_cg : 2;
+  BCK(fsc_phase_begin(ctx, PH_SHARED1, s));
+  if (cs) {
+    GemmLaunch a{};   // dh_s = G Ws3                      [T, c_s]
+    a.A = ctx->b_gb; a.a_rows = T; a.B0 = w->ws3; a.b_rows = d; a.b_group_rows = d; a.K = d; a.N = cs; a.G = 1;
+    a.m_total = T; a.out = ctx->hs; a.ldo = cs; a.epi = EPI_BF16; a.b_mn = true; a.num_ctas = ctx->gemm_ctas;
+    a.cta_group = cg;
+    BCK(launch_grouped_gemm(a, s));
+    GemmLaunch b{};   // recompute u, v on xn; du, dv, h
+    b.A = ctx->xn; b.a_rows = T; b.B0 = w->ws1; b.B1 = w->ws2; b.b_rows = cs; b.b_group_rows = cs; b.K = d; b.N = cs;
+    b.G = 1; b.m_total = T; b.out = ctx->b_duv; b.ldo = 2 * cs; b.out2 = ctx->b_hg; b.dh = ctx->hs;
+    b.epi = EPI_SWIGLU_BWD; b.num_ctas = ctx->gemm_ctas; b.cta_group = cg;
+    BCK(launch_grouped_gemm(b, s));
+    GemmLaunch cc{};  // dxn_s = [du | dv] [Ws1 ; Ws2]     fp32 [T, d]
+    cc.A = ctx->b_duv; cc.a_rows = T; cc.B0 = w->ws1; cc.B1 = w->ws2; cc.b_rows = cs; cc.b_group_rows = cs;
+    cc.K = 2 * cs; cc.N = d; cc.kb_split = cs / 64; cc.b_mn = true; cc.G = 1; cc.m_total = T; cc.out = ctx->tmp;
+    cc.ldo = d; cc.resid = nullptr; cc.ldr = d; cc.epi = EPI_RESID_F32; cc.num_ctas = ctx->gemm_ctas; cc.cta_group = cg;
+    BCK(launch_grouped_gemm(cc, s));
+    BRC(launch_wgrad(ctx, nullptr, 1, T, d, cs, ctx->b_gb, d, 0, ctx->b_hg, cs, gr->dws3, T, s));
+    BRC(launch_wgrad(ctx, nullptr, 1, T, cs, d, ctx->b_duv, 2 * cs, 0, ctx->xn, d, gr->dws1, T, s));
+    BRC(launch_wgrad(ctx, nullptr, 1, T, cs, d, ctx->b_duv, 2 * cs, cs, ctx->xn, d, gr->dws2, T, s));
+  } else {
+    BCK(cudaMemsetAsync(ctx->tmp, 0, sizeof(float) * (size_t)T * d, s));
+  }
+  BCK(fsc_phase_end(ctx, PH_SHARED1, s));
+
+  // ---- routed dgrad (after the dispatches)
+  BCK(fsc_phase_begin(ctx, PH_DISPATCH_STALL, s));
+  BCK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
+  BCK(fsc_phase_end(ctx, PH_DISPATCH_STALL, s));
+  const long avg_rows = R * ctx->ep / E;
+  const int rcg = ctx->gemm_cg ? ctx->gemm_cg : (avg_rows < 256 ? 1 : 2);
+  BCK(fsc_phase_begin(ctx, PH_GEMM1, s));
+  {
+    GemmLaunch a{};   // dh_u = G_r W3_e                     [rows, c]
+    a.A = g_rows; a.a_rows = rows_cap; a.B0 = w->w3; a.b_rows = (long)ctx->e_loc * d; a.b_group_rows = d; a.K = d;
+    a.N = cf; a.G = ctx->e_loc; a.counts = rcounts; a.out = ctx->h; a.ldo = cf; a.epi = EPI_BF16; a.b_mn = true;
+    a.num_ctas = ctx->gemm_ctas; a.cta_group = rcg;
+    BCK(launch_grouped_gemm(a, s));
+    GemmLaunch b{};   // recompute u, v; du, dv (gate-scaled), g h, dg partials
+    b.A = xrows; b.a_rows = rows_cap; b.B0 = w->w1; b.B1 = w->w2; b.b_rows = (long)ctx->e_loc * cf;
+    b.b_group_rows = cf; b.K = d; b.N = cf; b.G = ctx->e_loc; b.counts = rcounts; b.out = ctx->b_duv; b.ldo = 2 * cf;
+    b.out2 = ctx->b_hg; b.dh = ctx->h; b.row_gate = g_gate; b.dg_part = ctx->b_dgpart; b.dg_ld = ctx->b_dg_ld;
+    b.epi = EPI_SWIGLU_BWD; b.num_ctas = ctx->gemm_ctas; b.cta_group = rcg;
+    BCK(launch_grouped_gemm(b, s));
+  }
+  BCK(fsc_phase_end(ctx, PH_GEMM1, s));
+  // dg partials per row: 2 per N tile of the SwiGLU-backward GEMM (tile width HALF = BN / 2)
+  const int dg_n = 2 * (cf / (gemm_pick_bn(EPI_SWIGLU_BWD, cf) / 2));
+  BCK(fsc_phase_begin(ctx, PH_GEMM2, s));
+  {
+    GemmLaunch cc{};  // dX = [dU | dV] [W1_e ; W2_e]         [rows, d]
+    cc.A = ctx->b_duv; cc.a_rows = rows_cap; cc.B0 = w->w1; cc.B1 = w->w2; cc.b_rows = (long)ctx->e_loc * cf;
+    cc.b_group_rows = cf; cc.K = 2 * cf; cc.N = d; cc.kb_split = cf / 64; cc.b_mn = true; cc.G = ctx->e_loc;
+    cc.counts = rcounts; cc.out = ctx->y; cc.ldo = d; cc.epi = EPI_BF16; cc.num_ctas = ctx->gemm_ctas;
+    cc.cta_group = rcg;
+    BCK(launch_grouped_gemm(cc, s));
+  }
+  BCK(fsc_phase_end(ctx, PH_GEMM2, s));
+  // ---- gradient combine on the comm stream, routed wgrads beside it
+  if (ctx->ep > 1) {
+    BCK(cudaEventRecord(ctx->ev_g2, s));
+    BCK(cudaStreamWaitEvent(ctx->comm, ctx->ev_g2, 0));
+    BCK(fsc_phase_begin(ctx, PH_COMBINE, ctx->comm));
+    BRC(fsc_transport_combine_grad(ctx, ctx->y, ctx->b_dgpart, dg_n, ctx->b_dg_ld, ctx->comm));
+    BCK(fsc_phase_end(ctx, PH_COMBINE, ctx->comm));
+    BCK(cudaEventRecord(ctx->ev_comb, ctx->comm));
+  }
+  BCK(fsc_phase_begin(ctx, PH_SHARED2, s));
+  BRC(launch_wgrad(ctx, rcounts, ctx->e_loc, 0, d, cf, g_rows, d, 0, ctx->b_hg, cf, gr->dw3, rows_cap, s));
+  BRC(launch_wgrad(ctx, rcounts, ctx->e_loc, 0, cf, d, ctx->b_duv, 2 * cf, 0, xrows, d, gr->dw1, rows_cap, s));
+  BRC(launch_wgrad(ctx, rcounts, ctx->e_loc, 0, cf, d, ctx->b_duv, 2 * cf, cf, xrows, d, gr->dw2, rows_cap, s));
+  BCK(fsc_phase_end(ctx, PH_SHARED2, s));
+  const uint16_t* dxr = ctx->y;
+  if (ctx->ep > 1) {
+    BCK(fsc_phase_begin(ctx, PH_COMBINE_WAIT, s));
+    BCK(cudaStreamWaitEvent(s, ctx->ev_comb, 0));
+    BRC(fsc_transport_combine_grad_wait(ctx, s));
+    BCK(fsc_phase_end(ctx, PH_COMBINE_WAIT, s));
+    dxr = ctx->ys;
+  }
+  // ---- per token: router backward, sum of the copies, RMSNorm backward; dgamma; dW_R
+  BCK(fsc_phase_begin(ctx, PH_UNPERMUTE, s));
+  ++g_launches;
+  token_bwd_kernel<8><<<std::min(T, 8 * kNumSMs), 256, 0, s>>>(
+      x_in, grad_out, w->gamma, w->w_router, ctx->topk_idx, ctx->pos, ctx->topk_w, dxr, dgs, ctx->b_dgpart, dg_n,
+      ctx->b_dg_ld, ctx->tmp, gr->dx, ctx->b_dlrow, ctx->b_rtok, T, d, k, c.rms_eps);
+  BCK(cudaGetLastError());
+  if (gr->dgamma) {
+    ++g_launches;
+    colsum_kernel<<<(d + 255) / 256, 256, 0, s>>>(ctx->tmp, gr->dgamma, T, d);
+    BCK(cudaGetLastError());
+  }
+  if (gr->dw_router) {
+    ++g_launches;
+    dwr_kernel<<<dim3((d + 255) / 256, E), 256, 0, s>>>(x_in, w->gamma, ctx->b_rtok, ctx->offsets, ctx->src_row,
+                                                       ctx->b_dlrow, gr->dw_router, d);
+    BCK(cudaGetLastError());
+  }
+  BCK(fsc_phase_end(ctx, PH_UNPERMUTE, s));
+  return fsc_check_finite(ctx, gr->dx, (long)T * d, s, "fsc_moe_backward");
+}
+
+// ---------------------------------------------------------------------------- op-level entry points (tests)
+
+extern "C" int fsc_op_gemm_dgrad(fsc_ctx* ctx, int epi, const void* A, long a_rows, const void* B0, const void* B1,
+                                 long b_group_rows, int G, const int* counts, int m_total, int N, int K,
+                                 int kb_split, void* out, const float* resid, void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  BREQ(epi == EPI_BF16 || epi == EPI_RESID_F32, FSC_ERR_CONFIG, "dgrad epilogue must be bf16 or fp32-residual");
+  BREQ(K % 64 == 0 && N % 64 == 0 && G >= 1 && G <= 256 && kb_split >= 0 && kb_split * 64 <= K, FSC_ERR_CONFIG,
+       "bad dgrad GEMM shape");
+  GemmLaunch L{};
+  L.A = A; L.a_rows = a_rows; L.B0 = B0; L.B1 = B1 ? B1 : B0; L.b_rows = (long)G * b_group_rows;
+  L.b_group_rows = (int)b_group_rows; L.K = K; L.N = N; L.G = G; L.counts = counts; L.m_total = m_total; L.out = out;
+  L.ldo = N; L.resid = resid; L.ldr = N; L.epi = epi; L.b_mn = true; L.kb_split = kb_split;
+  L.num_ctas = ctx->gemm_ctas; L.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
+  BCK(launch_grouped_gemm(L, static_cast<cudaStream_t>(stream)));
+  return FSC_OK;
+}
+
+extern "C" int fsc_op_gemm_swiglu_bwd(fsc_ctx* ctx, const void* A, long a_rows, const void* B0, const void* B1, int G,
+                                      const int* counts, int m_total, int N, int K, const void* dh,
+                                      const float* row_gate, void* duv, void* hg, float* dg_part, int dg_ld,
+                                      void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  BREQ(K % 64 == 0 && N % 64 == 0 && G >= 1 && G <= 256 && dh && duv && hg, FSC_ERR_CONFIG,
+       "bad SwiGLU-backward GEMM arguments");
+  GemmLaunch L{};
+  L.A = A; L.a_rows = a_rows; L.B0 = B0; L.B1 = B1; L.b_rows = (long)G * N; L.b_group_rows = N; L.K = K; L.N = N;
+  L.G = G; L.counts = counts; L.m_total = m_total; L.out = duv; L.ldo = 2 * N; L.out2 = hg;
+  L.dh = static_cast<const uint16_t*>(dh); L.row_gate = row_gate; L.dg_part = dg_part; L.dg_ld = dg_ld;
+  L.epi = EPI_SWIGLU_BWD; L.num_ctas = ctx->gemm_ctas; L.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
+  BCK(launch_grouped_gemm(L, static_cast<cudaStream_t>(stream)));
+  return FSC_OK;
+}
+
+extern "C" int fsc_op_gemm_wgrad(fsc_ctx* ctx, const int* counts, int G, int m_total, int N1, int N2, const void* A,
+                                 long a_rows, long lda, int a_col0, const void* B, long ldb, int b_col0, float* out,
+                                 int accumulate, void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  WgradParams p{};
+  p.counts = counts; p.G = G; p.m_total = m_total; p.N1 = N1; p.N2 = N2;
+  p.A = static_cast<const uint16_t*>(A); p.lda = lda; p.a_col0 = a_col0;
+  p.B = static_cast<const uint16_t*>(B); p.ldb = ldb; p.b_col0 = b_col0; p.out = out; p.accumulate = accumulate;
+  BCK(launch_wgrad_gemm(p, a_rows, a_rows, ctx->gemm_ctas, static_cast<cudaStream_t>(stream)));
+  return FSC_OK;
+}

@@ -271,6 +271,22 @@ cudaError_t launch_copy_f32(const float* src, float* dst, long n, cudaStream_t s
   return cudaGetLastError();
 }
 
+__global__ void spin_kernel(long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(200);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while ((long long)(t - t0) < ns);
+}
+
+cudaError_t launch_spin(long long ns, cudaStream_t s) {
+  if (ns <= 0) return cudaSuccess;
+  ++g_launches;
+  spin_kernel<<<1, 1, 0, s>>>(ns);
+  return cudaGetLastError();
+}
+
 // Debug finiteness check (FSC_ERR_NONFINITE, fsc_set_debug_checks): count the
 // non-finite fp32 values of x [n] into *bad.
 __global__ void __launch_bounds__(256) nonfinite_kernel(const float4* __restrict__ x, long n4, int* bad) {

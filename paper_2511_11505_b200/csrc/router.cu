@@ -227,9 +227,10 @@ FSC_DEVINL void select_token_thread(const float* lg, long t, int tt, float B, co
   int idx[K1];
 #pragma unroll
   for (int j = 0; j < K1; ++j) {
-    val[j] = -FLT_MAX;
+    val[j] = -INFINITY;
     idx[j] = 0x7fffffff;
   }
+  bool finite = true;   // a non-finite input row (NaN logits) still selects valid ids, never refined
   // the row (16-byte aligned, E <= padded width, a multiple of 16) is read 16
   // logits at a time with independent LDS.128: one shared-memory latency per 16
   // insertions instead of one per logit (the MIO queue is busy with the xn warps)
@@ -246,7 +247,11 @@ FSC_DEVINL void select_token_thread(const float* lg, long t, int tt, float B, co
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int e = e0 + u;
-      const float v = e < E ? vv[u] : -FLT_MAX;
+      float v = e < E ? vv[u] : -INFINITY;
+      if (e < E && !(fabsf(v) <= FLT_MAX)) {
+        finite = false;
+        v = -FLT_MAX;
+      }
       if (v > val[K1 - 1]) {
         bool gt[K1];
 #pragma unroll
@@ -271,7 +276,7 @@ FSC_DEVINL void select_token_thread(const float* lg, long t, int tt, float B, co
 #endif
   const float vk = val[k - 1], vk1 = k < E ? val[k] : -FLT_MAX;
   const float thr2 = 2.f * B + 4.f * kU * (fabsf(vk) + fabsf(vk1)) + 1e-7f;
-  if (k < E && vk - vk1 <= thr2) {   // ambiguous boundary: refined by the block (refine_block)
+  if (finite && k < E && vk - vk1 <= thr2) {   // ambiguous boundary: refined by the block (refine_block)
     if (L.n_refined) atomicAdd(L.n_refined, 1);
     rs.flag[tt] = 1;
     rs.thr[tt][0] = thr2;

@@ -91,6 +91,13 @@ int ensure_workspace(fsc_ctx* ctx, const fsc_attn_weights* aw, int L) {
 int attention_a(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, const float* attn_in, cudaStream_t s) {
   const int d = ctx->cfg.d, Hq = aw->n_heads, Hkv = aw->n_kv_heads, hd = aw->head_dim;
   const int nqkv = (Hq + 2 * Hkv) * hd;
+  SCK(fsc_fuzz(ctx, s));
+  SCK(fsc_phase_begin(ctx, PH_ATTN_A, s));
+  if (ctx->spin) {
+    SCK(fsc_spin(ctx, SP_QKV, s));
+    SCK(fsc_phase_end(ctx, PH_ATTN_A, s));
+    return FSC_OK;
+  }
   SCK(launch_rmsnorm_bf16(attn_in, aw->gamma, ctx->hn, T, d, ctx->cfg.rms_eps, s));
   GemmLaunch g{};
   g.A = ctx->hn; g.a_rows = T; g.B0 = aw->w_qkv; g.b_rows = nqkv; g.b_group_rows = nqkv; g.K = d; g.N = nqkv;
@@ -98,6 +105,7 @@ int attention_a(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, co
   g.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
   SCK(launch_grouped_gemm(g, s));
   SCK(launch_rope(ctx->qkv, T, Hq, Hkv, hd, seq_len, aw->rope_theta, s));
+  SCK(fsc_phase_end(ctx, PH_ATTN_A, s));
   return FSC_OK;
 }
 
@@ -110,6 +118,13 @@ bool tp_mode(const fsc_ctx* ctx) { return ctx->ep > 1 && ctx->ep_mode == FSC_EP_
 int attention_b(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, const float* resid, float* out,
                 float* cache_attn_out, cudaStream_t s) {
   const int d = ctx->cfg.d, Hq = aw->n_heads, Hkv = aw->n_kv_heads, hd = aw->head_dim;
+  SCK(fsc_fuzz(ctx, s));
+  SCK(fsc_phase_begin(ctx, PH_ATTN_B, s));
+  if (ctx->spin) {   // wiring test: out = resid only
+    SCK(fsc_spin(ctx, SP_CORE, s));
+    SCK(fsc_phase_end(ctx, PH_ATTN_B, s));
+    return FSC_OK;
+  }
   SCK(launch_flash_attn(ctx->qkv, ctx->ao, T, Hq, Hkv, hd, seq_len, s));
   if (tp_mode(ctx)) {
     GemmLaunch g{};
@@ -128,6 +143,7 @@ int attention_b(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, co
     ctx->attn_pending = cs != s ? 2 : 1;
     ctx->attn_cache = cache_attn_out;
     ctx->attn_T = T;
+    SCK(fsc_phase_end(ctx, PH_ATTN_B, s));
     return FSC_OK;
   }
   GemmLaunch g{};
@@ -135,6 +151,7 @@ int attention_b(fsc_ctx* ctx, const fsc_attn_weights* aw, int T, int seq_len, co
   g.G = 1; g.m_total = T; g.out = out; g.ldo = d; g.resid = resid; g.ldr = d; g.epi = EPI_RESID_F32;
   g.num_ctas = ctx->gemm_ctas; g.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
   SCK(launch_grouped_gemm(g, s));
+  SCK(fsc_phase_end(ctx, PH_ATTN_B, s));
   if (cache_attn_out) {
     g.out = cache_attn_out;
     g.resid = nullptr;
@@ -250,7 +267,7 @@ static int stack_body(fsc_ctx* ctx, const fsc_attn_weights* attn, const fsc_moe_
       // partial := M (+= shared inside); routed pending. Nothing can overlap the
       // dispatch here (Regular wiring), so it runs on the compute stream.
       const int save = ctx->no_overlap;
-      ctx->no_overlap = 1;
+      ctx->no_overlap = ov ? 2 : 1;   // OVERLAPPED: Regular+ (shared expert beside the combine)
       int rc = fsc_moe_forward_farskip(ctx, mw, T, bufM, bufM, nullptr, nullptr, &h, dbgp, s);
       ctx->no_overlap = save;
       SRC(rc);

@@ -36,12 +36,13 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Layout {  // byte offsets inside every rank's symmetric region
-  size_t flags, cnt, ret, xr, ys, part[2], red[2], xq, xsc, total;
+  size_t flags, cnt, ret, xr, ys, part[2], red[2], xq, xsc, gr, gate, dgs, total;
 };
 
 // FLAG_CNT, FLAG_DISP, FLAG_COMB, then (READY, DONE) per all-reduce channel
-// (channel 0: MoE routed sum; channel 1: TP attention o-projection)
-constexpr int kFlagRows = 7;
+// (channel 0: MoE routed sum; channel 1: TP attention o-projection), then the backward's
+// gradient dispatch / gradient combine
+constexpr int kFlagRows = 9;
 constexpr int kEpochs = 2;     // epoch counters: [0] all-to-all + AR channel 0, [1] AR channel 1
 
 Layout layout_for(const fsc_ctx* c) {
@@ -58,13 +59,18 @@ Layout layout_for(const fsc_ctx* c) {
       L.red[ch] = align_up(L.part[ch] + T * d * sizeof(float));
       o = align_up(L.red[ch] + T * d * sizeof(float));
     }
-    L.xq = L.xsc = L.total = o;
+    L.xq = L.xsc = L.gr = L.gate = L.dgs = L.total = o;
     return L;
   }
   L.ret = align_up(L.cnt + P * E * sizeof(int));     // int [max_recv]
   L.xr = align_up(L.ret + (size_t)c->max_recv * sizeof(int));
   L.ys = align_up(L.xr + (size_t)c->max_recv * d * 2);
-  L.part[0] = L.part[1] = L.red[0] = L.red[1] = L.xq = L.xsc = L.total = align_up(L.ys + Tk * d * 2);
+  // backward (fsc_moe_backward): gradient rows + gates received per expert row, gate
+  // gradients combined back per send row (the dX rows come back into ys)
+  L.gr = align_up(L.ys + Tk * d * 2);
+  L.gate = align_up(L.gr + (size_t)c->max_recv * d * 2);
+  L.dgs = align_up(L.gate + (size_t)c->max_recv * sizeof(float));
+  L.part[0] = L.part[1] = L.red[0] = L.red[1] = L.xq = L.xsc = L.total = align_up(L.dgs + Tk * sizeof(float));
   if (c->dispatch_fp8) {                             // FP8 payload: e4m3 rows + fp32 per-128-column scales
     L.xq = L.total;
     L.xsc = align_up(L.xq + (size_t)c->max_recv * d);
@@ -77,7 +83,8 @@ struct Peers {
   char* base[kMaxP];
 };
 
-enum { FLAG_CNT = 0, FLAG_DISP = 1, FLAG_COMB = 2, FLAG_AR_READY = 3, FLAG_AR_DONE = 4 };   // + 2 ch for AR
+enum { FLAG_CNT = 0, FLAG_DISP = 1, FLAG_COMB = 2, FLAG_AR_READY = 3, FLAG_AR_DONE = 4,   // + 2 ch for AR
+       FLAG_GDISP = 7, FLAG_GCOMB = 8 };
 constexpr int kEpochSlot = kFlagRows * kMaxP;   // int index of the epoch counters in the flags area
 
 FSC_DEVINL int read_epoch(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
@@ -110,6 +117,21 @@ FSC_DEVINL void wait_flags(char* mybase, int slot, int P, int epoch) {
       __nanosleep(64);
       if (global_ns() - t0 > kFlagTimeoutNs) __trap();
     }
+  }
+}
+// Copy one row of dv uint4 with a warp, 8 loads in flight per lane before the stores
+// (remote stores are posted; the loads' latency is what limits a warp's throughput).
+// STREAM: the source is read once (evict-first); else it stays in L2 (xn rows are read k times).
+template <bool STREAM>
+FSC_DEVINL void copy_row_warp(const uint4* __restrict__ a, uint4* b, int dv, int lane) {
+  for (int i0 = lane; i0 < dv; i0 += 256) {
+    uint4 buf[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + 32 * u < dv) buf[u] = __ldcs(a + i0 + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + 32 * u < dv) b[i0 + 32 * u] = buf[u];
   }
 }
 }  // namespace
@@ -175,13 +197,14 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(Peers peers, int rank,
                                                           size_t off_ret,
                                                           const uint4* __restrict__ xn, const int* __restrict__ src_row,
                                                           const int* __restrict__ offsets,
-                                                          const int* __restrict__ send_base, int* ticket) {
+                                                          const int* __restrict__ send_base, int* ticket,
+                                                          int zero_bytes) {
   __shared__ int s_off[129];
   for (int i = threadIdx.x; i <= E; i += blockDim.x) s_off[i] = offsets[i];
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int dv = d / 8;
-  for (long q = (long)blockIdx.x * 8 + w; q < R; q += (long)gridDim.x * 8) {
+  for (long q = (long)blockIdx.x * 8 + w; q < (zero_bytes ? 0 : R); q += (long)gridDim.x * 8) {
     int lo = 0, hi = E;                    // expert of send row q
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -191,7 +214,7 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(Peers peers, int rank,
     const long dst = send_base[e] + (q - s_off[e]);
     const uint4* a = xn + (long)src_row[q] * dv;
     uint4* b = reinterpret_cast<uint4*>(peers.base[p] + off_xr) + dst * dv;
-    for (int i = lane; i < dv; i += 32) b[i] = a[i];
+    copy_row_warp<false>(a, b, dv, lane);
     if (lane == 0) reinterpret_cast<int*>(peers.base[p] + off_ret)[dst] = (rank << 24) | (int)q;
   }
   // last CTA out raises the dispatch flag at every destination
@@ -222,13 +245,14 @@ __global__ void __launch_bounds__(256) ep_dispatch_fp8_kernel(Peers peers, int r
                                                               const uint4* __restrict__ xn,
                                                               const int* __restrict__ src_row,
                                                               const int* __restrict__ offsets,
-                                                              const int* __restrict__ send_base, int* ticket) {
+                                                              const int* __restrict__ send_base, int* ticket,
+                                                          int zero_bytes) {
   __shared__ int s_off[129];
   for (int i = threadIdx.x; i <= E; i += blockDim.x) s_off[i] = offsets[i];
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int dv = d / 8;
-  for (long q = (long)blockIdx.x * 8 + w; q < R; q += (long)gridDim.x * 8) {
+  for (long q = (long)blockIdx.x * 8 + w; q < (zero_bytes ? 0 : R); q += (long)gridDim.x * 8) {
     int lo = 0, hi = E;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -312,6 +336,123 @@ __global__ void ep_signal_kernel(Peers peers, int rank, int P, int slot, const i
   const int epoch = read_epoch(epoch_ptr);
   __threadfence_system();
   if (threadIdx.x < P) st_release_sys(flag_ptr(peers.base[threadIdx.x], slot, rank), epoch);
+}
+
+// a9, decoupled from the down GEMM (FSC_COMBINE_STREAM): runs on the comm stream after
+// GEMM2 stored the expert outputs y locally in the receive layout; every received row r
+// goes back to its source rank (ret[r] >> 24), row (ret[r] & 0xFFFFFF) of that rank's
+// ys (the send layout, "Combine"). One warp per row, 16 B per lane; the
+// last CTA raises FLAG_COMB at every source. zero_bytes: flags only (test instrument).
+__global__ void __launch_bounds__(256) ep_combine_kernel(Peers peers, int rank, int P, int e_loc,
+                                                         const int* __restrict__ recv_counts,
+                                                         const int* __restrict__ ret, const uint4* __restrict__ y,
+                                                         size_t off_ys, int d, const int* epoch_ptr, int* ticket,
+                                                         int zero_bytes) {
+  __shared__ long s_rows;
+  if (threadIdx.x == 0) {
+    long n = 0;
+    for (int i = 0; i < e_loc; ++i) n += recv_counts[i];
+    s_rows = zero_bytes ? 0 : n;
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dv = d / 8;
+  for (long r = (long)blockIdx.x * 8 + w; r < s_rows; r += (long)gridDim.x * 8) {
+    const int v = __ldg(ret + r);
+    const uint4* a = y + r * dv;
+    uint4* b = reinterpret_cast<uint4*>(peers.base[(uint32_t)v >> 24] + off_ys) + (long)(v & 0xFFFFFF) * dv;
+    copy_row_warp<true>(a, b, dv, lane);
+  }
+  const int epoch = read_epoch(epoch_ptr);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(ticket, 1) == (int)gridDim.x - 1) {
+      *ticket = 0;
+      __threadfence_system();
+      for (int p = 0; p < P; ++p) st_release_sys(flag_ptr(peers.base[p], FLAG_COMB, rank), epoch);
+    }
+  }
+}
+
+// Backward gradient dispatch (the mirror of the Combine): every copy
+// (t, j) sends G[t] (fp32 -> bf16) and its gate g_tj to the row of the owner's receive
+// buffer where the forward's Dispatch put xn[t] (same send_base / offsets). One warp per
+// copy; the last CTA raises FLAG_GDISP at every destination.
+__global__ void __launch_bounds__(256) ep_dispatch_grad_kernel(Peers peers, int rank, int P, int T, int k, int d,
+                                                               int e_loc, const int* epoch_ptr, size_t off_gr,
+                                                               size_t off_gate, const float* __restrict__ G,
+                                                               const int* __restrict__ idx, const int* __restrict__ pos,
+                                                               const float* __restrict__ topk_w,
+                                                               const int* __restrict__ offsets,
+                                                               const int* __restrict__ send_base, int* ticket) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dv = d / 8;
+  for (long c = (long)blockIdx.x * 8 + w; c < (long)T * k; c += (long)gridDim.x * 8) {
+    const long t = c / k;
+    const int e = __ldg(idx + c), q = __ldg(pos + c), p = e / e_loc;
+    const long dst = __ldg(send_base + e) + (q - __ldg(offsets + e));
+    const float4* a = reinterpret_cast<const float4*>(G + t * d);
+    uint4* b = reinterpret_cast<uint4*>(peers.base[p] + off_gr) + dst * dv;
+    for (int i = lane; i < dv; i += 32) {
+      const float4 lo = __ldg(a + 2 * i), hi = __ldg(a + 2 * i + 1);
+      b[i] = make_uint4(pack_bf16x2(lo.x, lo.y), pack_bf16x2(lo.z, lo.w), pack_bf16x2(hi.x, hi.y),
+                        pack_bf16x2(hi.z, hi.w));
+    }
+    if (lane == 0) reinterpret_cast<float*>(peers.base[p] + off_gate)[dst] = __ldg(topk_w + c);
+  }
+  const int epoch = read_epoch(epoch_ptr);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(ticket, 1) == (int)gridDim.x - 1) {
+      *ticket = 0;
+      __threadfence_system();
+      for (int p = 0; p < P; ++p) st_release_sys(flag_ptr(peers.base[p], FLAG_GDISP, rank), epoch);
+    }
+  }
+}
+
+// Backward gradient combine (the mirror of the Dispatch): received row r's dX row (y, the
+// dgrad GEMM output, receive layout) goes back to its source's ys at the send row it came
+// from, with its gate gradient dg = sum of the row's dg_part entries (fixed order).
+__global__ void __launch_bounds__(256) ep_combine_grad_kernel(Peers peers, int rank, int P, int e_loc,
+                                                              const int* __restrict__ recv_counts,
+                                                              const int* __restrict__ ret,
+                                                              const uint4* __restrict__ y, size_t off_ys,
+                                                              size_t off_dgs, const float* __restrict__ dg_part,
+                                                              int dg_n, int dg_ld, int d, const int* epoch_ptr,
+                                                              int* ticket) {
+  __shared__ long s_rows;
+  if (threadIdx.x == 0) {
+    long n = 0;
+    for (int i = 0; i < e_loc; ++i) n += recv_counts[i];
+    s_rows = n;
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dv = d / 8;
+  for (long r = (long)blockIdx.x * 8 + w; r < s_rows; r += (long)gridDim.x * 8) {
+    const int v = __ldg(ret + r);
+    char* base = peers.base[(uint32_t)v >> 24];
+    const long q = v & 0xFFFFFF;
+    copy_row_warp<true>(y + r * dv, reinterpret_cast<uint4*>(base + off_ys) + q * dv, dv, lane);
+    if (lane == 0) {
+      float g = 0.f;
+      for (int i = 0; i < dg_n; ++i) g += __ldg(dg_part + r * dg_ld + i);
+      reinterpret_cast<float*>(base + off_dgs)[q] = g;
+    }
+  }
+  const int epoch = read_epoch(epoch_ptr);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(ticket, 1) == (int)gridDim.x - 1) {
+      *ticket = 0;
+      __threadfence_system();
+      for (int p = 0; p < P; ++p) st_release_sys(flag_ptr(peers.base[p], FLAG_GCOMB, rank), epoch);
+    }
+  }
 }
 
 __global__ void ep_wait_kernel(char* mybase, int slot, int P, const int* epoch_ptr) {
@@ -484,18 +625,19 @@ int fsc_transport_dispatch(fsc_ctx* ctx, int T, cudaStream_t s) {
   TCK(cudaGetLastError());
   const int R = T * c.top_k;
   int blocks = (R + 7) / 8;
-  if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
+  if (blocks > ctx->comm_ctas) blocks = ctx->comm_ctas;   // a fraction of the SMs
   if (blocks < 1) blocks = 1;
   ++g_launches;
   if (ctx->dispatch_fp8)
     ep_dispatch_fp8_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, P, R, c.d, E, ctx->e_loc, epoch_ptr(ctx),
                                                   st->lay.xq, st->lay.xsc, st->lay.ret,
                                                   reinterpret_cast<const uint4*>(ctx->xn), ctx->src_row, ctx->offsets,
-                                                  st->send_base, st->ticket);
+                                                  st->send_base, st->ticket, ctx->a2a_zero_bytes);
   else
     ep_dispatch_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, P, R, c.d, E, ctx->e_loc, epoch_ptr(ctx),
                                               st->lay.xr, st->lay.ret, reinterpret_cast<const uint4*>(ctx->xn),
-                                              ctx->src_row, ctx->offsets, st->send_base, st->ticket);
+                                              ctx->src_row, ctx->offsets, st->send_base, st->ticket,
+                                              ctx->a2a_zero_bytes);
   TCK(cudaGetLastError());
   return FSC_OK;
 }
@@ -524,6 +666,79 @@ int fsc_transport_combine(fsc_ctx* ctx, int, cudaStream_t s) {
   ep_signal_kernel<<<1, 32, 0, s>>>(ctx->peer->peers, ctx->rank, ctx->ep, FLAG_COMB, epoch_ptr(ctx));
   TCK(cudaGetLastError());
   return FSC_OK;
+}
+
+// decoupled combine (FSC_COMBINE_STREAM): y = this rank's expert outputs, receive layout
+int fsc_transport_combine_push(fsc_ctx* ctx, const uint16_t* y, cudaStream_t s) {
+  fsc_peer_state* st = ctx->peer;
+  const int d = ctx->cfg.d;
+  int blocks = (int)((ctx->max_recv + 7) / 8);
+  if (blocks > ctx->comm_ctas) blocks = ctx->comm_ctas;
+  if (blocks < 1) blocks = 1;
+  ++g_launches;
+  ep_combine_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, ctx->ep, ctx->e_loc, ctx->recv_counts,
+                                           reinterpret_cast<const int*>(st->local + st->lay.ret),
+                                           reinterpret_cast<const uint4*>(y), st->lay.ys, d, epoch_ptr(ctx),
+                                           st->ticket + 2, ctx->a2a_zero_bytes);
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+// ---- backward (fsc_moe_backward)
+void fsc_transport_bwd_ptrs(fsc_ctx* ctx, uint16_t** gr, float** gate, float** dgs) {
+  fsc_peer_state* st = ctx->peer;
+  *gr = reinterpret_cast<uint16_t*>(st->local + st->lay.gr);
+  *gate = reinterpret_cast<float*>(st->local + st->lay.gate);
+  *dgs = reinterpret_cast<float*>(st->local + st->lay.dgs);
+}
+
+// G rows + gates to the experts' owners (after fsc_transport_dispatch of the same call:
+// send_base and the epoch are that call's), then wait for every source's rows
+int fsc_transport_dispatch_grad(fsc_ctx* ctx, int T, const float* G, cudaStream_t s) {
+  fsc_peer_state* st = ctx->peer;
+  const fsc_moe_config& c = ctx->cfg;
+  const long R = (long)T * c.top_k;
+  int blocks = (int)((R + 7) / 8);
+  if (blocks > ctx->comm_ctas) blocks = ctx->comm_ctas;
+  if (blocks < 1) blocks = 1;
+  g_launches += 2;
+  ep_dispatch_grad_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, ctx->ep, T, c.top_k, c.d, ctx->e_loc,
+                                                 epoch_ptr(ctx), st->lay.gr, st->lay.gate, G, ctx->topk_idx, ctx->pos,
+                                                 ctx->topk_w, ctx->offsets, st->send_base, st->ticket);
+  TCK(cudaGetLastError());
+  ep_wait_kernel<<<1, 32, 0, s>>>(st->local, FLAG_GDISP, ctx->ep, epoch_ptr(ctx));
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+// dX rows (y, receive layout) + gate gradients back to their sources
+int fsc_transport_combine_grad(fsc_ctx* ctx, const uint16_t* y, const float* dg_part, int dg_n, int dg_ld,
+                               cudaStream_t s) {
+  fsc_peer_state* st = ctx->peer;
+  int blocks = (int)((ctx->max_recv + 7) / 8);
+  if (blocks > ctx->comm_ctas) blocks = ctx->comm_ctas;
+  if (blocks < 1) blocks = 1;
+  ++g_launches;
+  ep_combine_grad_kernel<<<blocks, 256, 0, s>>>(st->peers, ctx->rank, ctx->ep, ctx->e_loc, ctx->recv_counts,
+                                                reinterpret_cast<const int*>(st->local + st->lay.ret),
+                                                reinterpret_cast<const uint4*>(y), st->lay.ys, st->lay.dgs, dg_part,
+                                                dg_n, dg_ld, ctx->cfg.d, epoch_ptr(ctx), st->ticket + 2);
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+int fsc_transport_combine_grad_wait(fsc_ctx* ctx, cudaStream_t s) {
+  ++g_launches;
+  ep_wait_kernel<<<1, 32, 0, s>>>(ctx->peer->local, FLAG_GCOMB, ctx->ep, epoch_ptr(ctx));
+  TCK(cudaGetLastError());
+  return FSC_OK;
+}
+
+// device pointers of the exchanged counts matrix [P][E] and the receive map [max_recv]
+void fsc_transport_debug(fsc_ctx* ctx, const int** cnt, const int** ret) {
+  fsc_peer_state* st = ctx->peer;
+  *cnt = reinterpret_cast<const int*>(st->local + st->lay.cnt);
+  *ret = reinterpret_cast<const int*>(st->local + st->lay.ret);
 }
 
 int fsc_transport_combine_wait(fsc_ctx* ctx, cudaStream_t s) {

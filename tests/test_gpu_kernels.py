@@ -16,7 +16,7 @@ def ctx():
     from paper_2511_11505_b200 import build
     build.build()
     from paper_2511_11505_b200 import Context
-    c = Context(d=5120, n_experts=128, top_k=8, ffn=1408, shared_ffn=0, max_tokens=8192)
+    c = Context(d=5120, n_experts=128, top_k=8, ffn=1408, shared_ffn=0, max_tokens=16384)
     yield c
     c.close()
 
@@ -156,8 +156,10 @@ def test_gemm_inplace_resid(ctx, cg):
 # ----------------------------------------------------------------------------- K1 router
 # T < 148*32 tokens run the split-d path (partials over d, fixed-order finish kernel);
 # larger T the single-pass kernel with balanced waves (two CTAs per SM)
+# ... and the full BASELINE batch sizes the bench runs (T = 8192 / 16384 / 8192)
 ROUTER_CASES = [("tiny", 32), ("tiny", 1), ("dsv2lite", 700), ("qwen3", 513), ("scout", 256), ("dsv2lite", 64),
-                ("qwen3", 2400), ("dsv2lite", 4800), ("qwen3", 6000), ("scout", 5000)]
+                ("qwen3", 2400), ("dsv2lite", 4800), ("qwen3", 6000), ("scout", 5000),
+                ("dsv2lite", 8192), ("qwen3", 16384), ("scout", 8192)]
 
 
 @pytest.fixture(scope="module")
@@ -175,6 +177,12 @@ def test_router_parity(ctx, name, T):
     _router_parity(ctx, name, T)
 
 
+@pytest.mark.parametrize("name,T,skew", [("dsv2lite", 8192, synth.SKEW_DEFAULT), ("qwen3", 16384, 0.5)])
+def test_router_parity_skewed(ctx, name, T, skew):
+    """Skewed-load tokens: a shared mean shift makes some experts hot."""
+    _router_parity(ctx, name, T, skew)
+
+
 @pytest.mark.parametrize("name,T", [c for c in ROUTER_CASES if c[0] in ("dsv2lite", "scout")] +
                          [("dsv2lite", 8192), ("scout", 8192), ("dsv2lite", 129)])
 def test_router_parity_int8(ctx_i8, name, T):
@@ -185,10 +193,10 @@ def test_router_parity_int8(ctx_i8, name, T):
     assert nref <= max(4, T // 50)
 
 
-def _router_parity(ctx, name, T):
+def _router_parity(ctx, name, T, skew=0.0):
     shape = synth.CONFIGS[name]
     w = synth.moe_weights(dataclass_replace_small(shape), seed=1)
-    x = synth.tokens(shape, seed=1, T=T)
+    x = synth.tokens(shape, seed=1, T=T, skew=skew)
     d, E, k = shape.d, shape.n_experts, shape.top_k
     xn = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
     idx = torch.empty(T, k, dtype=torch.int32, device="cuda")

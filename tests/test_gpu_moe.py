@@ -139,31 +139,44 @@ def test_farskip_handle_depth_is_one():
     ctx.close()
 
 
-@pytest.mark.parametrize("name", ["dsv2lite", "qwen3"])
-def test_full_size_sampled_parity(name):
-    """BASELINE config sizes in the bench's launch configuration; the oracle
-    recomputes a sample of tokens one by one (the block is token-independent)."""
+def check_full_routing(shape, lay, x, dbg):
+    """Every token of the batch: the selection equals the fp64 oracle's (R-1 exclusions
+    counted), gates within 2e-5, counts / positions equal the oracle's stable maps."""
+    r, excl = om.adopt_router(lay, x, dbg["topk_idx"])
+    np.testing.assert_array_equal(dbg["topk_idx"], r.idx)
+    np.testing.assert_allclose(dbg["topk_w"], r.gates, rtol=0, atol=2e-5)
+    m = om.permutation_maps(r.idx, shape.n_experts)
+    np.testing.assert_array_equal(dbg["counts"], m.counts)
+    np.testing.assert_array_equal(dbg["pos"], m.pos)
+    return r, excl
+
+
+@pytest.mark.parametrize("name,skew", [("dsv2lite", 0.0), ("qwen3", 0.0), ("dsv2lite", synth.SKEW_DEFAULT),
+                                       ("qwen3", 0.5)])
+def test_full_size_parity(name, skew):
+    """BASELINE config sizes (T = 8192 / 16384) in the bench's launch configuration:
+    routing, gates, counts and positions of EVERY token against the fp64 oracle; the
+    outputs of a token sample recomputed by the oracle one by one (the block is
+    token-independent). skew > 0: the skewed-load token recipe."""
     shape = synth.CONFIGS[name]
     T = shape.tokens
     ctx = make_ctx(shape, T)
     w = synth.moe_weights(shape, seed=0)
-    x = synth.tokens(shape, seed=0, T=T)
+    x = synth.tokens(shape, seed=0, T=T, skew=skew)
     out, dbg = run_blocking(ctx, moe_weights_dev(w), x)
     assert dbg["counts"].sum() == T * shape.top_k
+    lay = om.layer_from_synth(w, shape.top_k)
+    r_all, excl = check_full_routing(shape, lay, x, dbg)
     rng = np.random.default_rng(0)
     sample = np.sort(np.concatenate([[0, T - 1], rng.choice(T, 62, replace=False)]))
-    lay = om.layer_from_synth(w, shape.top_k)
-    r, excl = om.adopt_router(lay, x[sample], dbg["topk_idx"][sample])
-    np.testing.assert_array_equal(dbg["topk_idx"][sample], r.idx)
+    r, _ = om.adopt_router(lay, x[sample], dbg["topk_idx"][sample])
     sh, ro, _ = om.moe_block(x[sample], lay, router=r)
     ref = (x[sample].astype(np.float64) + sh) + ro
     assert rel_l2(out[sample], ref) < TOL
     assert rel_l2(dbg["routed_out"][sample], ro) < TOL
-    # the full routing map is a valid stable permutation (checked on every token)
-    m = om.permutation_maps(dbg["topk_idx"], shape.n_experts)
-    np.testing.assert_array_equal(dbg["counts"], m.counts)
-    np.testing.assert_array_equal(dbg["pos"], m.pos)
-    print(f"{name}: refined={int(dbg['n_refined'][0])} excluded={int(excl.sum())}")
+    load = dbg["counts"].max() / dbg["counts"].mean()
+    print(f"{name} skew={skew}: refined={int(dbg['n_refined'][0])} excluded={int(excl.sum())} "
+          f"max/mean load={load:.2f}")
     ctx.close()
 
 
@@ -188,6 +201,14 @@ def test_scout_full_size_sampled_parity():
     lay = _layer_f32(w, shape.top_k)
     del w
     assert dbg["counts"].sum() == T
+    # every token's routing (fp64 router over the whole batch: rmsnorm + x W_R^T only)
+    xn = om.rmsnorm(x, lay.gamma)
+    rt = om.route(xn, lay.w_router, shape.top_k)
+    ok = rt.gap >= 1e-6                                       # R-1
+    np.testing.assert_array_equal(dbg["topk_idx"][ok], rt.idx[ok])
+    m = om.permutation_maps(dbg["topk_idx"], shape.n_experts)
+    np.testing.assert_array_equal(dbg["counts"], m.counts)
+    np.testing.assert_array_equal(dbg["pos"], m.pos)
     sample = np.array([0, 1, 777, 4095, 4096, 6000, 8190, 8191] + list(range(100, 108)))
     r, excl = om.adopt_router(lay, x[sample], dbg["topk_idx"][sample])
     np.testing.assert_array_equal(dbg["topk_idx"][sample], r.idx)
@@ -343,4 +364,26 @@ def test_bench_launch_configuration_graph_replay(name):
     r, _ = om.adopt_router(lay, x[sample], idx.cpu().numpy()[sample])
     sh, ro, _ = om.moe_block(x[sample], lay, router=r)
     assert rel_l2(outs[0].cpu().numpy()[sample], (x[sample].astype(np.float64) + sh) + ro) < TOL
+    ctx.close()
+
+
+def test_debug_finiteness_check():
+    """fsc_set_debug_checks: a non-finite output is reported as FSC_ERR_NONFINITE
+    (SPEC S:29 error class) instead of propagating silently; finite runs pass."""
+    from paper_2511_11505_b200 import FSC_ERR_NONFINITE, FscError
+    shape = synth.CONFIGS["tiny"]
+    T = 32
+    ctx = make_ctx(shape, T)
+    wd = moe_weights_dev(synth.moe_weights(shape, seed=0))
+    x = synth.tokens(shape, T=T)
+    ctx.set_debug_checks(True)
+    xin = dev_f32(x)
+    out = torch.empty_like(xin)
+    ctx.moe_forward_blocking(wd, xin, out)
+    x[3, 5] = np.inf
+    with pytest.raises(FscError) as ei:
+        ctx.moe_forward_blocking(wd, dev_f32(x), out)
+    assert ei.value.code == FSC_ERR_NONFINITE
+    ctx.moe_forward_blocking(wd, xin, out)          # not sticky
+    torch.cuda.synchronize()
     ctx.close()
