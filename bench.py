@@ -357,6 +357,11 @@ def run_gpu(args):
         ctx.moe_forward_blocking_host(wd, xh[0], oh[0], stream=stream.cuda_stream)
     e2e_sync_value = T * 3 / (time.perf_counter() - t0)
 
+    backward = None
+    if args.backward and not allreduce:
+        backward = backward_measure(ctx, shape, wd, x, max(3, min(args.steps, 10)), world, dev, e_loc, args.seed,
+                                    rank)
+
     stack = None
     if args.stack_layers > 0 and shape.tokens % shape.seq_len == 0 and not allreduce:
         stack = stack_measure(ctx, shape, wd, x, args.stack_layers, max(3, min(args.steps, 8)), world, dev,
@@ -447,6 +452,7 @@ def run_gpu(args):
         "exposed_a2a_us_per_layer": (stack or {}).get("exposed_a2a_us_per_layer",
                                                        {"farskip": None, "blocking": None}),
         "stack": stack,
+        "backward": backward,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": T * shape.d * 4 * world,
                 "d2h_bytes_per_step": T * shape.d * 4 * world,
                 "note": "fsc_moe_forward_host_async: every step uploads its pinned fp32 x and downloads its fp32 "
@@ -466,6 +472,49 @@ def run_gpu(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- backward (NEXT-2)
+def backward_measure(ctx, shape, wd, x, steps, world, dev, e_loc, seed, rank):
+    """fsc_moe_backward of the same layer (recompute + gradient all-to-all + dgrad / wgrad
+    GEMMs + router / RMSNorm backward), timed with CUDA events over `steps` calls after a
+    warm-up; FLOPs of its GEMMs: routed 16 R d c (dh, recomputed u|v, dX, dW3, dW1|dW2) +
+    shared 16 T d c_s. Per-phase times from the library's timeline."""
+    import torch
+    T, d, c, cs = shape.tokens, shape.d, shape.ffn, shape.shared_ffn
+    g = torch.from_numpy(np.random.default_rng([seed, rank, 77]).standard_normal((T, d)).astype(np.float32)).to(dev)
+    z = lambda *sh: torch.empty(sh, dtype=torch.float32, device=dev)  # noqa: E731
+    grads = {"dx": z(T, d), "dgamma": z(d), "dw_router": z(shape.n_experts, d), "dw1": z(e_loc, c, d),
+             "dw2": z(e_loc, c, d), "dw3": z(e_loc, d, c)}
+    if cs:
+        grads.update({"dws1": z(cs, d), "dws2": z(cs, d), "dws3": z(d, cs)})
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        ctx.moe_backward(wd, x, g, grads, stream=stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        ctx.moe_backward(wd, x, g, grads, stream=stream.cuda_stream)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = allreduce_max([a.elapsed_time(b) / steps], dev)[0]
+    ctx.set_timing(True)
+    ctx.moe_backward(wd, x, g, grads, stream=stream.cuda_stream)
+    tl = ctx.timeline()
+    ctx.set_timing(False)
+    names = {"router": "recompute_router_maps", "dispatch": "dispatch_xn_and_grad (comm)",
+             "shared1": "shared_backward", "gemm1": "routed_dh_and_swiglu_bwd", "gemm2": "routed_dX",
+             "combine": "grad_combine (comm)", "shared2": "routed_wgrads", "unpermute": "token_router_rmsnorm_bwd",
+             "dispatch_stall": "dispatch_stall", "combine_wait": "combine_wait"}
+    R = T * shape.top_k
+    flop = 16.0 * R * d * c + 16.0 * T * d * cs
+    return {"ms": ms, "tokens_per_s": T * world / (ms * 1e-3), "gemm_flop": flop,
+            "gemm_tflops_over_step": flop / (ms * 1e-3) / 1e12,
+            "phase_ms": {names.get(p, p): du for p, _, _, du in tl},
+            "note": "fsc_moe_backward: activation recomputation of the routing and expert inputs, dgrad + wgrad "
+                    "tcgen05 GEMMs, gradient all-to-all on the comm stream (overlapped with the shared-expert "
+                    "backward and the routed wgrads)"}
 
 
 # ----------------------------------------------------------------------------- stack (FarSkip vs blocking)
@@ -669,6 +718,7 @@ def main():
     ap.add_argument("--comm-ctas", type=int, default=0, help="CTAs of the dispatch / combine kernels (0 = library default)")
     ap.add_argument("--no-live-timing", action="store_true", help="no CUDA events inside the timed graphs")
     ap.add_argument("--stack-layers", type=int, default=4, help="0 disables the FarSkip-vs-blocking stack timing")
+    ap.add_argument("--no-backward", dest="backward", action="store_false", help="skip the backward timing")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -316,9 +316,10 @@ class Context:
         P:215-217). Call before connect()."""
         self._ck(self.lib.fsc_set_ep_mode(self.h, mode))
 
-    def set_router_int8(self, on: bool):
-        """Router on the int8 tensor cores (exact fixed-point planes); E <= 64, d % 128 == 0."""
-        self._ck(self.lib.fsc_set_router_int8(self.h, int(on)))
+    def set_router_int8(self, on):
+        """Router on the int8 tensor cores (exact fixed-point planes; E <= 128, d % 128 == 0):
+        True / False, or None = auto (the default: int8 for E > 64 at prefill sizes)."""
+        self._ck(self.lib.fsc_set_router_int8(self.h, -1 if on is None else int(on)))
 
     def set_fused_unpermute(self, on):
         """Blocking EP = 1: gate-weighted unpermute fused into the down GEMM epilogue

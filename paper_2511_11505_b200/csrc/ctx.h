@@ -31,7 +31,7 @@ struct fsc_ctx {
   int fuse_unpermute = -1;     // blocking EP = 1: unpermute fused into GEMM2 (-1 auto: top-1)
   int dispatch_fp8 = 0;        // FP8 (e4m3, per-128-column scales) dispatch payload, EP > 1 all-to-all
   int ep_mode = 0;             // FSC_EP_ALLTOALL (dispatch / combine) or FSC_EP_ALLREDUCE (replicated tokens)
-  int router_i8 = 0;           // exact int8 tensor-core router (fsc_set_router_int8)
+  int router_i8 = -1;          // exact int8 tensor-core router: 1 on, 0 off, -1 auto (fsc_set_router_int8)
   int gather_a = 0;            // EP = 1: GEMM1 gathers A through src_row (fused permute)
   int combine_mode = 0;        // FSC_COMBINE_STREAM (comm-stream push after GEMM2) or FSC_COMBINE_FUSED
   int blocking_mode = 0;       // fsc_moe_forward_blocking: FSC_BLOCKING_REGULAR_PLUS or FSC_BLOCKING_SERIAL
@@ -128,6 +128,7 @@ struct fsc_ctx {
   int b_dg_ld = 0;
   float* b_dlrow = nullptr;     // fp32 [T * k]             logit gradients per send row
   float* b_rtok = nullptr;      // fp32 [T]                 RMS factors
+  float* b_colpart = nullptr;   // fp32 [T / 64, d]         dgamma partial column sums
   uint16_t* b_gr = nullptr;     // EP = 1: bf16 [T * k, d]  gradient rows (expert-sorted)
   float* b_gate = nullptr;      // EP = 1: fp32 [T * k]     their gates
 };

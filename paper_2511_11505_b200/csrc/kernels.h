@@ -136,13 +136,13 @@ struct RouterLaunch {
   float* w_scaled;       // workspace [E, d]: gamma * W_R
   float* w_sq;           // workspace [E]: ||gamma * W_R[e]||^2
   int rpb = 32;          // tokens per CTA (set by launch_router)
-  // exact int8 tensor-core path (E <= 64, d % 128 == 0); nullptr planes = fp32 SIMT path
+  // exact int8 tensor-core path (E <= 128, d % 128 == 0); nullptr planes = fp32 SIMT path
   int8_t* i8_x;          // workspace [3, T, d]: 7-bit planes of x_t / s_t
-  int8_t* i8_w;          // workspace [3, 64, d]: 7-bit planes of (gamma W_R)_e / s_e
+  int8_t* i8_w;          // workspace [3, 128, d]: 7-bit planes of (gamma W_R)_e / s_e
   float* i8_tok;         // workspace [3, T]: s_t, ||x_t / s_t||_1, (float) r_t
   double* i8_r;          // workspace [T]: r_t (fp64)
-  float* i8_exp;         // workspace [3, 64]: s_e and the two per-expert error-bound coefficients
-  int* i8_part;          // workspace [kI8SplitRows, 256]: split-d int32 partial sums
+  float* i8_exp;         // workspace [3, 128]: s_e and the two per-expert error-bound coefficients
+  int* i8_part;          // workspace [kI8SplitRows * 512]: split-d int32 partial sums, [split][col][T]
   int* i8_cnt;           // workspace [ceil(T/128)]: split arrival tickets, zero between calls
 };
 constexpr int kI8SplitRows = 148 * 128;

@@ -80,14 +80,15 @@ __global__ void __launch_bounds__(256) permute_grad_kernel(const float* __restri
   }
 }
 
-// Per token t (one CTA of 256 threads):
+// Per token t (one WARP per token, 8 per CTA; lane l owns columns 8l + 256 m):
 //   dg_j   = gate gradient of copy j (dgs[pos] at EP > 1, sum of dg_part[pos] at EP = 1)
 //   dl_j   = g_j (dg_j - sum_i g_i dg_i)                (softmax over the selected logits)
-//   dxn    = dxn_shared[t] + sum_j dX[pos[t,j]] + sum_j dl_j W_R[e_j]
+//   dxn    = dxn_shared[t] + sum_j (dX[pos[t,j]] + dl_j W_R[e_j])   (slot order, fp32)
 //   r      = (mean x^2 + eps)^-1/2;  q = dxn gamma;  dx = G + r q - x r^3 (q . x) / d
-//   zg[t]  = dxn x r  (dgamma summands, summed over tokens by colsum_kernel)
-//   dl_row[pos[t,j]] = dl_j, r_tok[t] = r   (for dW_R)
-template <int K_MAX>
+//   zg[t]  = dxn x r  (dgamma summands, summed over tokens by the colsum kernels)
+// dxn is staged in place in dxn_zg (each lane re-reads only what it wrote) between the
+// pass that forms it (and reduces sum x^2, q . x over the warp) and the pass that needs r.
+// Also dl_row[pos[t,j]] = dl_j and r_tok[t] = r (for dW_R).
 __global__ void __launch_bounds__(256) token_bwd_kernel(const float* __restrict__ x, const float* __restrict__ G,
                                                         const float* __restrict__ gamma, const float* __restrict__ w_router,
                                                         const int* __restrict__ idx, const int* __restrict__ pos,
@@ -96,117 +97,152 @@ __global__ void __launch_bounds__(256) token_bwd_kernel(const float* __restrict_
                                                         int dg_n, int dg_ld, float* dxn_zg, float* __restrict__ dx,
                                                         float* __restrict__ dl_row, float* __restrict__ r_tok, int T,
                                                         int d, int k, float eps) {
-  __shared__ float s_red[8][2];
-  __shared__ float s_dl[K_MAX];
-  __shared__ int s_e[K_MAX], s_q[K_MAX];
-  __shared__ float s_r, s_qx;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (long t = blockIdx.x; t < T; t += gridDim.x) {
-    const float* xt = x + t * d;
-    if (tid < k) {
-      const int q = __ldg(pos + t * k + tid);
-      s_q[tid] = q;
-      s_e[tid] = __ldg(idx + t * k + tid);
-      float g = 0.f;
-      if (dgs) {
-        g = __ldcg(dgs + q);
-      } else {
-        for (int i = 0; i < dg_n; ++i) g += __ldg(dg_part + (long)q * dg_ld + i);
-      }
-      s_dl[tid] = g;   // dg_j for now
+  const int lane = threadIdx.x & 31;
+  const long t = (long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= T) return;
+  // slot j lives in lane j (k <= 8)
+  int qj = 0, ej = 0;
+  float gj = 0.f, dgj = 0.f;
+  if (lane < k) {
+    qj = __ldg(pos + t * k + lane);
+    ej = __ldg(idx + t * k + lane);
+    gj = __ldg(topk_w + t * k + lane);
+    if (dgs) {
+      dgj = __ldcg(dgs + qj);
+    } else {
+      for (int i = 0; i < dg_n; ++i) dgj += __ldg(dg_part + (long)qj * dg_ld + i);
     }
-    // sum x^2 (r) in fp32, fixed reduction order
-    float ss = 0.f;
-    for (int i = tid; i < d; i += 256) ss = fmaf(xt[i], xt[i], ss);
-    __syncthreads();
-    if (tid == 0) {
-      float gd = 0.f;
-      for (int j = 0; j < k; ++j) gd = fmaf(__ldg(topk_w + t * k + j), s_dl[j], gd);
-      for (int j = 0; j < k; ++j) {
-        const float g = __ldg(topk_w + t * k + j);
-        s_dl[j] = g * (s_dl[j] - gd);
-      }
-    }
-    // block reduction of ss
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if (lane == 0) s_red[w][0] = ss;
-    __syncthreads();
-    if (tid == 0) {
-      float a = 0.f;
-      for (int i = 0; i < 8; ++i) a += s_red[i][0];
-      s_r = rsqrtf(a / (float)d + eps);
-    }
-    __syncthreads();
-    const float r = s_r;
-    // dxn (kept in registers per thread: d / 256 <= 32 columns), q . x
-    float qx = 0.f;
-    float dxn_v[32];
-#pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int i = tid + 256 * u;
-      dxn_v[u] = 0.f;
-      if (i < d) {
-        float v = dxn_zg[t * d + i];   // shared-expert part (fp32)
-        for (int j = 0; j < k; ++j) {
-          const uint16_t b = __ldcg(dxr + (long)s_q[j] * d + i);
-          v += __uint_as_float((uint32_t)b << 16);
-          v = fmaf(s_dl[j], __ldg(w_router + (long)s_e[j] * d + i), v);
-        }
-        dxn_v[u] = v;
-        qx = fmaf(v * __ldg(gamma + i), xt[i], qx);
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) qx += __shfl_xor_sync(0xffffffffu, qx, o);
-    if (lane == 0) s_red[w][1] = qx;
-    __syncthreads();
-    if (tid == 0) {
-      float a = 0.f;
-      for (int i = 0; i < 8; ++i) a += s_red[i][1];
-      s_qx = a;
-    }
-    __syncthreads();
-    const float c3 = r * r * r * s_qx / (float)d;
-#pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int i = tid + 256 * u;
-      if (i < d) {
-        const float xv = xt[i];
-        const float qv = dxn_v[u] * __ldg(gamma + i);
-        dx[t * d + i] = __ldg(G + t * d + i) + r * qv - xv * c3;
-        dxn_zg[t * d + i] = dxn_v[u] * xv * r;
-      }
-    }
-    if (tid < k) dl_row[s_q[tid]] = s_dl[tid];
-    if (tid == 0) r_tok[t] = r;
-    __syncthreads();
   }
+  float gd = gj * dgj;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) gd += __shfl_xor_sync(0xffffffffu, gd, o);
+  const float dlj = gj * (dgj - gd);
+  int qs[8], es[8];
+  float dl[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {                // (full-warp shuffles: before the column loop)
+    qs[j] = __shfl_sync(0xffffffffu, qj, j);
+    es[j] = __shfl_sync(0xffffffffu, ej, j);
+    dl[j] = __shfl_sync(0xffffffffu, dlj, j);
+  }
+  const float* xt = x + t * d;
+  float* zt = dxn_zg + t * d;
+  float ss = 0.f, qx = 0.f;
+  for (int c = 8 * lane; c < d; c += 256) {
+    const float4 x0 = __ldg(reinterpret_cast<const float4*>(xt + c)), x1 = __ldg(reinterpret_cast<const float4*>(xt + c + 4));
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c)), g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
+    float4 a0 = *reinterpret_cast<const float4*>(zt + c), a1 = *reinterpret_cast<const float4*>(zt + c + 4);
+    float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    uint4 yv[8];
+    float4 w0[8], w1[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {              // every slot's loads in flight together
+      const int q = qs[j], e = es[j];
+      if (j < k) {
+        yv[j] = __ldcg(reinterpret_cast<const uint4*>(dxr + (long)q * d + c));
+        w0[j] = __ldg(reinterpret_cast<const float4*>(w_router + (long)e * d + c));
+        w1[j] = __ldg(reinterpret_cast<const float4*>(w_router + (long)e * d + c + 4));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < k) {
+        const float wv[8] = {w0[j].x, w0[j].y, w0[j].z, w0[j].w, w1[j].x, w1[j].y, w1[j].z, w1[j].w};
+        const uint32_t yw[4] = {yv[j].x, yv[j].y, yv[j].z, yv[j].w};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v[u] += (u & 1) ? bf16hi(yw[u >> 1]) : bf16lo(yw[u >> 1]);
+          v[u] = fmaf(dl[j], wv[u], v[u]);
+        }
+      }
+    }
+    const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      ss = fmaf(xv[u], xv[u], ss);
+      qx = fmaf(v[u] * gv[u], xv[u], qx);
+    }
+    *reinterpret_cast<float4*>(zt + c) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(zt + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    qx += __shfl_xor_sync(0xffffffffu, qx, o);
+  }
+  const float r = rsqrtf(ss / (float)d + eps);
+  const float c3 = r * r * r * qx / (float)d;
+  const float* gt = G + t * d;
+  float* dxt = dx + t * d;
+  for (int c = 8 * lane; c < d; c += 256) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float4 a = *reinterpret_cast<const float4*>(zt + c + 4 * h);
+      const float4 xx = __ldg(reinterpret_cast<const float4*>(xt + c + 4 * h));
+      const float4 gg = __ldg(reinterpret_cast<const float4*>(gamma + c + 4 * h));
+      const float4 G4 = __ldg(reinterpret_cast<const float4*>(gt + c + 4 * h));
+      *reinterpret_cast<float4*>(dxt + c + 4 * h) =
+          make_float4(G4.x + r * a.x * gg.x - xx.x * c3, G4.y + r * a.y * gg.y - xx.y * c3,
+                      G4.z + r * a.z * gg.z - xx.z * c3, G4.w + r * a.w * gg.w - xx.w * c3);
+      *reinterpret_cast<float4*>(zt + c + 4 * h) =
+          make_float4(a.x * xx.x * r, a.y * xx.y * r, a.z * xx.z * r, a.w * xx.w * r);
+    }
+  }
+  if (lane < k) dl_row[qj] = dlj;
+  if (lane == 0) r_tok[t] = r;
 }
 
-// dgamma[i] = sum_t zg[t, i] (token order; 256 columns per CTA, 4 row phases summed in order)
-__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ zg, float* __restrict__ out, int T, int d) {
+// dgamma[i] = sum_t zg[t, i]: partial sums over 64-token chunks (token order), then the
+// chunks in order - deterministic and spread over the GPU
+constexpr int kColChunk = 64;
+__global__ void __launch_bounds__(256) colsum_part_kernel(const float* __restrict__ zg, float* __restrict__ part, int T,
+                                                          int d) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  const int t0 = blockIdx.y * kColChunk, t1 = min(T, t0 + kColChunk);
+  if (i >= d) return;
+  float a = 0.f;
+#pragma unroll 8
+  for (int t = t0; t < t1; ++t) a += __ldcg(zg + (long)t * d + i);
+  part[(long)blockIdx.y * d + i] = a;
+}
+__global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restrict__ part, float* __restrict__ out,
+                                                           int nchunk, int d) {
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= d) return;
   float a = 0.f;
-  for (int t = 0; t < T; ++t) a += zg[(long)t * d + i];
+  for (int c = 0; c < nchunk; ++c) a += part[(long)c * d + i];
   out[i] = a;
 }
 
 // dW_R[e, i] = sum over the copies q of expert e (send order) of dl_row[q] * xn32[src_row[q], i],
-// xn32 = x r gamma in fp32
+// xn32 = x r gamma in fp32 (gamma applied once at the end). Copies are staged 256 at a time
+// in shared memory (token, dl r), so every thread's x loads are independent (8 in flight).
 __global__ void __launch_bounds__(256) dwr_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
                                                   const float* __restrict__ r_tok, const int* __restrict__ offsets,
                                                   const int* __restrict__ src_row, const float* __restrict__ dl_row,
                                                   float* __restrict__ dwr, int d) {
+  __shared__ int s_t[256];
+  __shared__ float s_c[256];
   const int e = blockIdx.y;
   const int i = blockIdx.x * 256 + threadIdx.x;
-  if (i >= d) return;
   const int q0 = offsets[e], q1 = offsets[e + 1];
   float a = 0.f;
-  for (int q = q0; q < q1; ++q) {
-    const int t = __ldg(src_row + q);
-    a = fmaf(__ldg(dl_row + q), x[(long)t * d + i] * __ldg(r_tok + t), a);
+  for (int b = q0; b < q1; b += 256) {
+    const int n = min(256, q1 - b);
+    __syncthreads();
+    if ((int)threadIdx.x < n) {
+      const int t = __ldg(src_row + b + threadIdx.x);
+      s_t[threadIdx.x] = t;
+      s_c[threadIdx.x] = __ldg(dl_row + b + threadIdx.x) * __ldg(r_tok + t);
+    }
+    __syncthreads();
+    if (i < d) {
+#pragma unroll 8
+      for (int u = 0; u < n; ++u) a = fmaf(s_c[u], __ldg(x + (long)s_t[u] * d + i), a);
+    }
   }
-  dwr[(long)e * d + i] = a * __ldg(gamma + i);
+  if (i < d) dwr[(long)e * d + i] = a * __ldg(gamma + i);
 }
 
 }  // namespace
@@ -234,6 +270,7 @@ int ensure_bwd_workspace(fsc_ctx* ctx) {
   BCK(balloc(&ctx->b_dgpart, rows * ctx->b_dg_ld));
   BCK(balloc(&ctx->b_dlrow, T * k));
   BCK(balloc(&ctx->b_rtok, T));
+  BCK(balloc(&ctx->b_colpart, ((T + 63) / 64) * d));
   if (ctx->ep == 1) {
     BCK(balloc(&ctx->b_gr, T * k * d));
     BCK(balloc(&ctx->b_gate, T * k));
@@ -266,6 +303,7 @@ extern "C" int fsc_moe_backward(fsc_ctx* ctx, const fsc_moe_weights* w, int T, c
   const fsc_moe_config& c = ctx->cfg;
   const int d = c.d, E = c.n_experts, k = c.top_k, cf = c.ffn, cs = c.shared_ffn;
   BREQ(cf % 64 == 0 && cs % 64 == 0, FSC_ERR_CONFIG, "backward: ffn widths must be multiples of 64");
+  BREQ(k <= 8, FSC_ERR_CONFIG, "backward: top_k <= 8");
   BCK(cudaSetDevice(ctx->device));
   if (T == 0) return FSC_OK;
   BRC(ensure_bwd_workspace(ctx));
@@ -277,7 +315,7 @@ extern "C" int fsc_moe_backward(fsc_ctx* ctx, const fsc_moe_weights* w, int T, c
   BCK(fsc_phase_begin(ctx, PH_ROUTER, s));
   RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
                   nullptr, nullptr, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, 32,
-                  nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+                  nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // (fp32 SIMT router)
   BCK(launch_router(rl, s));
   PermLaunch pl{ctx->topk_idx, T, k, E, ctx->hist, ctx->base, ctx->counts, ctx->offsets, ctx->pos, ctx->src_row};
   BCK(launch_perm_maps(pl, s));
@@ -407,13 +445,15 @@ extern "C" int fsc_moe_backward(fsc_ctx* ctx, const fsc_moe_weights* w, int T, c
   // ---- per token: router backward, sum of the copies, RMSNorm backward; dgamma; dW_R
   BCK(fsc_phase_begin(ctx, PH_UNPERMUTE, s));
   ++g_launches;
-  token_bwd_kernel<8><<<std::min(T, 8 * kNumSMs), 256, 0, s>>>(
-      x_in, grad_out, w->gamma, w->w_router, ctx->topk_idx, ctx->pos, ctx->topk_w, dxr, dgs, ctx->b_dgpart, dg_n,
-      ctx->b_dg_ld, ctx->tmp, gr->dx, ctx->b_dlrow, ctx->b_rtok, T, d, k, c.rms_eps);
+  token_bwd_kernel<<<(T + 7) / 8, 256, 0, s>>>(x_in, grad_out, w->gamma, w->w_router, ctx->topk_idx, ctx->pos,
+                                               ctx->topk_w, dxr, dgs, ctx->b_dgpart, dg_n, ctx->b_dg_ld, ctx->tmp,
+                                               gr->dx, ctx->b_dlrow, ctx->b_rtok, T, d, k, c.rms_eps);
   BCK(cudaGetLastError());
   if (gr->dgamma) {
-    ++g_launches;
-    colsum_kernel<<<(d + 255) / 256, 256, 0, s>>>(ctx->tmp, gr->dgamma, T, d);
+    const int nchunk = (T + kColChunk - 1) / kColChunk;
+    g_launches += 2;
+    colsum_part_kernel<<<dim3((d + 255) / 256, nchunk), 256, 0, s>>>(ctx->tmp, ctx->b_colpart, T, d);
+    colsum_final_kernel<<<(d + 255) / 256, 256, 0, s>>>(ctx->b_colpart, gr->dgamma, nchunk, d);
     BCK(cudaGetLastError());
   }
   if (gr->dw_router) {

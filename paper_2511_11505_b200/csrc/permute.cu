@@ -152,7 +152,17 @@ __global__ void __launch_bounds__(256) permute_rows_kernel(const uint4* __restri
   const long src = src_row[r];
   const uint4* a = xn + src * dv;
   uint4* b = xs + r * dv;
-  for (int i = lane; i < dv; i += 32) b[i] = a[i];
+  // 8 loads in flight per lane before the stores (one row of d = 2048 per warp round):
+  // the copy is bound by the bytes in flight per SM, not by instruction issue
+  for (int i0 = lane; i0 < dv; i0 += 256) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + 32 * u < dv) v[u] = __ldg(a + i0 + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + 32 * u < dv) b[i0 + 32 * u] = v[u];
+  }
 }
 
 cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t* xs, int R, int d,
@@ -176,18 +186,31 @@ __global__ void __launch_bounds__(256) unpermute_kernel(const uint4* __restrict_
     float acc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-    for (int j = 0; j < k; ++j) {
-      const long p = pos[t * k + j];
-      const float g = w[t * k + j];
-      const uint4 v = y[p * dv + c];
-      acc[0] = fmaf(g, bf16lo(v.x), acc[0]);
-      acc[1] = fmaf(g, bf16hi(v.x), acc[1]);
-      acc[2] = fmaf(g, bf16lo(v.y), acc[2]);
-      acc[3] = fmaf(g, bf16hi(v.y), acc[3]);
-      acc[4] = fmaf(g, bf16lo(v.z), acc[4]);
-      acc[5] = fmaf(g, bf16hi(v.z), acc[5]);
-      acc[6] = fmaf(g, bf16lo(v.w), acc[6]);
-      acc[7] = fmaf(g, bf16hi(v.w), acc[7]);
+    // up to 8 slots: every copy's row load in flight at once, then the fp32 sum in slot order
+    for (int j0 = 0; j0 < k; j0 += 8) {
+      uint4 v[8];
+      float g[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (j0 + u < k) {
+          const long p = __ldg(pos + t * k + j0 + u);
+          g[u] = __ldg(w + t * k + j0 + u);
+          v[u] = y[p * dv + c];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (j0 + u < k) {
+          acc[0] = fmaf(g[u], bf16lo(v[u].x), acc[0]);
+          acc[1] = fmaf(g[u], bf16hi(v[u].x), acc[1]);
+          acc[2] = fmaf(g[u], bf16lo(v[u].y), acc[2]);
+          acc[3] = fmaf(g[u], bf16hi(v[u].y), acc[3]);
+          acc[4] = fmaf(g[u], bf16lo(v[u].z), acc[4]);
+          acc[5] = fmaf(g[u], bf16hi(v[u].z), acc[5]);
+          acc[6] = fmaf(g[u], bf16lo(v[u].w), acc[6]);
+          acc[7] = fmaf(g[u], bf16hi(v[u].w), acc[7]);
+        }
+      }
     }
     const float4* rr = reinterpret_cast<const float4*>(resid + t * (long)dv * 8 + c * 8);
     float4* oo = reinterpret_cast<float4*>(out + t * (long)dv * 8 + c * 8);

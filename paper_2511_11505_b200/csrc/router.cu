@@ -25,6 +25,7 @@
 // workspace and router_finish_kernel sums them in a fixed order and selects.
 #include <cudaTypedefs.h>
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -341,8 +342,15 @@ FSC_DEVINL void write_xn(const RouterLaunch& L, long t0, int rows, const float* 
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g__));                          \
     reinterpret_cast<unsigned long long*>(L.logits)[blockIdx.x * 8 + (kk)] = g__;    \
   }
+#define I8STAMP(kk)                                                                                  \
+  if (threadIdx.x == 64) {                                                                           \
+    unsigned long long g__;                                                                          \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g__));                                          \
+    reinterpret_cast<unsigned long long*>(L.logits)[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (kk)] = g__; \
+  }
 #else
 #define RSTAMP(kk)
+#define I8STAMP(kk)
 #endif
 
 // Band refinement of the block's flagged tokens, by the whole CTA (after the
@@ -565,9 +573,10 @@ __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
     }
     cp_async_commit();
   };
+  auto chunk = [&](int i) { return ch0 + i; };
 #pragma unroll
   for (int i = 0; i < NS - 1; ++i) {
-    if (i < nch) issue_chunk((ch0 + i) * DC, stage0 + i * BUF);
+    if (i < nch) issue_chunk(chunk(i) * DC, stage0 + i * BUF);
     else cp_async_commit();
   }
   if (nsplit == 1)
@@ -586,7 +595,7 @@ __global__ void __launch_bounds__(256, 2) router_kernel(RouterLaunch L) {
     const float* buf = stage0 + (it % NS) * BUF;
     cp_async_wait<NS - 2>();
     __syncthreads();
-    if (it + NS - 1 < nch) issue_chunk((ch0 + it + NS - 1) * DC, stage0 + ((it + NS - 1) % NS) * BUF);
+    if (it + NS - 1 < nch) issue_chunk(chunk(it + NS - 1) * DC, stage0 + ((it + NS - 1) % NS) * BUF);
     else cp_async_commit();
     {
       const float4 p = *reinterpret_cast<const float4*>(buf + srow * LDS + scol);
@@ -709,7 +718,7 @@ __global__ void __launch_bounds__(256) router_finish_kernel(RouterLaunch L, int 
 }
 
 // ============================================================================
-// Exact int8 tensor-core router (E <= 64, d % 128 == 0, k <= 8).
+// Exact int8 tensor-core router (E <= 128, d % 128 == 0, k <= 8).
 //
 // Fixed point, exactly: with s_t, s_e powers of two (|x_t| / s_t < 1, |w_e| / s_e < 1,
 // w_e = gamma (.) W_R[e] formed exactly in fp64), truncating base-2^7 digits give
@@ -718,26 +727,31 @@ __global__ void __launch_bounds__(256) router_finish_kernel(RouterLaunch L, int 
 //   l_te = r_t s_t s_e ( sum_{i+j<=3} 2^{-7(i+j+2)} <a_i, b_j>  + err ),
 //   |err| <= 2^-21 (||x_t/s_t||_1 + ||w_e/s_e||_1 + 2d 2^-21) + d 2^-42 + 2^-42 127^2 d
 // where every <a_i, b_j> is an exact int32 tensor-core sum (|.| <= 127^2 d), pairs with
-// equal i + j share one TMEM accumulator (4 x 64 columns) and the one dropped pair
+// equal i + j share one TMEM accumulator (4 x EP columns) and the one dropped pair
 // (2, 2) is bounded by the last term. That bound (~2e-4 of the logit scale, vs ~7e-4
 // for the fp32 SIMT chain) decides the band exactly as in the SIMT path; flagged
 // tokens go through the same fp64 refine_block. One CTA = 128 tokens (TMEM lanes) x
-// 64 padded experts x a 1/nsplit slice of d: warp 0 TMA (3-stage ring of 3 + 3
+// EP (64 or 128) padded experts x a 1/nsplit slice of d: warp 0 TMA (ring of 3 + 3
 // planes), warp 1 MMA (8 plane pairs x 4 K-steps of 32 per 128-wide k-block), warps
 // 2-5 epilogue (one thread per token). nsplit > 1 (to fill the SMs): each CTA writes
-// its int32 partial sums; the last CTA of a token block (ticket) adds them - integer
-// sums, so exact and order-free - then combines in fp64, selects and refines.
+// its int32 partial sums, column-major [split][column][token] so that a warp's stores
+// and loads are 128-byte rows; the last CTA of a token block (ticket) adds them -
+// integer sums, so exact and order-free - then combines in fp64, selects and refines.
 namespace {
-constexpr int I8_BM = 128, I8_EP = 64, I8_BK = 128, I8_NP = 3, I8_NACC = 2 * I8_NP - 2;   // 4 accumulators
+constexpr int I8_BM = 128, I8_BK = 128, I8_NP = 3, I8_NACC = 2 * I8_NP - 2;   // 4 accumulators
 constexpr int I8_A_TILE = I8_BM * I8_BK;                    // 16 KB
-constexpr int I8_B_TILE = I8_EP * I8_BK;                    // 8 KB
-constexpr int I8_STAGE = I8_NP * (I8_A_TILE + I8_B_TILE);   // 72 KB
-constexpr int I8_STAGES = 3;
-constexpr int I8_LGS = I8_EP + 4;
 constexpr int I8_THREADS = 192;
-constexpr int I8_SMEM = 1024 + I8_STAGES * I8_STAGE + 256;
-constexpr int I8_ACC_COLS = I8_NACC * I8_EP;                // 256 int32 per token
 constexpr int I8_MAX_SPLIT = 8;
+template <int EP>
+struct I8Cfg {
+  static constexpr int B_TILE = EP * I8_BK;                 // 8 / 16 KB
+  static constexpr int STAGE = I8_NP * (I8_A_TILE + B_TILE); // 72 / 96 KB
+  static constexpr int STAGES = EP == 64 ? 3 : 2;
+  static constexpr int LGS = EP + 4;
+  static constexpr int ACC_COLS = I8_NACC * EP;             // 256 / 512 int32 per token
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static_assert(I8_BM * LGS * 4 <= STAGES * STAGE, "logits must fit in the stages");
+};
 
 template <typename F>
 FSC_DEVINL void split3(F v, int8_t (&q)[I8_NP]) {   // |v| < 1: truncating base-128 digits, exact
@@ -749,9 +763,29 @@ FSC_DEVINL void split3(F v, int8_t (&q)[I8_NP]) {   // |v| < 1: truncating base-
     v -= t;
   }
 }
+
+// xn + planes of 4 consecutive columns of one token (c = float4 index)
+FSC_DEVINL float quant_store4(const RouterLaunch& L, long t, int c, float4 v, float4 g, float rf, float inv) {
+  uint2* xo = reinterpret_cast<uint2*>(L.xn + t * L.d);
+  xo[c] = make_uint2(pack_bf16x2(v.x * g.x * rf, v.y * g.y * rf), pack_bf16x2(v.z * g.z * rf, v.w * g.w * rf));
+  int8_t q0[I8_NP], q1[I8_NP], q2[I8_NP], q3[I8_NP];
+  split3(v.x * inv, q0);
+  split3(v.y * inv, q1);
+  split3(v.z * inv, q2);
+  split3(v.w * inv, q3);
+#pragma unroll
+  for (int i = 0; i < I8_NP; ++i) {
+    const uint32_t pk = (uint32_t)(uint8_t)q0[i] | ((uint32_t)(uint8_t)q1[i] << 8) |
+                        ((uint32_t)(uint8_t)q2[i] << 16) | ((uint32_t)(uint8_t)q3[i] << 24);
+    reinterpret_cast<uint32_t*>(L.i8_x + ((long)i * L.T + t) * L.d)[c] = pk;
+  }
+  return (fabsf(v.x) + fabsf(v.y) + fabsf(v.z) + fabsf(v.w)) * inv;
+}
 }  // namespace
 
 // Per token (one warp): r_t, s_t, ||x_t/s_t||_1, xn = bf16(x gamma r) and the planes of x_t/s_t.
+// NV > 0: the row stays in registers (d = 128 NV, one read of x); NV = 0: two passes over x.
+template <int NV>
 __global__ void __launch_bounds__(256) router_i8_quant_x_kernel(RouterLaunch L) {
   const int lane = threadIdx.x & 31;
   const long t = (long)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -761,14 +795,26 @@ __global__ void __launch_bounds__(256) router_i8_quant_x_kernel(RouterLaunch L) 
   const float4* g4 = reinterpret_cast<const float4*>(L.gamma);
   double ss = 0.0;
   float mx = 0.f;
-  for (int c0 = lane; c0 < dv; c0 += 128) {           // 4 float4 per lane in flight
-    float4 v[4];
+  float4 row[NV > 0 ? NV : 1];
+  if (NV > 0) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = c0 + 32 * u < dv ? x4[c0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < NV; ++u) row[u] = __ldcs(x4 + lane + 32 * u);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      ss += ((double)v[u].x * v[u].x + (double)v[u].y * v[u].y) + ((double)v[u].z * v[u].z + (double)v[u].w * v[u].w);
-      mx = fmaxf(fmaxf(mx, fmaxf(fabsf(v[u].x), fabsf(v[u].y))), fmaxf(fabsf(v[u].z), fabsf(v[u].w)));
+    for (int u = 0; u < NV; ++u) {
+      const float4 v = row[u];
+      ss += ((double)v.x * v.x + (double)v.y * v.y) + ((double)v.z * v.z + (double)v.w * v.w);
+      mx = fmaxf(fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
+    }
+  } else {
+    for (int c0 = lane; c0 < dv; c0 += 128) {           // 4 float4 per lane in flight
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = c0 + 32 * u < dv ? x4[c0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ss += ((double)v[u].x * v[u].x + (double)v[u].y * v[u].y) + ((double)v[u].z * v[u].z + (double)v[u].w * v[u].w);
+        mx = fmaxf(fmaxf(mx, fmaxf(fabsf(v[u].x), fabsf(v[u].y))), fmaxf(fabsf(v[u].z), fabsf(v[u].w)));
+      }
     }
   }
   ss = warp_sum_f64(ss);
@@ -780,32 +826,23 @@ __global__ void __launch_bounds__(256) router_i8_quant_x_kernel(RouterLaunch L) 
   const float st = mx > 0.f ? ldexpf(1.f, ex) : 1.f;  // |x| / st < 1
   const float inv = 1.f / st;                        // exact (power of two)
   float l1 = 0.f;
-  uint2* xo = reinterpret_cast<uint2*>(L.xn + t * d);
-  for (int c0 = lane; c0 < dv; c0 += 128) {
-    float4 v[4], g[4];
+  if (NV > 0) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const bool ok = c0 + 32 * u < dv;
-      v[u] = ok ? x4[c0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
-      g[u] = ok ? g4[c0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int u = 0; u < NV; ++u) l1 += quant_store4(L, t, lane + 32 * u, row[u], __ldg(g4 + lane + 32 * u), rf, inv);
+  } else {
+    for (int c0 = lane; c0 < dv; c0 += 128) {
+      float4 v[4], g[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + 32 * u;
-      if (c >= dv) break;
-      xo[c] = make_uint2(pack_bf16x2(v[u].x * g[u].x * rf, v[u].y * g[u].y * rf),
-                         pack_bf16x2(v[u].z * g[u].z * rf, v[u].w * g[u].w * rf));
-      int8_t q0[I8_NP], q1[I8_NP], q2[I8_NP], q3[I8_NP];
-      split3(v[u].x * inv, q0);
-      split3(v[u].y * inv, q1);
-      split3(v[u].z * inv, q2);
-      split3(v[u].w * inv, q3);
-      l1 += (fabsf(v[u].x) + fabsf(v[u].y) + fabsf(v[u].z) + fabsf(v[u].w)) * inv;
+      for (int u = 0; u < 4; ++u) {
+        const bool ok = c0 + 32 * u < dv;
+        v[u] = ok ? x4[c0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+        g[u] = ok ? g4[c0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-      for (int i = 0; i < I8_NP; ++i) {
-        const uint32_t pk = (uint32_t)(uint8_t)q0[i] | ((uint32_t)(uint8_t)q1[i] << 8) |
-                            ((uint32_t)(uint8_t)q2[i] << 16) | ((uint32_t)(uint8_t)q3[i] << 24);
-        reinterpret_cast<uint32_t*>(L.i8_x + ((long)i * L.T + t) * d)[c] = pk;
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 32 * u;
+        if (c >= dv) break;
+        l1 += quant_store4(L, t, c, v[u], g[u], rf, inv);
       }
     }
   }
@@ -820,7 +857,7 @@ __global__ void __launch_bounds__(256) router_i8_quant_x_kernel(RouterLaunch L) 
 
 // Per padded expert (one CTA): w = gamma (.) W_R[e] exactly in fp64, s_e, the planes of
 // w / s_e and the per-expert error-bound coefficients; zero planes for e >= E.
-__global__ void __launch_bounds__(256) router_i8_quant_w_kernel(RouterLaunch L) {
+__global__ void __launch_bounds__(256) router_i8_quant_w_kernel(RouterLaunch L, int EP) {
   __shared__ double red_l1[8];
   __shared__ float red_mx[8];
   const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -850,7 +887,7 @@ __global__ void __launch_bounds__(256) router_i8_quant_w_kernel(RouterLaunch L) 
       l1 += fabs(v);
     }
 #pragma unroll
-    for (int j = 0; j < I8_NP; ++j) L.i8_w[((long)j * I8_EP + e) * d + c] = q[j];
+    for (int j = 0; j < I8_NP; ++j) L.i8_w[((long)j * EP + e) * d + c] = q[j];
   }
   l1 = warp_sum_f64(l1);
   if (lane == 0) red_l1[warp] = l1;
@@ -860,25 +897,27 @@ __global__ void __launch_bounds__(256) router_i8_quant_w_kernel(RouterLaunch L) 
     for (int w = 0; w < 8; ++w) tot += red_l1[w];
     const double u21 = ldexp(1.0, -21), u42 = ldexp(1.0, -42);
     L.i8_exp[e] = (float)se;
-    L.i8_exp[I8_EP + e] = e < L.E ? (float)(se * u21 * 1.0001) : 0.f;
-    L.i8_exp[2 * I8_EP + e] =
+    L.i8_exp[EP + e] = e < L.E ? (float)(se * u21 * 1.0001) : 0.f;
+    L.i8_exp[2 * EP + e] =
         e < L.E ? (float)(se * (u21 * (tot * 1.0001 + 2.0 * d * u21) + d * u42 + u42 * 127.0 * 127.0 * d) * 1.0001)
                 : 0.f;
   }
 }
 
+template <int EP>
 __global__ void __launch_bounds__(I8_THREADS, 1)
     router_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, RouterLaunch L) {
+  using C = I8Cfg<EP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                        // [stage][plane][128][128]
-  uint8_t* sB = smem + I8_STAGES * I8_NP * I8_A_TILE;        // [stage][plane][64][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + I8_STAGES * I8_STAGE);
-  uint64_t* empty = full + I8_STAGES;
-  uint64_t* tfull = empty + I8_STAGES;
+  uint8_t* sB = smem + C::STAGES * I8_NP * I8_A_TILE;        // [stage][plane][EP][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tfull + 1);
   int* s_last = reinterpret_cast<int*>(s_tmem + 1);
-  float* lg = reinterpret_cast<float*>(smem);                // [128][I8_LGS] after the MMAs (stages free)
+  float* lg = reinterpret_cast<float*>(smem);                // [128][LGS] after the MMAs (stages free)
   __shared__ RefineSmemT<I8_BM> rs;
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   const int blk = blockIdx.x, nsplit = gridDim.y, split = blockIdx.y;
@@ -890,39 +929,40 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int st = 0; st < I8_STAGES; ++st) {
+    for (int st = 0; st < C::STAGES; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], 1);
     }
     mbar_init(tfull, 1);
     fence_barrier_init();
   } else if (warp == 1) {
-    tmem_alloc<I8_ACC_COLS>(s_tmem);
+    tmem_alloc<C::ACC_COLS>(s_tmem);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+  I8STAMP(0);
   if (warp == 0) {
     if (elect_one()) {                                     // TMA producer
       int st = 0;
       uint32_t ph = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&full[st], I8_STAGE);
+        mbar_arrive_expect_tx(&full[st], C::STAGE);
 #pragma unroll
         for (int i = 0; i < I8_NP; ++i)
           tma_load_2d(sA + (st * I8_NP + i) * I8_A_TILE, &tmA, &full[st], kb * I8_BK, (int)(i * L.T + t0),
                       kEvictNormal);
 #pragma unroll
         for (int j = 0; j < I8_NP; ++j)
-          tma_load_2d(sB + (st * I8_NP + j) * I8_B_TILE, &tmB, &full[st], kb * I8_BK, j * I8_EP, kEvictLast);
-        if (++st == I8_STAGES) { st = 0; ph ^= 1; }
+          tma_load_2d(sB + (st * I8_NP + j) * C::B_TILE, &tmB, &full[st], kb * I8_BK, j * EP, kEvictLast);
+        if (++st == C::STAGES) { st = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
     if (elect_one()) {                                     // MMA issuer
-      const uint32_t idesc = idesc_s8_s32(I8_BM, I8_EP);
+      const uint32_t idesc = idesc_s8_s32(I8_BM, EP);
       int st = 0;
       uint32_t ph = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -935,32 +975,33 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
           for (int j = 0; j < I8_NP; ++j) {
             if (i + j >= I8_NACC) continue;               // the dropped pair (2, 2)
             const uint32_t a = smem_u32(sA + (st * I8_NP + i) * I8_A_TILE);
-            const uint32_t b = smem_u32(sB + (st * I8_NP + j) * I8_B_TILE);
+            const uint32_t b = smem_u32(sB + (st * I8_NP + j) * C::B_TILE);
 #pragma unroll
             for (int kk = 0; kk < I8_BK / 32; ++kk)
-              umma_s8_ss(tmem + (i + j) * I8_EP, umma_desc_sw128(a + kk * 32), umma_desc_sw128(b + kk * 32), idesc,
+              umma_s8_ss(tmem + (i + j) * EP, umma_desc_sw128(a + kk * 32), umma_desc_sw128(b + kk * 32), idesc,
                          (kk > 0 || ((touched >> (i + j)) & 1u)) ? 1u : 0u);
             touched |= 1u << (i + j);
           }
         umma_commit(&empty[st]);
-        if (++st == I8_STAGES) { st = 0; ph ^= 1; }
+        if (++st == C::STAGES) { st = 0; ph ^= 1; }
       }
       umma_commit(tfull);
     }
   } else if (nsplit > 1) {                                 // warps 2-5: write this split's int32 partials
     mbar_wait(tfull, 0);
     tc_fence_after();
+    I8STAMP(1);
     const int q = warp & 3, row = q * 32 + lane;
     const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
-    uint4* dst = reinterpret_cast<uint4*>(L.i8_part + ((long)split * L.T + t0 + row) * I8_ACC_COLS);
+    int* dst = L.i8_part + (long)split * C::ACC_COLS * L.T + t0 + row;   // column-major: token fastest
 #pragma unroll 1
-    for (int c = 0; c < I8_ACC_COLS; c += 16) {
+    for (int c = 0; c < C::ACC_COLS; c += 16) {
       uint32_t S[16];
       tmem_ld16(tb + c, S);
       tmem_ld_wait();
       if (row < rows)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) dst[c / 4 + u] = make_uint4(S[4 * u], S[4 * u + 1], S[4 * u + 2], S[4 * u + 3]);
+        for (int u = 0; u < 16; ++u) __stcg(dst + (long)(c + u) * L.T, (int)S[u]);
     }
   }
   tc_fence_before();
@@ -973,10 +1014,11 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       if (prev == nsplit - 1) L.i8_cnt[blk] = 0;
     }
     __syncthreads();
+    I8STAMP(2);
     if (!*s_last) {
       if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<I8_ACC_COLS>(tmem);
+        tmem_dealloc<C::ACC_COLS>(tmem);
       }
       return;
     }
@@ -993,11 +1035,11 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     const double sc = valid ? L.i8_r[t] * (double)L.i8_tok[t] : 0.0;
     const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-    for (int e0 = 0; e0 < I8_EP; e0 += 16) {
+    for (int e0 = 0; e0 < EP; e0 += 16) {
       int S[I8_NACC][16];
       if (nsplit == 1) {
 #pragma unroll
-        for (int a = 0; a < I8_NACC; ++a) tmem_ld16(tb + a * I8_EP + e0, reinterpret_cast<uint32_t(&)[16]>(S[a]));
+        for (int a = 0; a < I8_NACC; ++a) tmem_ld16(tb + a * EP + e0, reinterpret_cast<uint32_t(&)[16]>(S[a]));
         tmem_ld_wait();
       } else {
 #pragma unroll
@@ -1006,38 +1048,33 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
           for (int u = 0; u < 16; ++u) S[a][u] = 0;
         if (valid)
           for (int sp = 0; sp < nsplit; ++sp) {
-            const int4* src = reinterpret_cast<const int4*>(L.i8_part + ((long)sp * L.T + t) * I8_ACC_COLS);
+            const int* src = L.i8_part + (long)sp * C::ACC_COLS * L.T + t;
 #pragma unroll
             for (int a = 0; a < I8_NACC; ++a)
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int4 v = __ldcg(src + (a * I8_EP + e0) / 4 + u);
-                S[a][4 * u] += v.x;
-                S[a][4 * u + 1] += v.y;
-                S[a][4 * u + 2] += v.z;
-                S[a][4 * u + 3] += v.w;
-              }
+              for (int u = 0; u < 16; ++u) S[a][u] += __ldcg(src + (long)(a * EP + e0 + u) * L.T);
           }
       }
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const double v = (double)S[0][u] * 0x1p-14 + (double)S[1][u] * 0x1p-21 + (double)S[2][u] * 0x1p-28 +
                          (double)S[3][u] * 0x1p-35;
-        lg[row * I8_LGS + e0 + u] = (float)(sc * (double)L.i8_exp[e0 + u] * v);
+        lg[row * C::LGS + e0 + u] = (float)(sc * (double)L.i8_exp[e0 + u] * v);
       }
     }
   }
   tc_fence_before();
   __syncthreads();                                         // all logits in shared memory
+  I8STAMP(3);
   if (warp >= 2) {
     const int q = warp & 3, row = q * 32 + lane;
     if (row < rows) {
       const long t = t0 + row;
       const float l1x = L.i8_tok[L.T + t];
       float bmax = 0.f;
-      for (int e = 0; e < L.E; ++e) bmax = fmaxf(bmax, fmaf(L.i8_exp[I8_EP + e], l1x, L.i8_exp[2 * I8_EP + e]));
+      for (int e = 0; e < L.E; ++e) bmax = fmaxf(bmax, fmaf(L.i8_exp[EP + e], l1x, L.i8_exp[2 * EP + e]));
       const float B = (float)(L.i8_r[t] * (double)L.i8_tok[t] * (double)bmax * 1.0001) + 1e-12f;
-      const float* rowp = lg + row * I8_LGS;
+      const float* rowp = lg + row * C::LGS;
       switch (L.k) {
         case 1: select_token_thread<2>(rowp, t, row, B, L, rs); break;
         case 2: select_token_thread<3>(rowp, t, row, B, L, rs); break;
@@ -1051,11 +1088,13 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     }
   }
   __syncthreads();
-  refine_block<2>(L, lg, I8_LGS, rs, t0, rows);
+  I8STAMP(4);
+  refine_block<EP / 32>(L, lg, C::LGS, rs, t0, rows);
   __syncthreads();
+  I8STAMP(5);
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<I8_ACC_COLS>(tmem);
+    tmem_dealloc<C::ACC_COLS>(tmem);
   }
 }
 
@@ -1084,22 +1123,33 @@ static bool i8_make_map(CUtensorMap* m, const void* base, long rows, long cols, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static cudaError_t launch_router_i8(const RouterLaunch& L, cudaStream_t s) {
+template <int EP>
+static cudaError_t launch_router_i8_t(const RouterLaunch& L, cudaStream_t s) {
+  using C = I8Cfg<EP>;
   CUtensorMap ma, mb;
   if (!i8_make_map(&ma, L.i8_x, (long)I8_NP * L.T, L.d, I8_BM)) return cudaErrorInvalidValue;
-  if (!i8_make_map(&mb, L.i8_w, (long)I8_NP * I8_EP, L.d, I8_EP)) return cudaErrorInvalidValue;
+  if (!i8_make_map(&mb, L.i8_w, (long)I8_NP * EP, L.d, EP)) return cudaErrorInvalidValue;
   static std::atomic<unsigned long long> attr{0};
-  if (cudaError_t e = ensure_smem_attr(router_i8_kernel, I8_SMEM, attr)) return e;
+  if (cudaError_t e = ensure_smem_attr(router_i8_kernel<EP>, C::SMEM, attr)) return e;
   const int nblk = (L.T + I8_BM - 1) / I8_BM;
   int nsplit = kNumSMs / nblk;                                 // fill the SMs: split d across CTAs
   if (nsplit > I8_MAX_SPLIT) nsplit = I8_MAX_SPLIT;
   if (nsplit > L.d / I8_BK) nsplit = L.d / I8_BK;
   if (nsplit < 1 || (long)nsplit * L.T > kI8SplitRows) nsplit = 1;
-  router_i8_quant_w_kernel<<<I8_EP, 256, 0, s>>>(L);
-  router_i8_quant_x_kernel<<<(L.T + 7) / 8, 256, 0, s>>>(L);
-  router_i8_kernel<<<dim3(nblk, nsplit), I8_THREADS, I8_SMEM, s>>>(ma, mb, L);
+  router_i8_quant_w_kernel<<<EP, 256, 0, s>>>(L, EP);
+  if (L.d == 2048)
+    router_i8_quant_x_kernel<16><<<(L.T + 7) / 8, 256, 0, s>>>(L);
+  else if (L.d == 1024)
+    router_i8_quant_x_kernel<8><<<(L.T + 7) / 8, 256, 0, s>>>(L);
+  else
+    router_i8_quant_x_kernel<0><<<(L.T + 7) / 8, 256, 0, s>>>(L);
+  router_i8_kernel<EP><<<dim3(nblk, nsplit), I8_THREADS, C::SMEM, s>>>(ma, mb, L);
   g_launches += 3;
   return cudaGetLastError();
+}
+
+static cudaError_t launch_router_i8(const RouterLaunch& L, cudaStream_t s) {
+  return L.E <= 64 ? launch_router_i8_t<64>(L, s) : launch_router_i8_t<128>(L, s);
 }
 
 template <int EW>
@@ -1146,7 +1196,7 @@ cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s) {
   if (L.d % DC || L.d > kMaxD || L.E < 1 || L.E > 128 || L.k < 1 || L.k > L.E) return cudaErrorInvalidValue;
   if (!L.part || !L.part_sq || !L.w_scaled || !L.w_sq)
     return cudaErrorInvalidValue;
-  if (L.i8_x && L.E <= 64 && L.d % 128 == 0 && L.k <= 8) return launch_router_i8(L, s);
+  if (L.i8_x && L.E <= 128 && L.d % 128 == 0 && L.k <= 8) return launch_router_i8(L, s);
   if (L.E <= 32) return launch_router_t<1>(L, s);   // padded to 32 / 64 / 128 (zero W' columns)
   if (L.E <= 64) return launch_router_t<2>(L, s);
   return launch_router_t<4>(L, s);

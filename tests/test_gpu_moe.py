@@ -269,7 +269,7 @@ def test_fused_unpermute_is_bitwise_identical(name, T):
     ctx.close()
 
 
-@pytest.mark.parametrize("name,T", [("dsv2lite", 512), ("scout", 300)])
+@pytest.mark.parametrize("name,T", [("dsv2lite", 512), ("scout", 300), ("qwen3", 2048)])
 def test_int8_router_moe_parity(name, T):
     """The whole MoE block with the int8 tensor-core router: routing bit-exact against
     the fp64 oracle and the output within tolerance; identical to the SIMT-router run
@@ -279,6 +279,7 @@ def test_int8_router_moe_parity(name, T):
     w = synth.moe_weights(shape, seed=6)
     wd = moe_weights_dev(w)
     x = synth.tokens(shape, seed=6, T=T)
+    ctx.set_router_int8(False)                          # fp32 SIMT router
     ref_out, ref_dbg = run_blocking(ctx, wd, x)
     ctx.set_router_int8(True)
     out, dbg = run_blocking(ctx, wd, x)
