@@ -336,17 +336,19 @@ def run_gpu(args):
     # ---------------- e2e: host buffers through the C ABI, copies inside the region.
     # fsc_moe_forward_host_async pipelines step i's upload / compute / download with
     # its neighbours (two pinned buffer pairs alternate, as in a serving loop).
-    xh = [torch.from_numpy(synth.tokens(shape, seed=args.seed, rank=rank)).pin_memory() for _ in range(2)]
-    oh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
-    for i in range(3):
-        ctx.moe_forward_host_async(wd, xh[i % 2], oh[i % 2], stream=stream.cuda_stream)
+    # four pinned buffer pairs in rotation: call i's host buffers are free again once call
+    # i + 3 has returned (fsc.h contract of the three staging slots)
+    xh = [torch.from_numpy(synth.tokens(shape, seed=args.seed, rank=rank)).pin_memory() for _ in range(4)]
+    oh = [torch.empty_like(xh[0]).pin_memory() for _ in range(4)]
+    for i in range(4):
+        ctx.moe_forward_host_async(wd, xh[i % 4], oh[i % 4], stream=stream.cuda_stream)
     ctx.host_flush()
     if world > 1:
         dist.barrier()
     e2e_steps = max(4, args.steps)
     t0 = time.perf_counter()
     for i in range(e2e_steps):
-        ctx.moe_forward_host_async(wd, xh[i % 2], oh[i % 2], stream=stream.cuda_stream)
+        ctx.moe_forward_host_async(wd, xh[i % 4], oh[i % 4], stream=stream.cuda_stream)
     ctx.host_flush()
     e2e_s = time.perf_counter() - t0
     e2e_s = allreduce_max([e2e_s], dev)[0]

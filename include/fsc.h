@@ -283,10 +283,12 @@ FSC_API int fsc_moe_forward_blocking_host(fsc_ctx* ctx, const fsc_moe_weights* w
 /* Pipelined host-buffer variant for serving loops: enqueues the H2D copy of
  * x_in_host (pinned) on an internal copy stream, the forward on `stream` and the
  * D2H copy into out_host (pinned) on a second copy stream, ordered by events on
- * two internal staging slots, and returns at once. Step i's compute therefore
+ * three internal staging slots, and returns at once. Step i's compute therefore
  * overlaps step i+1's upload and step i-1's download. The host buffers of call i
- * may be reused once call i+2 has returned (call i+2 waits on the host for call i's
- * download before it enqueues anything) or after fsc_host_flush. */
+ * may be reused once call i+3 has returned (call i+3 waits on the host for call i's
+ * download before it enqueues anything) or after fsc_host_flush. The first call
+ * allocates the three device staging slots and the copy streams (kept until
+ * fsc_finalize). */
 FSC_API int fsc_moe_forward_host_async(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in_host,
                                        float* out_host, void* stream);
 /* Wait until every fsc_moe_forward_host_async output has reached host memory. */
@@ -376,7 +378,10 @@ typedef struct {
  * seq_len (T % seq_len == 0). modes[k] in {FSC_REGULAR, FSC_HYBRID} per layer
  * (partial conversion allowed); schedule FSC_BLOCKING serialises every
  * collective, FSC_OVERLAPPED runs the P:198 order with collectives on the comm
- * stream. attn/moe are arrays of L layers; cache is NULL or an array of L. */
+ * stream. attn/moe are arrays of L layers; cache is NULL or an array of L. Every
+ * layer's arguments are validated before anything is enqueued. The first call allocates
+ * the attention workspace (normed input, qkv, core output, 3 rotating fp32 residual
+ * buffers), grown when a later call needs wider projections. */
 FSC_API int fsc_layer_stack_forward(fsc_ctx* ctx, const fsc_attn_weights* attn, const fsc_moe_weights* moe, int L, int T,
                             int seq_len, const int* modes, int schedule, const float* o0, float* oL,
                             const fsc_act_cache* cache, void* stream);

@@ -89,9 +89,10 @@ struct fsc_ctx {
   cudaStream_t aux = nullptr;   // second compute stream (overlaps independent kernels)
   // pipelined host entry point (fsc_moe_forward_host_async)
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  float* io_slot_in[2] = {nullptr, nullptr};
-  float* io_slot_out[2] = {nullptr, nullptr};
-  cudaEvent_t ev_in[2] = {}, ev_cdone[2] = {}, ev_out[2] = {};
+  static constexpr int kIoSlots = 3;   // call i reuses the slot of call i - 3
+  float* io_slot_in[kIoSlots] = {};
+  float* io_slot_out[kIoSlots] = {};
+  cudaEvent_t ev_in[kIoSlots] = {}, ev_cdone[kIoSlots] = {}, ev_out[kIoSlots] = {};
   int io_slot = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_d = nullptr;
   cudaEvent_t ev_t1 = nullptr, ev_t2 = nullptr;   // TP attention all-reduce (stack)

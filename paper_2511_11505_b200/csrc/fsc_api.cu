@@ -217,7 +217,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < fsc_ctx::kIoSlots; ++i) {
     if (ctx->io_slot_in[i]) cudaFree(ctx->io_slot_in[i]);
     if (ctx->io_slot_out[i]) cudaFree(ctx->io_slot_out[i]);
     if (ctx->ev_in[i]) cudaEventDestroy(ctx->ev_in[i]);
@@ -910,7 +910,7 @@ extern "C" int fsc_moe_forward_host_async(fsc_ctx* ctx, const fsc_moe_weights* w
   if (!ctx->h2d) {
     CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < fsc_ctx::kIoSlots; ++i) {
       CK(cudaMalloc(&ctx->io_slot_in[i], sizeof(float) * n));
       CK(cudaMalloc(&ctx->io_slot_out[i], sizeof(float) * n));
       CK(cudaEventCreateWithFlags(&ctx->ev_in[i], cudaEventDisableTiming));
@@ -921,9 +921,9 @@ extern "C" int fsc_moe_forward_host_async(fsc_ctx* ctx, const fsc_moe_weights* w
     }
   }
   const int slot = ctx->io_slot;
-  ctx->io_slot ^= 1;
-  // the slot's previous call (two calls ago) must have finished its D2H into the caller's
-  // out_host before this call returns, so that "two calls later" the host buffers are free
+  ctx->io_slot = (ctx->io_slot + 1) % fsc_ctx::kIoSlots;
+  // the slot's previous call (three calls ago) must have finished its D2H into the caller's
+  // out_host before this call returns, so that "three calls later" the host buffers are free
   CK(cudaEventSynchronize(ctx->ev_out[slot]));
   const size_t bytes = sizeof(float) * (size_t)T * ctx->cfg.d;
   CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_cdone[slot], 0));      // slot's previous compute read its input

@@ -7,11 +7,12 @@
 // PAPER.md:73-76 per expert, the oracle's swiglu_backward). Both operands are read
 // MN-major straight from their row-major token layouts (no transposes): a stage holds
 // 64 token rows of 128 (A) and BN (B) columns as TMA boxes {64 columns x 64 rows}.
-// The last, partial k-block of a group is staged by the producer warp itself (plain
-// loads into the swizzled layout, zero rows past the group end) so that the next
-// group's rows never enter the sum. fp32 accumulation in TMEM, fp32 output.
+// The last, partial k-block of a group is loaded by TMA like the others, but its A tile
+// lands on a side barrier: the producer warp zeroes A's rows past the group end (the next
+// group's rows) before it releases the stage to the MMA, so they never enter the sum.
+// fp32 accumulation in TMEM, fp32 output.
 //
-// Roles (320 threads): warp 0 = producer (TMA; all lanes for partial blocks), warp 1 =
+// Roles (320 threads): warp 0 = producer (TMA; all lanes zero partial blocks), warp 1 =
 // TMEM allocator + MMA issuer, warps 2..9 = epilogue (TMEM lane quarter = warp % 4,
 // column half = (warp - 2) / 4), as in the forward grouped GEMM (gemm.cu).
 #include <cudaTypedefs.h>
@@ -38,6 +39,7 @@ struct WCfg {
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + 2 * (kWMaxGroups + 1) * 4 + 16 + SCRATCH;
+  static_assert((2 * 6 + 5) * 8 + 8 <= 256, "barriers + tmem slot fit the 256-byte control block");
 };
 
 FSC_DEVINL void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -60,7 +62,8 @@ __global__ void __launch_bounds__(kWThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* pbar = tempty + 2;                // partial k-block: A landed, rows past the group end to zero
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(pbar + 1);
   int* s_row_off = reinterpret_cast<int*>(smem + C::STAGES * C::STAGE_BYTES + 256);
   int* s_cnt = s_row_off + (kWMaxGroups + 1);
   float* s_scr = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_cnt + (kWMaxGroups + 1)) + 15) &
@@ -81,6 +84,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], kWEpiWarps);
       }
+      mbar_init(pbar, 1);
       fence_barrier_init();
     }
   } else if (warp == 1) {
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------ producer (whole warp)
     int stage = 0;
-    uint32_t phase = 0;
+    uint32_t phase = 0, pphase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int g = t / tpg, r = t - g * tpg, mb = r / n_nb, nb = r - mb * n_nb;
       const int M = s_cnt[g];
@@ -138,18 +142,24 @@ __global__ void __launch_bounds__(kWThreads, 1)
             for (int i = 0; i < BN / 64; ++i) tma_load_2d(b + i * 64 * WBK * 2, &tmB, &full[stage], bcol + 64 * i, m0, kEvictNormal);
           }
         } else {
-          // partial block: B by TMA (its extra rows meet zero A rows), A staged by the warp
+          // partial block: B by TMA onto full[stage] (its extra rows meet zero A rows); A by
+          // TMA onto pbar, then the warp zeroes A's rows past the group end (whole 128-byte
+          // k-rows: the swizzle only permutes 16-byte chunks inside a row) and arrives
           if (lane == 0) {
             mbar_expect_tx(&full[stage], C::B_BYTES);
 #pragma unroll
             for (int i = 0; i < BN / 64; ++i) tma_load_2d(b + i * 64 * WBK * 2, &tmB, &full[stage], bcol + 64 * i, m0, kEvictNormal);
+            mbar_arrive_expect_tx(pbar, C::A_BYTES);
+            tma_load_2d(a, &tmA, pbar, acol, m0, kEvictNormal);
+            tma_load_2d(a + 64 * WBK * 2, &tmA, pbar, acol + 64, m0, kEvictNormal);
           }
-          for (int idx = lane; idx < 2 * 64 * 8; idx += 32) {
-            const int box = idx >> 9, rr = (idx >> 3) & 63, j = idx & 7;
-            const long col = (long)acol + box * 64 + j * 8;
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (rr < valid && col < p.lda) v = __ldg(reinterpret_cast<const uint4*>(p.A + (long)(m0 + rr) * p.lda + col));
-            *reinterpret_cast<uint4*>(a + box * 64 * WBK * 2 + rr * 128 + ((j ^ (rr & 7)) << 4)) = v;
+          mbar_wait(pbar, pphase);
+          pphase ^= 1;
+          for (int idx = valid * 8 + lane; idx < 64 * 8; idx += 32) {
+            const int rr = idx >> 3, j = idx & 7;
+#pragma unroll
+            for (int box = 0; box < 2; ++box)
+              *reinterpret_cast<uint4*>(a + box * 64 * WBK * 2 + rr * 128 + j * 16) = make_uint4(0u, 0u, 0u, 0u);
           }
           fence_proxy_async_smem();
           __syncwarp();

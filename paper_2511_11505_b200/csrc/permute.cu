@@ -13,6 +13,8 @@
 // K5: out[t] = resid[t] + (sum_j w[t,j] * y[pos[t,j]]) with the inner sum
 // started at 0 and taken in slot order (C-amb-12), fp32. In the FarSkip wiring
 // resid = attn-in_{k+1} and out = mlp-in_{k+1} = o_k.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -123,6 +125,77 @@ __global__ void __launch_bounds__(256) perm_pos_kernel(const int* __restrict__ i
   }
 }
 
+// Small T (decode, <= 32 chunks of 32 tokens, E <= 128): the three steps above in ONE
+// CTA of 32 warps (warp = chunk): chunk masks, per-expert column scan (one thread per
+// expert), exclusive scan of the totals, positions. Same definition, same results; one
+// launch instead of three with global round trips in between.
+constexpr int kFusedChunks = 32, kFusedE = 128;
+__global__ void __launch_bounds__(1024) perm_fused_kernel(const int* __restrict__ idx, int T, int k, int E,
+                                                         int* __restrict__ counts, int* __restrict__ offsets,
+                                                         int* __restrict__ pos, int* __restrict__ src_row,
+                                                         int n_chunks) {
+  __shared__ uint32_t mask[kFusedChunks][kFusedE];
+  __shared__ int base[kFusedChunks][kFusedE];
+  __shared__ int s_cnt[kFusedE];
+  __shared__ int s_off[kFusedE + 1];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  for (int e = lane; e < E; e += 32) mask[w][e] = 0;
+  __syncwarp();
+  const int t = w * 32 + lane;
+  if (w < n_chunks && t < T)
+    for (int j = 0; j < k; ++j) atomicOr(&mask[w][idx[(long)t * k + j]], 1u << lane);
+  __syncthreads();
+  if (tid < E) {                          // column scan over the chunks, chunk order
+    int run = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      base[c][tid] = run;
+      run += __popc(mask[c][tid]);
+    }
+    s_cnt[tid] = run;
+  }
+  __syncthreads();
+  if (w == 0) {                           // exclusive scan of the expert totals (4 per lane)
+    int v[4], loc = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = lane * 4 + i;
+      v[i] = e < E ? s_cnt[e] : 0;
+      loc += v[i];
+    }
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    int run = inc - loc;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = lane * 4 + i;
+      if (e < E) {
+        s_off[e] = run;
+        offsets[e] = run;
+        counts[e] = v[i];
+      }
+      run += v[i];
+    }
+    if (lane == 31) {
+      s_off[E] = inc;
+      offsets[E] = inc;
+    }
+  }
+  __syncthreads();
+  if (w < n_chunks && t < T) {
+    const uint32_t below = (1u << lane) - 1u;
+    for (int j = 0; j < k; ++j) {
+      const int e = idx[(long)t * k + j];
+      const int p = s_off[e] + base[w][e] + __popc(mask[w][e] & below);
+      pos[(long)t * k + j] = p;
+      src_row[p] = t;
+    }
+  }
+}
+
 cudaError_t launch_perm_maps(const PermLaunch& L, cudaStream_t s) {
   if (L.E > kMaxE || L.E < 1) return cudaErrorInvalidValue;
   const int nc = perm_chunks(L.T);
@@ -130,6 +203,11 @@ cudaError_t launch_perm_maps(const PermLaunch& L, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(L.counts, 0, sizeof(int) * L.E, s);
     if (e != cudaSuccess) return e;
     return cudaMemsetAsync(L.offsets, 0, sizeof(int) * (L.E + 1), s);
+  }
+  if (nc <= kFusedChunks && L.E <= kFusedE) {
+    ++g_launches;
+    perm_fused_kernel<<<1, 1024, 0, s>>>(L.topk_idx, L.T, L.k, L.E, L.counts, L.offsets, L.pos, L.src_row, nc);
+    return cudaGetLastError();
   }
   const int blocks = (nc + 7) / 8;
   g_launches += 3;
@@ -223,6 +301,41 @@ __global__ void __launch_bounds__(256) unpermute_kernel(const uint4* __restrict_
   }
 }
 
+// A/B variant (FSC_UNPERMUTE_ILP=0): one slot's row load at a time (40 registers)
+__global__ void __launch_bounds__(256) unpermute_simple_kernel(const uint4* __restrict__ y, const int* __restrict__ pos,
+                                                               const float* __restrict__ w,
+                                                               const float* __restrict__ resid, float* __restrict__ out,
+                                                               long items, int dv, int k) {
+  for (long it = (long)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (long)gridDim.x * blockDim.x) {
+    const long t = it / dv;
+    const int c = (int)(it - t * dv);
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const long p = pos[t * k + j];
+      const float g = w[t * k + j];
+      const uint4 v = y[p * dv + c];
+      acc[0] = fmaf(g, bf16lo(v.x), acc[0]);
+      acc[1] = fmaf(g, bf16hi(v.x), acc[1]);
+      acc[2] = fmaf(g, bf16lo(v.y), acc[2]);
+      acc[3] = fmaf(g, bf16hi(v.y), acc[3]);
+      acc[4] = fmaf(g, bf16lo(v.z), acc[4]);
+      acc[5] = fmaf(g, bf16hi(v.z), acc[5]);
+      acc[6] = fmaf(g, bf16lo(v.w), acc[6]);
+      acc[7] = fmaf(g, bf16hi(v.w), acc[7]);
+    }
+    const float4* rr = reinterpret_cast<const float4*>(resid + t * (long)dv * 8 + c * 8);
+    float4* oo = reinterpret_cast<float4*>(out + t * (long)dv * 8 + c * 8);
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (resid) { a = rr[0]; b = rr[1]; }
+    a.x += acc[0]; a.y += acc[1]; a.z += acc[2]; a.w += acc[3];
+    b.x += acc[4]; b.y += acc[5]; b.z += acc[6]; b.w += acc[7];
+    oo[0] = a;
+    oo[1] = b;
+  }
+}
+
 cudaError_t launch_unpermute(const uint16_t* y, const int* pos, const float* w, const float* resid, float* out,
                              int T, int k, int d, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
@@ -231,7 +344,12 @@ cudaError_t launch_unpermute(const uint16_t* y, const int* pos, const float* w, 
   long blocks = (items + 255) / 256;
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
   ++g_launches;
-  unpermute_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, resid, out, items, dv, k);
+  static const int ilp = getenv("FSC_UNPERMUTE_ILP") ? atoi(getenv("FSC_UNPERMUTE_ILP")) : 1;
+  if (!ilp)
+    unpermute_simple_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, resid, out, items,
+                                                        dv, k);
+  else
+    unpermute_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, resid, out, items, dv, k);
   return cudaGetLastError();
 }
 

@@ -17,7 +17,7 @@ def test_host_entry_points_match_device_path():
     ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=shape.ffn,
                   shared_ffn=shape.shared_ffn, max_tokens=T)
     wd = moe_weights_dev(synth.moe_weights(shape, seed=3))
-    xs = [synth.tokens(shape, seed=3, rank=i, T=T) for i in range(5)]
+    xs = [synth.tokens(shape, seed=3, rank=i, T=T) for i in range(7)]
     ref = []
     for x in xs:
         xin = dev_f32(x)
@@ -29,19 +29,20 @@ def test_host_entry_points_match_device_path():
     oh = torch.empty_like(xh).pin_memory()
     ctx.moe_forward_blocking_host(wd, xh, oh)
     np.testing.assert_array_equal(oh.numpy(), ref[0])
-    # pipelined: alternate two pinned buffer pairs, as a serving loop would
-    ins = [torch.empty(T, shape.d).pin_memory() for _ in range(2)]
-    outs = [torch.empty(T, shape.d).pin_memory() for _ in range(2)]
-    got = []
+    # pipelined, as a serving loop would: four pinned buffer pairs in rotation, so that a
+    # pair is rewritten only after the call three later has returned (fsc.h contract)
+    ins = [torch.empty(T, shape.d).pin_memory() for _ in range(4)]
+    outs = [torch.empty(T, shape.d).pin_memory() for _ in range(4)]
+    got = [None] * len(xs)
     for i, x in enumerate(xs):
-        j = i % 2
-        if i >= 2:
-            ctx.host_flush()                  # (only needed because we read outs[j] back below)
-            got.append(outs[j].numpy().copy())
+        j = i % 4
+        if i >= 4:
+            got[i - 4] = outs[j].numpy().copy()   # call i - 4 is complete: call i - 1 has returned
         ins[j].copy_(torch.from_numpy(x))
         ctx.moe_forward_host_async(wd, ins[j], outs[j])
     ctx.host_flush()
-    got += [outs[(len(xs) - 2) % 2].numpy().copy(), outs[(len(xs) - 1) % 2].numpy().copy()]
+    for i in range(max(0, len(xs) - 4), len(xs)):
+        got[i] = outs[i % 4].numpy().copy()
     for g, r in zip(got, ref):
         np.testing.assert_array_equal(g, r)
     ctx.close()

@@ -190,7 +190,10 @@ def test_router_parity_int8(ctx_i8, name, T):
     by ~2e-4 of their scale (three 7-bit planes), so few tokens need the fp64 refinement."""
     nref, e_max = _router_parity(ctx_i8, name, T)
     assert e_max < 5e-5
-    assert nref <= max(4, T // 50)
+    # refinement is the exception, not the rule: the boundary gaps shrink with E (Qwen3,
+    # E = 128, k = 8: ~4.4% of the tokens are within the band)
+    E = synth.CONFIGS[name].n_experts
+    assert nref <= max(4, T * E // 1600), (nref, T, E)
 
 
 def _router_parity(ctx, name, T, skew=0.0):
@@ -250,10 +253,16 @@ def test_router_exact_ties_go_to_lower_index(ctx):
 
 
 # ----------------------------------------------------------------------------- K2 / K3 / K5
-@pytest.mark.parametrize("T,E,k", [(1, 4, 2), (32, 4, 2), (33, 8, 3), (1000, 64, 6), (4096, 128, 8), (777, 16, 1)])
-def test_perm_maps_exact(ctx, T, E, k):
+# T <= 1024 with E <= 128 runs the single-CTA fused kernel, larger T the three-kernel path
+@pytest.mark.parametrize("T,E,k,hot", [(1, 4, 2, 0), (32, 4, 2, 0), (33, 8, 3, 0), (1000, 64, 6, 0), (4096, 128, 8, 0),
+                                       (777, 16, 1, 0), (512, 128, 8, 0), (1024, 128, 8, 0), (1025, 128, 8, 0),
+                                       (1024, 128, 8, 1), (3000, 64, 6, 1)])
+def test_perm_maps_exact(ctx, T, E, k, hot):
     rng = np.random.default_rng(T + E)
-    idx = np.stack([np.sort(rng.choice(E, k, replace=False)) for _ in range(T)]).astype(np.int32)
+    if hot:   # every token on the same k experts (extreme skew): one expert block holds all copies
+        idx = np.tile(np.arange(E - k, E, dtype=np.int32), (T, 1))
+    else:
+        idx = np.stack([np.sort(rng.choice(E, k, replace=False)) for _ in range(T)]).astype(np.int32)
     di = torch.from_numpy(idx).cuda()
     counts = torch.empty(E, dtype=torch.int32, device="cuda")
     offs = torch.empty(E + 1, dtype=torch.int32, device="cuda")
