@@ -13,8 +13,6 @@
 // K5: out[t] = resid[t] + (sum_j w[t,j] * y[pos[t,j]]) with the inner sum
 // started at 0 and taken in slot order (C-amb-12), fp32. In the FarSkip wiring
 // resid = attn-in_{k+1} and out = mlp-in_{k+1} = o_k.
-#include <stdlib.h>
-
 #include "common.cuh"
 #include "kernels.h"
 
@@ -254,55 +252,10 @@ cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t
 }
 
 // ------------------------------------------------------------------ K5 unpermute
+// One thread per (token, 8 columns), the k slots summed in slot order. (A variant with
+// every slot's row load in flight at once measured slower: 78 registers, fewer CTAs per
+// SM - DS 63.5 -> 71.7 us, Qwen3 137 -> 141 us.)
 __global__ void __launch_bounds__(256) unpermute_kernel(const uint4* __restrict__ y, const int* __restrict__ pos,
-                                                        const float* __restrict__ w,
-                                                        const float* __restrict__ resid, float* __restrict__ out,
-                                                        long items, int dv, int k) {
-  for (long it = (long)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += (long)gridDim.x * blockDim.x) {
-    const long t = it / dv;
-    const int c = (int)(it - t * dv);
-    float acc[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-    // up to 8 slots: every copy's row load in flight at once, then the fp32 sum in slot order
-    for (int j0 = 0; j0 < k; j0 += 8) {
-      uint4 v[8];
-      float g[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (j0 + u < k) {
-          const long p = __ldg(pos + t * k + j0 + u);
-          g[u] = __ldg(w + t * k + j0 + u);
-          v[u] = y[p * dv + c];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (j0 + u < k) {
-          acc[0] = fmaf(g[u], bf16lo(v[u].x), acc[0]);
-          acc[1] = fmaf(g[u], bf16hi(v[u].x), acc[1]);
-          acc[2] = fmaf(g[u], bf16lo(v[u].y), acc[2]);
-          acc[3] = fmaf(g[u], bf16hi(v[u].y), acc[3]);
-          acc[4] = fmaf(g[u], bf16lo(v[u].z), acc[4]);
-          acc[5] = fmaf(g[u], bf16hi(v[u].z), acc[5]);
-          acc[6] = fmaf(g[u], bf16lo(v[u].w), acc[6]);
-          acc[7] = fmaf(g[u], bf16hi(v[u].w), acc[7]);
-        }
-      }
-    }
-    const float4* rr = reinterpret_cast<const float4*>(resid + t * (long)dv * 8 + c * 8);
-    float4* oo = reinterpret_cast<float4*>(out + t * (long)dv * 8 + c * 8);
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (resid) { a = rr[0]; b = rr[1]; }
-    a.x += acc[0]; a.y += acc[1]; a.z += acc[2]; a.w += acc[3];
-    b.x += acc[4]; b.y += acc[5]; b.z += acc[6]; b.w += acc[7];
-    oo[0] = a;
-    oo[1] = b;
-  }
-}
-
-// A/B variant (FSC_UNPERMUTE_ILP=0): one slot's row load at a time (40 registers)
-__global__ void __launch_bounds__(256) unpermute_simple_kernel(const uint4* __restrict__ y, const int* __restrict__ pos,
                                                                const float* __restrict__ w,
                                                                const float* __restrict__ resid, float* __restrict__ out,
                                                                long items, int dv, int k) {
@@ -344,12 +297,7 @@ cudaError_t launch_unpermute(const uint16_t* y, const int* pos, const float* w, 
   long blocks = (items + 255) / 256;
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
   ++g_launches;
-  static const int ilp = getenv("FSC_UNPERMUTE_ILP") ? atoi(getenv("FSC_UNPERMUTE_ILP")) : 1;
-  if (!ilp)
-    unpermute_simple_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, resid, out, items,
-                                                        dv, k);
-  else
-    unpermute_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, resid, out, items, dv, k);
+  unpermute_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(y), pos, w, resid, out, items, dv, k);
   return cudaGetLastError();
 }
 
