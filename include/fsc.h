@@ -183,14 +183,14 @@ FSC_API int fsc_set_gemm_gather(fsc_ctx* ctx, int on);
  * runs the separate unpermute kernel, on < 0 (default) fuses for top-1 routing only.
  * Bitwise the same result either way. */
 FSC_API int fsc_set_fused_unpermute(fsc_ctx* ctx, int on);
-/* Router (K1) on the int8 tensor cores (E <= 128, d % 128 == 0, k <= 8): x and
- * gamma (.) W_R split into three exact 7-bit fixed-point planes, the plane products
- * summed exactly in int32 (tcgen05 kind::i8), combined in fp64; the same selection,
- * fp64 band refinement and results contract as the fp32 SIMT router (both equal the
- * fp64 oracle's selection). on > 0: always (where allowed); 0: never; < 0 (default):
- * auto = for E > 64 at T >= 2048 (measured: Qwen3 T = 16384 310 -> 165 us; DS-V2-Lite
- * and Scout shapes are as fast or faster on the SIMT path). Allocates its workspace on
- * first use (at fsc_init when auto applies). */
+/* Router (K1) on the tensor cores, one fused kernel (router_tc_kernel; E <= 128,
+ * d % 128 == 0, k <= 8): RMS statistics, xn, base-2^7 digit planes of x_t / s_t and
+ * of gamma (.) W_R / s_e (s powers of two), their products summed exactly in int32
+ * (tcgen05 kind::i8) and combined exactly in fp64, then the same selection, fp64 band
+ * refinement and results contract as the fp32 SIMT router (both equal the fp64
+ * oracle's selection; the fp32 gates differ by rounding). on != 0 (default -1 = auto):
+ * wherever the shape allows it; 0: the fp32 SIMT router. The digit workspace
+ * (3 x 128 x d int8) is allocated at fsc_init. */
 FSC_API int fsc_set_router_int8(fsc_ctx* ctx, int on);
 /* Select the EP data movement (FSC_EP_ALLTOALL default, FSC_EP_ALLREDUCE). Must be
  * called before fsc_bootstrap_export (it re-creates the peer region). In

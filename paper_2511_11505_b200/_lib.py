@@ -317,8 +317,9 @@ class Context:
         self._ck(self.lib.fsc_set_ep_mode(self.h, mode))
 
     def set_router_int8(self, on):
-        """Router on the int8 tensor cores (exact fixed-point planes; E <= 128, d % 128 == 0):
-        True / False, or None = auto (the default: int8 for E > 64 at prefill sizes)."""
+        """Router on the tensor cores (the fused exact int8-digit kernel; E <= 128, d % 128 == 0,
+        k <= 8): True / None (auto, the default: wherever the shape allows) or False (the fp32
+        SIMT router)."""
         self._ck(self.lib.fsc_set_router_int8(self.h, -1 if on is None else int(on)))
 
     def set_fused_unpermute(self, on):

@@ -58,13 +58,8 @@ struct fsc_ctx {
   int* counts = nullptr;       // [E]                copies per global expert (this rank)
   int* offsets = nullptr;      // [E+1]
   int* comb_cnt = nullptr;     // [T, d/32]         fused-unpermute arrival counters
-  int8_t* i8_x = nullptr;      // exact int8 router workspace (E <= 64): planes of x, W'
-  int8_t* i8_w = nullptr;
-  float* i8_tok = nullptr;
-  double* i8_r = nullptr;
-  float* i8_exp = nullptr;
-  int* i8_part = nullptr;
-  int* i8_cnt = nullptr;
+  int8_t* i8_w = nullptr;      // exact tensor-core router workspace: digit planes of gamma W_R, [3, 128, d]
+  float* i8_exp = nullptr;     // per-expert scale and error-bound coefficients, [3, 128]
   float* r_part = nullptr;     // [kRouterSplitRows, 128] split-d partial logits (small T)
   double* r_part_sq = nullptr; // [kRouterSplitRows]      split-d partial sums of x^2
   float* w_scaled = nullptr;   // [E, d]             gamma * W_R
@@ -144,6 +139,8 @@ cudaError_t fsc_fuzz(fsc_ctx* ctx, cudaStream_t st);
 // argument checks of one MoE call (weights, T, activation pointers, alignment); no enqueue
 int fsc_validate_moe(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, const void* out);
 // debug finiteness check of an fp32 [n] output (fsc_set_debug_checks): synchronises s
+// the exact tensor-core router (router_tc_kernel) is used for this context's forward and backward
+bool router_tc_on(const fsc_ctx* ctx);
 int fsc_check_finite(fsc_ctx* ctx, const float* out, long n, cudaStream_t s, const char* what);
 
 // transport (EP > 1). All return fsc_status.

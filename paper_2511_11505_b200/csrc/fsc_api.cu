@@ -202,7 +202,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->i8_x, ctx->i8_w, ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2], ctx->nf_count, ctx->b_gb, ctx->b_duv, ctx->b_hg, ctx->b_dgpart, ctx->b_dlrow, ctx->b_rtok, ctx->b_gr, ctx->b_gate, ctx->b_colpart};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->i8_w, ctx->i8_exp, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2], ctx->nf_count, ctx->b_gb, ctx->b_duv, ctx->b_hg, ctx->b_dgpart, ctx->b_dlrow, ctx->b_rtok, ctx->b_gr, ctx->b_gate, ctx->b_colpart};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -401,28 +401,18 @@ static bool router_i8_ok(const fsc_ctx* ctx) {
 }
 
 static int router_i8_alloc(fsc_ctx* ctx) {
-  const fsc_moe_config& c = ctx->cfg;
-  const long T = c.max_tokens, d = c.d;
-  if (ctx->i8_x) return FSC_OK;   // workspace on first use
+  if (ctx->i8_w) return FSC_OK;   // allocated once (fsc_init / fsc_set_router_int8)
   CK(cudaSetDevice(ctx->device));
-  CK(dalloc(&ctx->i8_x, 3 * T * d));
-  CK(dalloc(&ctx->i8_w, 3 * 128 * d));
-  CK(dalloc(&ctx->i8_part, (long)kI8SplitRows * 512));
-  CK(dalloc(&ctx->i8_cnt, (T + 127) / 128 + 1));
-  CK(cudaMemset(ctx->i8_cnt, 0, sizeof(int) * ((T + 127) / 128 + 1)));
-  CK(dalloc(&ctx->i8_tok, 3 * T));
-  CK(dalloc(&ctx->i8_r, T));
+  CK(dalloc(&ctx->i8_w, 3L * 128 * ctx->cfg.d));
   CK(dalloc(&ctx->i8_exp, 3 * 128));
   return FSC_OK;
 }
 
-// auto (router_i8 < 0): the int8 tensor-core router where it measured faster than the
-// fp32 SIMT one (E > 64 at prefill batch sizes: Qwen3 T = 16384, 310 -> 165 us); both
-// select exactly the fp64 oracle's experts
-static bool use_router_i8(const fsc_ctx* ctx, int T) {
-  if (!ctx->i8_x || !router_i8_ok(ctx)) return false;
-  if (ctx->router_i8 > 0) return true;
-  return ctx->router_i8 < 0 && ctx->cfg.n_experts > 64 && T >= 2048;
+// The exact tensor-core router (router_tc_kernel) wherever the shape allows it (auto or on);
+// the fp32 SIMT router otherwise or when switched off. Both select exactly the fp64 oracle's
+// experts; their fp32 gates differ by rounding.
+bool router_tc_on(const fsc_ctx* ctx) {
+  return ctx->i8_w && router_i8_ok(ctx) && ctx->router_i8 != 0;
 }
 
 extern "C" int fsc_set_router_int8(fsc_ctx* ctx, int on) {
@@ -433,7 +423,7 @@ extern "C" int fsc_set_router_int8(fsc_ctx* ctx, int on) {
   }
   if (on < 0) {
     ctx->router_i8 = -1;
-    if (router_i8_ok(ctx) && ctx->cfg.n_experts > 64) return router_i8_alloc(ctx);
+    if (router_i8_ok(ctx)) return router_i8_alloc(ctx);
     return FSC_OK;
   }
   REQUIRE(router_i8_ok(ctx), FSC_ERR_CONFIG, "int8 router needs E <= 128, d %% 128 == 0, k <= 8");
@@ -515,8 +505,7 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
                     dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr,
                     ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, TB_DEFAULT,
-                    use_router_i8(ctx, T) ? ctx->i8_x : nullptr, ctx->i8_w,
-                    ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt};
+                    ctx->i8_w, ctx->i8_exp, router_tc_on(ctx) ? 1 : 0};
     CK(launch_router(rl, s));
   }
   PH_END(PH_ROUTER);
@@ -1002,7 +991,7 @@ extern "C" int fsc_op_router(fsc_ctx* ctx, const float* x, const float* gamma, c
           "router shape beyond the context workspace");
   RouterLaunch rl{x, gamma, w_router, T, d, E, k, ctx->cfg.rms_eps, static_cast<uint16_t*>(xn), topk_idx, topk_w,
                   logits, n_refined, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, TB_DEFAULT,
-                  (use_router_i8(ctx, T) && d == ctx->cfg.d && E <= 128) ? ctx->i8_x : nullptr, ctx->i8_w, ctx->i8_tok, ctx->i8_r, ctx->i8_exp, ctx->i8_part, ctx->i8_cnt};
+                  ctx->i8_w, ctx->i8_exp, (router_tc_on(ctx) && d == ctx->cfg.d && E <= 128) ? 1 : 0};
   CK(launch_router(rl, static_cast<cudaStream_t>(stream)));
   return FSC_OK;
 }

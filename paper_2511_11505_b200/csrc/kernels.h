@@ -136,16 +136,11 @@ struct RouterLaunch {
   float* w_scaled;       // workspace [E, d]: gamma * W_R
   float* w_sq;           // workspace [E]: ||gamma * W_R[e]||^2
   int rpb = 32;          // tokens per CTA (set by launch_router)
-  // exact int8 tensor-core path (E <= 128, d % 128 == 0); nullptr planes = fp32 SIMT path
-  int8_t* i8_x;          // workspace [3, T, d]: 7-bit planes of x_t / s_t
-  int8_t* i8_w;          // workspace [3, 128, d]: 7-bit planes of (gamma W_R)_e / s_e
-  float* i8_tok;         // workspace [3, T]: s_t, ||x_t / s_t||_1, (float) r_t
-  double* i8_r;          // workspace [T]: r_t (fp64)
-  float* i8_exp;         // workspace [3, 128]: s_e and the two per-expert error-bound coefficients
-  int* i8_part;          // workspace [kI8SplitRows * 512]: split-d int32 partial sums, [split][col][T]
-  int* i8_cnt;           // workspace [ceil(T/128)]: split arrival tickets, zero between calls
+  // exact tensor-core path (router_tc_kernel; E <= 128, d % 128 == 0, k <= 8), used when tc != 0
+  int8_t* i8_w;          // workspace [3, EP, d]: base-2^7 digit planes of floor((gamma W_R)_e 2^21 / s_e)
+  float* i8_exp;         // workspace [3, EP]: s_e and the two per-expert error-bound coefficients
+  int tc;
 };
-constexpr int kI8SplitRows = 148 * 128;
 // split-d partials: (token blocks) x (d splits) <= 2 x 148 CTAs of <= 32 rows
 constexpr int kRouterSplitRows = 2 * 148 * 32;
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s);

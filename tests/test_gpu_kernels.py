@@ -17,7 +17,7 @@ def ctx():
     build.build()
     from paper_2511_11505_b200 import Context
     c = Context(d=5120, n_experts=128, top_k=8, ffn=1408, shared_ffn=0, max_tokens=16384)
-    c.set_router_int8(False)   # K1 tests below: the fp32 SIMT router (ctx_i8: the int8 one)
+    c.set_router_int8(False)   # K1 tests below: the fp32 SIMT router (ctx_i8: the tensor-core one)
     yield c
     c.close()
 
@@ -165,7 +165,7 @@ ROUTER_CASES = [("tiny", 32), ("tiny", 1), ("dsv2lite", 700), ("qwen3", 513), ("
 
 @pytest.fixture(scope="module")
 def ctx_i8():
-    """E <= 128 and d % 128 == 0: the exact int8 tensor-core router (router_i8_kernel)."""
+    """E <= 128 and d % 128 == 0: the exact fused tensor-core router (router_tc_kernel)."""
     from paper_2511_11505_b200 import Context
     c = Context(d=5120, n_experts=128, top_k=8, ffn=128, shared_ffn=0, max_tokens=16384)
     c.set_router_int8(True)
@@ -186,8 +186,9 @@ def test_router_parity_skewed(ctx, name, T, skew):
 
 @pytest.mark.parametrize("name,T", [c for c in ROUTER_CASES if c[0] != "tiny"] + [("dsv2lite", 129), ("qwen3", 1)])
 def test_router_parity_int8(ctx_i8, name, T):
-    """Exact int8 tensor-core path: same bit-exact indices; the logits' error is bounded
-    by ~2e-4 of their scale (three 7-bit planes), so few tokens need the fp64 refinement."""
+    """Exact fused tensor-core path (int8 digit planes, tcgen05 kind::i8): same bit-exact
+    indices; the logits' rigorous error bound is ~1e-4 of their scale (three 7-bit digits,
+    one-signed truncation), so few tokens need the fp64 refinement."""
     nref, e_max = _router_parity(ctx_i8, name, T)
     assert e_max < 5e-5
     # refinement is the exception, not the rule: the boundary gaps shrink with E (Qwen3,
@@ -235,7 +236,9 @@ def dataclass_replace_small(shape):
     return dataclasses.replace(shape, ffn=1, shared_ffn=0)
 
 
-def test_router_exact_ties_go_to_lower_index(ctx):
+@pytest.mark.parametrize("which", ["simt", "tc"])
+def test_router_exact_ties_go_to_lower_index(ctx, ctx_i8, which):
+    ctx = ctx if which == "simt" else ctx_i8
     rng = np.random.default_rng(5)
     T, d, E, k = 64, 128, 16, 3
     x = rng.standard_normal((T, d)).astype(np.float32)
@@ -250,6 +253,26 @@ def test_router_exact_ties_go_to_lower_index(ctx):
     torch.cuda.synchronize()
     r = om.route(om.rmsnorm(x, gamma), W.astype(np.float64), k)
     np.testing.assert_array_equal(idx.cpu().numpy(), r.idx)
+
+
+def test_router_all_experts_tied(ctx_i8):
+    """Every router row equal: every logit of a token ties, every token is ambiguous and its
+    band is all E experts - more (token, expert) pairs than the fused kernel's pair list, so
+    its overflow path runs too. The exact answer: experts 0..k-1 (ties -> lower id), gates 1/k."""
+    rng = np.random.default_rng(6)
+    T, d, E, k = 300, 256, 128, 8
+    x = rng.standard_normal((T, d)).astype(np.float32)
+    gamma = (1.0 + 0.1 * rng.standard_normal(d)).astype(np.float32)
+    W = np.repeat((rng.standard_normal((1, d)) / np.sqrt(d)).astype(np.float32), E, axis=0)
+    xn = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    gw = torch.empty(T, k, dtype=torch.float32, device="cuda")
+    nref = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx_i8.op_router(dev_f32(x), dev_f32(gamma), dev_f32(W), k, xn, idx, gw, None, nref)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(idx.cpu().numpy(), np.tile(np.arange(k, dtype=np.int32), (T, 1)))
+    np.testing.assert_allclose(gw.cpu().numpy(), 1.0 / k, rtol=0, atol=1e-6)
+    assert int(nref.item()) == T
 
 
 # ----------------------------------------------------------------------------- K2 / K3 / K5

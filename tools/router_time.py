@@ -19,8 +19,8 @@ for name in sys.argv[1:] or ["dsv2lite", "qwen3", "scout"]:
     w = synth.moe_weights(dataclasses.replace(shape, ffn=64, shared_ffn=0), seed=0)
     x = dev_f32(synth.tokens(shape, T=T))
     ctx = Context(d=shape.d, n_experts=shape.n_experts, top_k=shape.top_k, ffn=64, shared_ffn=0, max_tokens=T)
-    if os.environ.get("FSC_ROUTER_I8") == "1":
-        ctx.set_router_int8(True)
+    if os.environ.get("FSC_ROUTER_I8") == "0":
+        ctx.set_router_int8(False)   # the fp32 SIMT router (default: the fused tensor-core one)
     g, wr = dev_f32(w.gamma), dev_f32(w.w_router)
     xn = torch.empty(T, shape.d, dtype=torch.bfloat16, device="cuda")
     idx = torch.empty(T, shape.top_k, dtype=torch.int32, device="cuda")
@@ -39,5 +39,5 @@ for name in sys.argv[1:] or ["dsv2lite", "qwen3", "scout"]:
     flop = 2.0 * T * shape.d * shape.n_experts
     med = statistics.median(ts)
     print(f"{name} T={T}: router {med:.1f} us (min {min(ts):.1f}), {flop / med / 1e6:.1f} TFLOP/s fp32, "
-          f"int8={os.environ.get('FSC_ROUTER_I8', '0')}")
+          f"tc={os.environ.get('FSC_ROUTER_I8', '1')} cs={os.environ.get('FSC_ROUTER_CS', 'auto')}")
     ctx.close()
