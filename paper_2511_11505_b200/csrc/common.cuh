@@ -295,6 +295,21 @@ FSC_DEVINL void tmem_dealloc_2sm(uint32_t base) {
 }
 
 // ------------------------------------------------------------------ misc
+// 16-byte global load kept in L2 (evict_last: data read again soon, e.g. gathered rows
+// read k times) and 16-byte store that streams through L2 (evict_first: written once,
+// read back much later), both bypassing L1
+FSC_DEVINL uint4 ld_keep_u4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(kEvictLast));
+  return v;
+}
+FSC_DEVINL void st_stream_u4(uint4* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(kEvictFirst)
+               : "memory");
+}
 FSC_DEVINL void st_global_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");

@@ -128,7 +128,7 @@ FSC_DEVINL void copy_row_warp(const uint4* __restrict__ a, uint4* b, int dv, int
     uint4 buf[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (i0 + 32 * u < dv) buf[u] = __ldcs(a + i0 + 32 * u);
+      if (i0 + 32 * u < dv) buf[u] = STREAM ? __ldcs(a + i0 + 32 * u) : ld_keep_u4(a + i0 + 32 * u);
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (i0 + 32 * u < dv) b[i0 + 32 * u] = buf[u];
