@@ -635,6 +635,15 @@ def stack_measure(ctx, shape, wd, x, L, steps, world, dev, rank, seed):
     overlappable = sum(rp.get(k, 0.0) for k in ("attn_a", "attn_b", "shared1", "shared2"))
     comm = sum(rp.get(k, 0.0) for k in ("dispatch", "combine"))
     eq9 = {"overlappable_us": overlappable * 1e3, "comm_us": comm * 1e3, "slack_us": (overlappable - comm) * 1e3}
+    # the same slack with the attention at its tensor-core roofline (FLOPs / measured bf16
+    # peak): what a fused attention would leave to hide the all-to-all behind (P:325
+    # "fused attention makes comm more critical"), so the overlap is not judged against the
+    # slow mma.sync filler alone
+    peaks, _ = load_peaks()
+    attn_roof_ms = (fa + fb) / (peaks["bf16_tflops"] * 1e12) * 1e3
+    ovl_roof = attn_roof_ms + sum(rp.get(k, 0.0) for k in ("shared1", "shared2"))
+    eq9["attention_roofline_us"] = attn_roof_ms * 1e3
+    eq9["slack_us_at_roofline_attention"] = (ovl_roof - comm) * 1e3
     out = {"layers": L, "attention": f"GQA {shape.n_heads}/{shape.n_kv_heads}x{shape.head_dim}, seq {shape.seq_len}",
            **res, "attention_throughput": attn, "eq9": eq9,
            "speedup_farskip_vs_regular": res["regular"]["ms_per_stack"] / res["farskip"]["ms_per_stack"],

@@ -183,6 +183,12 @@ FSC_API int fsc_set_gemm_gather(fsc_ctx* ctx, int on);
  * runs the separate unpermute kernel, on < 0 (default) fuses for top-1 routing only.
  * Bitwise the same result either way. */
 FSC_API int fsc_set_fused_unpermute(fsc_ctx* ctx, int on);
+/* Grouped-GEMM tile schedule: on > 0 dynamic (each CTA pair after its first tile claims
+ * the next one from an atomic counter and hands it to its roles through a shared-memory
+ * queue, so pairs that start late beside co-running kernels take fewer tiles), 0 the
+ * static stride, < 0 (default) dynamic at EP > 1 only (where the dispatch / combine CTAs
+ * share the SMs). The results are bitwise the same either way. */
+FSC_API int fsc_set_gemm_dynamic(fsc_ctx* ctx, int on);
 /* Router (K1) on the tensor cores, one fused kernel (router_tc_kernel; E <= 128,
  * d % 128 == 0, k <= 8): RMS statistics, xn, base-2^7 digit planes of x_t / s_t and
  * of gamma (.) W_R / s_e (s powers of two), their products summed exactly in int32

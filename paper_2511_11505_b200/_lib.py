@@ -79,6 +79,7 @@ _SIGS = {
     "fsc_set_gemm_gather": (_I, [_P, _I]),
     "fsc_set_fused_unpermute": (_I, [_P, _I]),
     "fsc_set_router_int8": (_I, [_P, _I]),
+    "fsc_set_gemm_dynamic": (_I, [_P, _I]),
     "fsc_set_ep_mode": (_I, [_P, _I]),
     "fsc_set_dispatch_fp8": (_I, [_P, _I]),
     "fsc_set_debug_checks": (_I, [_P, _I]),
@@ -315,6 +316,11 @@ class Context:
         """FSC_EP_ALLTOALL (Dispatch / Combine) or FSC_EP_ALLREDUCE (replicated tokens,
         P:215-217). Call before connect()."""
         self._ck(self.lib.fsc_set_ep_mode(self.h, mode))
+
+    def set_gemm_dynamic(self, on):
+        """Grouped-GEMM tile schedule: True (dynamic), False (static stride) or None (auto:
+        dynamic at EP > 1)."""
+        self._ck(self.lib.fsc_set_gemm_dynamic(self.h, -1 if on is None else int(on)))
 
     def set_router_int8(self, on):
         """Router on the tensor cores (the fused exact int8-digit kernel; E <= 128, d % 128 == 0,

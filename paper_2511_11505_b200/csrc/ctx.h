@@ -31,6 +31,7 @@ struct fsc_ctx {
   int fuse_unpermute = -1;     // blocking EP = 1: unpermute fused into GEMM2 (-1 auto: top-1)
   int dispatch_fp8 = 0;        // FP8 (e4m3, per-128-column scales) dispatch payload, EP > 1 all-to-all
   int ep_mode = 0;             // FSC_EP_ALLTOALL (dispatch / combine) or FSC_EP_ALLREDUCE (replicated tokens)
+  int gemm_dyn = -1;           // dynamic GEMM tile schedule: 1 on, 0 off, -1 auto (EP > 1)
   int router_i8 = -1;          // exact int8 tensor-core router: 1 on, 0 off, -1 auto (fsc_set_router_int8)
   int gather_a = 0;            // EP = 1: GEMM1 gathers A through src_row (fused permute)
   int combine_mode = 0;        // FSC_COMBINE_STREAM (comm-stream push after GEMM2) or FSC_COMBINE_FUSED
@@ -58,6 +59,7 @@ struct fsc_ctx {
   int* counts = nullptr;       // [E]                copies per global expert (this rank)
   int* offsets = nullptr;      // [E+1]
   int* comb_cnt = nullptr;     // [T, d/32]         fused-unpermute arrival counters
+  int* gemm_sched = nullptr;   // [kSchedSlots, 2]  dynamic GEMM tile schedules, one per launch site (zero between launches)
   int8_t* i8_w = nullptr;      // exact tensor-core router workspace: digit planes of gamma W_R, [3, 128, d]
   float* i8_exp = nullptr;     // per-expert scale and error-bound coefficients, [3, 128]
   float* r_part = nullptr;     // [kRouterSplitRows, 128] split-d partial logits (small T)
@@ -139,6 +141,16 @@ cudaError_t fsc_fuzz(fsc_ctx* ctx, cudaStream_t st);
 // argument checks of one MoE call (weights, T, activation pointers, alignment); no enqueue
 int fsc_validate_moe(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float* x_in, const void* out);
 // debug finiteness check of an fp32 [n] output (fsc_set_debug_checks): synchronises s
+// dynamic tile-schedule counter pairs of the grouped GEMM, one per launch site (launches
+// that may run concurrently must not share one)
+enum { SCHED_SHARED1 = 0, SCHED_SHARED2, SCHED_ROUTED1, SCHED_ROUTED2, SCHED_OP, kSchedSlots = 32 };
+// The dynamic schedule is on where kernels co-run with the GEMMs on the same SMs (EP > 1:
+// dispatch / combine CTAs); at EP = 1 the static stride is as balanced and avoids the per-tile
+// hand-off (A/B). fsc_set_gemm_dynamic overrides.
+inline int* gemm_sched_slot(const fsc_ctx* ctx, int slot) {
+  const bool on = ctx->gemm_dyn >= 0 ? ctx->gemm_dyn != 0 : ctx->ep > 1;
+  return on && ctx->gemm_sched ? ctx->gemm_sched + 2 * slot : nullptr;
+}
 // the exact tensor-core router (router_tc_kernel) is used for this context's forward and backward
 bool router_tc_on(const fsc_ctx* ctx);
 int fsc_check_finite(fsc_ctx* ctx, const float* out, long n, cudaStream_t s, const char* what);

@@ -159,6 +159,8 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(dalloc(&ctx->offsets, E + 1));
   CK(dalloc(&ctx->comb_cnt, T * (d / 32)));   // [T, d / (BN/2)] fused-unpermute counters, BN/2 >= 32
   CK(cudaMemset(ctx->comb_cnt, 0, sizeof(int) * T * (d / 32)));
+  CK(dalloc(&ctx->gemm_sched, 2 * kSchedSlots));
+  CK(cudaMemset(ctx->gemm_sched, 0, sizeof(int) * 2 * kSchedSlots));
   CK(dalloc(&ctx->r_part, (long)kRouterSplitRows * 128));
   CK(dalloc(&ctx->r_part_sq, (long)kRouterSplitRows));
   CK(dalloc(&ctx->w_scaled, (E > 128 ? E : 128) * d));  // e-major [E][d] or k-major [d][EP<=128]
@@ -202,7 +204,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->i8_w, ctx->i8_exp, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2], ctx->nf_count, ctx->b_gb, ctx->b_duv, ctx->b_hg, ctx->b_dgpart, ctx->b_dlrow, ctx->b_rtok, ctx->b_gr, ctx->b_gate, ctx->b_colpart};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->gemm_sched, ctx->i8_w, ctx->i8_exp, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2], ctx->nf_count, ctx->b_gb, ctx->b_duv, ctx->b_hg, ctx->b_dgpart, ctx->b_dlrow, ctx->b_rtok, ctx->b_gr, ctx->b_gate, ctx->b_colpart};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -430,6 +432,12 @@ extern "C" int fsc_set_router_int8(fsc_ctx* ctx, int on) {
   int rc = router_i8_alloc(ctx);
   if (rc) return rc;
   ctx->router_i8 = 1;
+  return FSC_OK;
+}
+
+extern "C" int fsc_set_gemm_dynamic(fsc_ctx* ctx, int on) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  ctx->gemm_dyn = on < 0 ? -1 : (on ? 1 : 0);
   return FSC_OK;
 }
 
@@ -663,6 +671,7 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     g1.a_idx = a_idx;
     g1.row_base = row_base;
     g1.bn = pick_bn(c.ffn, true);
+    g1.sched = gemm_sched_slot(ctx, SCHED_ROUTED1);
     PH_BEGIN(PH_GEMM1);
     CK(launch_grouped_gemm(g1, s));
     PH_END(PH_GEMM1);
@@ -672,6 +681,7 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     g2.out = ctx->y; g2.ldo = d; g2.epi = EPI_BF16; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = routed_cg;
     g2.row_base = row_base;
     g2.bn = pick_bn(d, false);
+    g2.sched = gemm_sched_slot(ctx, SCHED_ROUTED2);
     if (fused_combine) fsc_transport_scatter_target(ctx, &g2.ret, g2.peer_out);  // P:100 Combine, fused
     if (fused_out && ctx->ep == 1) {   // P:100 "sum the routed experts", fused into the down GEMM
       g2.comb_out = fused_out; g2.comb_resid = fused_resid; g2.src_row = ctx->src_row; g2.pos = ctx->pos;
@@ -768,6 +778,7 @@ static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float
   g1.A = ctx->xn; g1.a_rows = T; g1.B0 = w->ws1; g1.B1 = w->ws2; g1.b_rows = c.shared_ffn; g1.b_group_rows = c.shared_ffn;
   g1.K = d; g1.N = c.shared_ffn; g1.G = 1; g1.counts = nullptr; g1.m_total = T; g1.out = ctx->hs; g1.ldo = c.shared_ffn;
   g1.epi = EPI_SWIGLU; g1.num_ctas = ctx->gemm_ctas; g1.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
+  g1.sched = gemm_sched_slot(ctx, SCHED_SHARED1);
   PH_BEGIN(PH_SHARED1);
   CK(launch_grouped_gemm(g1, s));
   PH_END(PH_SHARED1);
@@ -775,6 +786,7 @@ static int moe_shared(fsc_ctx* ctx, const fsc_moe_weights* w, int T, const float
   g2.A = ctx->hs; g2.a_rows = T; g2.B0 = w->ws3; g2.B1 = nullptr; g2.b_rows = d; g2.b_group_rows = d;
   g2.K = c.shared_ffn; g2.N = d; g2.G = 1; g2.counts = nullptr; g2.m_total = T; g2.out = out; g2.ldo = d;
   g2.resid = resid; g2.ldr = d; g2.epi = EPI_RESID_F32; g2.num_ctas = ctx->gemm_ctas; g2.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
+  g2.sched = gemm_sched_slot(ctx, SCHED_SHARED2);
   PH_BEGIN(PH_SHARED2);
   CK(launch_grouped_gemm(g2, s));
   PH_END(PH_SHARED2);
@@ -1038,6 +1050,7 @@ extern "C" int fsc_op_grouped_gemm_gather(fsc_ctx* ctx, int epi, const void* A, 
   L.num_ctas = ctx->gemm_ctas;
   L.cta_group = ctx->gemm_cg ? ctx->gemm_cg : 2;
   L.a_idx = a_idx;
+  L.sched = gemm_sched_slot(ctx, SCHED_OP);
   CK(launch_grouped_gemm(L, static_cast<cudaStream_t>(stream)));
   return FSC_OK;
 }

@@ -17,6 +17,7 @@
 // column half = (warp-2)/4).
 // Tiles: BM=128 rows x BN cols, BK=64 (one 128-byte swizzle atom of bf16).
 #include <cudaTypedefs.h>
+#include <limits.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -47,6 +48,10 @@ struct Cfg {
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;                     // double-buffered accumulator
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + 2 * (kMaxGroups + 1) * 4 + 16 + SCRATCH;
+  // dynamic schedule: tile queue depth, as deep as the rest of the 256-byte barrier area allows
+  static constexpr int TQ_RAW = (256 - (2 * STAGES + 4) * 8 - 8) / 20;   // (8-byte aligned barriers)
+  static constexpr int TQ = TQ_RAW > 8 ? 8 : TQ_RAW;
+  static_assert(TQ >= 4, "barriers + tile queue in the 256-byte area");
 };
 
 // SiLU with the fast divide (2 ulp; 0 for denominators beyond 2^126, where SiLU ~ 0)
@@ -241,6 +246,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+  // tile queue of the dynamic schedule: the last 80 bytes of the 256-byte barrier area
+  constexpr int kTQ = C::TQ;
+  uint64_t* tq_full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + ((256 - 20 * kTQ) & ~7));
+  uint64_t* tq_empty = tq_full + kTQ;
+  int* s_tq = reinterpret_cast<int*>(tq_empty + kTQ);
   int* s_row_off = reinterpret_cast<int*>(smem + C::STAGES * C::STAGE_BYTES + 256);
   int* s_tile_off = s_row_off + (kMaxGroups + 1);
   float* s_scr = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_tile_off + (kMaxGroups + 1)) + 15) &
@@ -266,6 +276,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], kEpiWarps * CG);
+      }
+      for (int i = 0; i < kTQ; ++i) {     // consumers of a queue entry: MMA + epilogue warps (+ the peer producer)
+        mbar_init(&tq_full[i], 1);
+        mbar_init(&tq_empty[i], 1 + kEpiWarps * CG + (CG == 2 ? 1 : 0));
       }
       fence_barrier_init();
     }
@@ -309,6 +323,62 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total = s_tile_off[G] * n_tiles;
   const int kblocks = p.K / BK;
   const int t_first = blockIdx.x / CG, t_step = gridDim.x / CG;
+  // Tile schedule. Static: the u-th tile of this CTA (pair) is t_first + u t_step. Dynamic
+  // (p.sched): the first tile is static, later ones are claimed from an atomic counter by
+  // the (leader's) producer and handed to every role through a kTQ-deep shared-memory queue
+  // (the peer CTA's copy written over DSMEM): a CTA (pair) that gets its SMs late, beside
+  // co-running kernels, takes fewer tiles instead of leaving a tail of pre-assigned ones.
+  const bool dyn = p.sched != nullptr && !p.a_idx;
+  const uint32_t tq_empty_leader = CG == 2 ? mapa_shared(smem_u32(tq_empty), 0) : smem_u32(tq_empty);
+  // claimer (producer thread of the leader CTA): the u-th tile, published to the queue
+  // The claimer publishes entry u + 1 when it starts tile u (so the peer CTA's producer
+  // learns its next tile a tile ahead, as with the static stride), and the atomic behind
+  // entry u + 2 is issued right after, so its round trip overlaps the tile's loads.
+  int pend = 0, last = 0;
+  auto publish = [&](int u, int t) {
+    const int sl = u % kTQ;
+    if (u >= kTQ) mbar_wait(&tq_empty[sl], ((u / kTQ) - 1) & 1);
+    s_tq[sl] = t;
+    if (CG == 2) {
+      st_cluster_s32(mapa_shared(smem_u32(&s_tq[sl]), 1), t);
+      mbar_arrive_cluster(mapa_shared(smem_u32(&tq_full[sl]), 1));   // release.cluster: after the store
+    }
+    mbar_arrive(&tq_full[sl]);
+  };
+  auto claim_tile = [&](int u) -> int {
+    if (!dyn) return t_first + u * t_step < total ? t_first + u * t_step : -1;
+    if (u == 0) {
+      last = t_first < total ? t_first : -1;
+      publish(0, last);
+      if (last >= 0) pend = atomicAdd(p.sched, 1);
+    }
+    const int t = last;                                  // entry u (published one tile ago)
+    if (t >= 0) {
+      int nx = pend + t_step;
+      if (nx >= total) nx = -1;
+      publish(u + 1, nx);
+      if (nx >= 0) pend = atomicAdd(p.sched, 1);
+      last = nx;
+    }
+    return t;
+  };
+  // consumer: the u-th tile from the queue (arrive = this consumer is done reading the entry;
+  // an epilogue warp passes arrive only on lane 0, after __syncwarp)
+  auto next_tile = [&](int u, bool arrive) -> int {
+    if (!dyn) return t_first + u * t_step < total ? t_first + u * t_step : -1;
+    const int sl = u % kTQ;
+    if (CG == 2 && !leader) mbar_wait_acq_cluster(&tq_full[sl], (u / kTQ) & 1);   // published over DSMEM
+    else mbar_wait(&tq_full[sl], (u / kTQ) & 1);
+    const int t = s_tq[sl];
+    __syncwarp(__activemask());
+    // relaxed arrive: a release here would make an epilogue warp wait for its global stores
+    // to drain; the branch on the loaded value orders the shared-memory read before it
+    if (arrive && t != INT_MIN) {
+      if (CG == 2) mbar_arrive_cluster_relaxed(tq_empty_leader + sl * 8);
+      else mbar_arrive_relaxed(&tq_empty[sl]);
+    }
+    return t;
+  };
 
   if (warp == 0 && p.a_idx) {
     // ------------------------------------------------ TMA producer, gathered A (whole warp 0):
@@ -376,7 +446,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = t_first; t < total; t += t_step) {
+      for (int u = 0;; ++u) {
+        const int t = leader ? claim_tile(u) : next_tile(u, true);
+        if (t < 0) break;
         TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
         ti.row0 += rbase;
         const int arow = ti.row0 + (int)rank * BM;
@@ -451,8 +523,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = idesc_bf16_f32(C::TILE_M, BN) | (BMN ? kIdescBMN : 0u);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int t = t_first; t < total; t += t_step, ++it) {
+      for (int it = 0;; ++it) {
+        if (next_tile(it, true) < 0) break;
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -486,8 +558,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = (warp - 2) >> 2;   // column half handled by this warp
     const int r = q * 32 + lane;
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
-    int it = 0;
-    for (int t = t_first; t < total; t += t_step, ++it) {
+    for (int it = 0;; ++it) {
+      const int t = next_tile(it, lane == 0);
+      if (t < 0) break;
       TileInfo ti = decode_tile<C::TILE_M>(t, n_tiles, G, s_row_off, s_tile_off);
       ti.row0 += rbase;
       const int acc = it & 1;
@@ -661,6 +734,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (CG == 2) cluster_sync();   // the peer may still arrive on / commit to our barriers until here
+  if (dyn && threadIdx.x == 0) {  // the last CTA out resets the schedule for the next launch
+    __threadfence();
+    if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
+      __threadfence();
+    }
+  }
   if (warp == 1) {
     tc_fence_after();
     if (CG == 2) tmem_dealloc_2sm<C::TMEM_COLS>(tmem_base);
@@ -748,6 +829,7 @@ static cudaError_t launch_t(const GemmLaunch& L, cudaStream_t s) {
   // FSC_GEMM_STAGE_ROWS = 0 / 1 overrides the K-based choice (A/B measurements)
   static const int stage_env = getenv("FSC_GEMM_STAGE_ROWS") ? atoi(getenv("FSC_GEMM_STAGE_ROWS")) : -1;
   p.stage_rows = stage_env >= 0 ? stage_env : (L.epi == EPI_BF16 ? 1 : 0);
+  p.sched = L.sched;
   int grid = L.num_ctas > 0 ? L.num_ctas : kNumSMs;
   if (CG == 2) grid &= ~1;
   if (grid < CG) grid = CG;

@@ -43,6 +43,7 @@ struct GemmParams {
   int* comb_cnt;               // [T, n_cb] zero between calls (the last arrival resets)
   int top_k, n_cb;
   int stage_rows;              // bf16 epilogue: 1 = staged row-contiguous stores, 0 = direct
+  int* sched;                  // dynamic tile schedule {claim counter, done counter} or nullptr
   // MN-major B (dgrad GEMMs, template BMN): B is [K rows, N cols] per group, group g's K rows
   // start at g * b_group_rows; kb_split > 0: k-blocks >= kb_split read tmB1 (rows restart at
   // 0), i.e. the K dimension is [B0 rows ; B1 rows] (dX = [dU | dV] [W1 ; W2])
@@ -75,6 +76,7 @@ struct GemmLaunch {
   long ldr;
   int epi;
   int num_ctas;       // persistent grid (<= 148); 0 = all SMs
+  int* sched = nullptr;  // dynamic tile schedule: 2 ints, zero between launches (nullptr: static stride)
   int cta_group = 2;  // 2: CTA pairs, MMA M=256 (default); 1: single-CTA M=128 tiles
   const int* ret = nullptr;           // scatter map (see GemmParams)
   void* peer_out[8] = {};

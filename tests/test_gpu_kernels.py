@@ -63,6 +63,40 @@ def test_grouped_gemm_bf16(ctx, counts, N, K, cg):
         r += m
 
 
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("epi,counts,N,K", [(0, [517, 64, 1, 129, 0, 255, 256, 1000], 2048, 1408),
+                                            (0, [70, 71], 192, 64), (1, [600, 0, 257, 255], 768, 2048),
+                                            (2, [777], 2048, 256), (0, [0, 0], 256, 64)])
+def test_grouped_gemm_dynamic_schedule_bitwise(ctx, epi, counts, N, K, cg):
+    """The dynamic tile schedule (atomic claims, shared-memory tile queue, DSMEM hand-off to
+    the peer CTA) computes every tile exactly as the static stride does: bitwise equal
+    outputs, on the full grid and on a small grid (many tiles per CTA), twice in a row
+    (the last CTA out resets the counters)."""
+    ctx.set_gemm_cta_group(cg)
+    rng = np.random.default_rng(21 + N + K + epi)
+    G, M = len(counts), sum(counts)
+    A = dev_bf16(rand_bf16(rng, (max(M, 1), K)))
+    B0 = dev_bf16(rand_bf16(rng, (G * N, K), 1.0 / np.sqrt(K)))
+    B1 = dev_bf16(rand_bf16(rng, (G * N, K), 1.0 / np.sqrt(K))) if epi == 1 else None
+    resid = dev_f32(rng.standard_normal((max(M, 1), N)).astype(np.float32)) if epi == 2 else None
+    cnt = torch.tensor(counts, dtype=torch.int32, device="cuda") if epi != 2 else None
+    dt = torch.float32 if epi == 2 else torch.bfloat16
+    outs = []
+    try:
+        for dyn, ctas in [(False, 148), (True, 148), (True, 148), (True, 20)]:
+            ctx.set_gemm_dynamic(dyn)
+            ctx.set_gemm_ctas(ctas)
+            out = torch.zeros(max(M, 1), N, dtype=dt, device="cuda")
+            ctx.op_grouped_gemm(epi, A, B0, B1, G, cnt, M if epi == 2 else 0, N, K, out, resid)
+            torch.cuda.synchronize()
+            outs.append(out.cpu())
+    finally:
+        ctx.set_gemm_dynamic(None)
+        ctx.set_gemm_ctas(148)
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
 @pytest.mark.parametrize("counts,N,K", [([1], 128, 64), ([0, 130, 257], 128, 128), ([333, 900, 17], 1408, 2048),
                                         ([40], 64, 64), ([256, 1], 8192, 128), ([600, 0, 257, 255], 768, 2048)])
 @pytest.mark.parametrize("cg", [1, 2])

@@ -40,7 +40,7 @@ for name in sys.argv[1:] or ["dsv2lite"]:
         ctx.op_router(x, g, wr, shape.top_k, xn, idx, gw, logits=stamps)
     torch.cuda.synchronize()
     allst = stamps.cpu().numpy().astype(np.float64)
-    qw = allst[148 * 8 * 8 - 2: 148 * 8 * 8]
+    qw = allst[148 * 8 * 8 - 2: 148 * 8 * 8].copy()
     allst[148 * 8 * 8 - 2: 148 * 8 * 8] = 0
     s = allst.reshape(-1, 8)
     s = s[s[:, 0] > 0]
