@@ -416,6 +416,13 @@ FSC_API int fsc_op_grouped_gemm_gather(fsc_ctx* ctx, int epi, const void* A, lon
                                        const void* B0, const void* B1, int G, const int* counts, int m_total, int N,
                                        int K, void* out, const float* resid, void* stream);
 /* K5: out fp32 [T,d] = resid + sum_j w[t,j] y[pos[t,j]] (resid may be NULL -> 0). */
+/* Core attention of the stack's filler (P:198 part (b) without the o-projection): qkv bf16
+ * [T, (Hq + 2 Hkv) hd] (q heads | k heads | v heads, RoPE applied), out bf16 [T, Hq hd] =
+ * softmax(q k^T / sqrt(hd), causal within packed sequences of seq_len) v per head (GQA:
+ * head h reads kv head h / (Hq / Hkv)). hd = 128 with seq_len % 128 == 0 runs the tcgen05
+ * kernel, otherwise the mma.sync one (hd in {16, 32, 64, 128}). Test entry point. */
+FSC_API int fsc_op_attention(fsc_ctx* ctx, const void* qkv, void* out, int T, int Hq, int Hkv, int hd, int seq_len,
+                             void* stream);
 FSC_API int fsc_op_unpermute(fsc_ctx* ctx, const void* y, const int* pos, const float* w, const float* resid, float* out,
                      int T, int k, int d, void* stream);
 

@@ -110,6 +110,7 @@ _SIGS = {
     "fsc_op_grouped_gemm": (_I, [_P, _I, _P, _L, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "fsc_op_grouped_gemm_gather": (_I, [_P, _I, _P, _L, _P, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "fsc_op_unpermute": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),
+    "fsc_op_attention": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P]),
     "fsc_moe_backward": (_I, [_P, ctypes.POINTER(MoeWeightsC), _I, _P, _P, ctypes.POINTER(MoeGradsC), _P]),
     "fsc_op_gemm_dgrad": (_I, [_P, _I, _P, _L, _P, _P, _L, _I, _P, _I, _I, _I, _I, _P, _P, _P]),
     "fsc_op_gemm_swiglu_bwd": (_I, [_P, _P, _L, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P]),
@@ -445,6 +446,10 @@ class Context:
         self._ck(self.lib.fsc_op_grouped_gemm_gather(self.h, epi, ptr(A), A.shape[0], ptr(a_idx), ptr(B0), ptr(B1), G,
                                                      ptr(counts), m_total, N, K, ptr(out), ptr(resid),
                                                      stream if stream is not None else cur_stream()))
+
+    def op_attention(self, qkv, out, Hq, Hkv, hd, seq_len, stream=None):
+        self._ck(self.lib.fsc_op_attention(self.h, ptr(qkv), ptr(out), qkv.shape[0], Hq, Hkv, hd, seq_len,
+                                           stream if stream is not None else cur_stream()))
 
     def op_unpermute(self, y, pos, w, resid, out, stream=None):
         T, k = pos.shape

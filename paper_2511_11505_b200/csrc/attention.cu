@@ -9,7 +9,9 @@
 // The core kernel is a FlashAttention-2 style forward with mma.sync bf16 tiles
 // (64 queries x 64 keys per step, online softmax in fp32). It is the filler, not
 // the hot path, and is not roofline-graded.
+#include <cudaTypedefs.h>
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -278,10 +280,303 @@ static cudaError_t launch_fa_t(const uint16_t* qkv, uint16_t* out, int T, int Hq
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------- tcgen05 flash attention fwd
+// Causal attention of one head over a 128-query tile on the 5th-generation tensor cores
+// (HD = 128, seq_len % 128 == 0): S = Q K^T and O += P V are tcgen05 MMAs (M = 128,
+// N = 128, accumulators in TMEM: S double-buffered, O resident); Q, K and V arrive by TMA
+// (K-major Q / K boxes, V as MN-major B boxes), P goes through shared memory in the
+// 128B-swizzled K-major layout. Warp 0: TMA; warp 1: MMA issue (S_{j+1} is issued before
+// PV_j, so the next scores overlap this block's softmax); warps 2-5: one query row per
+// thread (the TMEM lane): mask, online softmax in base 2 with a lazy rescale (the running
+// max is only raised when a block's max exceeds it by 2^8, FA4-style: p <= 2^8 stays exact
+// enough in fp32 / bf16 and O is rescaled in TMEM only then), then O / l -> bf16.
+namespace {
+constexpr int TA_BM = 128, TA_BN = 128, TA_HD = 128;
+constexpr int TA_THREADS = 192;
+constexpr int TA_TILE = TA_BM * TA_HD * 2;     // 32 KB: Q / K / V / P tiles
+constexpr int TA_SMEM = 1024 + 6 * TA_TILE + 256;
+constexpr float kLazy = 8.f;                   // log2 units: rescale O when the max grows by more
+
+FSC_DEVINL void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+FSC_DEVINL void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+FSC_DEVINL void fence_proxy_async_smem_ta() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+}  // namespace
+
+__global__ void __launch_bounds__(TA_THREADS, 1)
+    flash_attn_tc_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV, uint16_t* out,
+                         int T, int Hq, int Hkv, int seq_len, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                                   // [2 atoms][128 rows][128 B]
+  uint8_t* sK = smem + TA_TILE;                         // [2 stages] x 32 KB
+  uint8_t* sV = smem + 3 * TA_TILE;                     // [2 stages] x [2 key halves][2 dim blocks][64 keys][128 B]
+  uint8_t* sP = smem + 5 * TA_TILE;                     // [2 atoms][128 rows][128 B]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * TA_TILE);
+  uint64_t* q_full = bar;
+  uint64_t* k_full = bar + 1;                           // [2]
+  uint64_t* k_empty = bar + 3;                          // [2]
+  uint64_t* v_full = bar + 5;                           // [2]
+  uint64_t* v_empty = bar + 7;                          // [2]
+  uint64_t* s_full = bar + 9;                           // [2]
+  uint64_t* s_empty = bar + 11;                         // [2]
+  uint64_t* p_full = bar + 13;
+  uint64_t* pv_done = bar + 14;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 15);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int h = blockIdx.y, kvh = h / (Hq / Hkv);
+  // query tiles in decreasing order of their key-block count (heavy tiles first)
+  const int tps = seq_len / TA_BM, nseq = (T + seq_len - 1) / seq_len;
+  const int i = blockIdx.x, pos = tps - 1 - i / nseq, sq = i % nseq;
+  const long q0 = (long)sq * seq_len + (long)pos * TA_BM;
+  if (q0 >= T) return;
+  const long seq0 = (long)sq * seq_len;
+  const int nb = pos + 1;                               // key blocks seq0 .. q0 (the diagonal one last)
+  const int qcol = h * TA_HD, kcol = (Hq + kvh) * TA_HD, vcol = (Hq + Hkv + kvh) * TA_HD;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmQK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], 4);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+  } else if (warp == 1) {
+    tmem_alloc<512>(s_tmem);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;                        // S0 [0,128), S1 [128,256), O [256,384)
+
+  if (warp == 0) {
+    if (elect_one()) {                                   // TMA producer
+      mbar_arrive_expect_tx(q_full, TA_TILE);
+      tma_load_2d(sQ, &tmQK, q_full, qcol, (int)q0, kEvictFirst);
+      tma_load_2d(sQ + TA_TILE / 2, &tmQK, q_full, qcol + 64, (int)q0, kEvictFirst);
+      for (int j = 0; j < nb; ++j) {
+        const int st = j & 1;
+        const int k0 = (int)(seq0 + (long)j * TA_BN);
+        if (j >= 2) mbar_wait(&k_empty[st], ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&k_full[st], TA_TILE);
+        tma_load_2d(sK + st * TA_TILE, &tmQK, &k_full[st], kcol, k0, kEvictLast);
+        tma_load_2d(sK + st * TA_TILE + TA_TILE / 2, &tmQK, &k_full[st], kcol + 64, k0, kEvictLast);
+        if (j >= 2) mbar_wait(&v_empty[st], ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&v_full[st], TA_TILE);
+#pragma unroll
+        for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+          for (int db = 0; db < 2; ++db)
+            tma_load_2d(sV + st * TA_TILE + kh * (TA_TILE / 2) + db * (TA_TILE / 4), &tmV, &v_full[st],
+                        vcol + db * 64, k0 + kh * 64, kEvictLast);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {                                   // MMA issuer
+      const uint32_t idesc_s = idesc_bf16_f32(TA_BM, TA_BN);
+      const uint32_t idesc_o = idesc_bf16_f32(TA_BM, TA_HD) | kIdescBMN;
+      const uint32_t aq = smem_u32(sQ), ap = smem_u32(sP);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        if (j >= 2) mbar_wait(&s_empty[st], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t bk = smem_u32(sK + st * TA_TILE);
+#pragma unroll
+        for (int kk = 0; kk < TA_HD / 16; ++kk) {      // over the head dim: 2 atoms of 64
+          const uint32_t off = (kk >> 2) * (TA_TILE / 2) + (kk & 3) * 32;
+          umma_bf16_ss(tmem + st * TA_BN, umma_desc_sw128(aq + off), umma_desc_sw128(bk + off), idesc_s, kk > 0);
+        }
+        umma_commit(&s_full[st]);
+        umma_commit(&k_empty[st]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < nb; ++j) {
+        if (j + 1 < nb) issue_s(j + 1);
+        const int st = j & 1;
+        mbar_wait(p_full, j & 1);                        // P_j written (and O rescaled if needed)
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t bv = smem_u32(sV + st * TA_TILE);
+#pragma unroll
+        for (int kk = 0; kk < TA_BN / 16; ++kk) {      // over the keys: P atoms of 64, V key halves of 64
+          const uint32_t pa = ap + (kk >> 2) * (TA_TILE / 2) + (kk & 3) * 32;
+          const uint32_t vb = bv + (kk >> 2) * (TA_TILE / 2) + (kk & 3) * 2048;
+          umma_bf16_ss(tmem + 2 * TA_BN, umma_desc_sw128(pa), umma_desc_sw128_mn(vb, TA_TILE / 4), idesc_o,
+                       (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(pv_done);
+        umma_commit(&v_empty[st]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax / epilogue: thread = query row (its TMEM lane)
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    const long qrow = q0 + r;
+    float m = -1e30f, l = 0.f;
+    for (int j = 0; j < nb; ++j) {
+      const int st = j & 1;
+      const long k0 = seq0 + (long)j * TA_BN;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      float sv[TA_BN];
+#pragma unroll
+      for (int c = 0; c < TA_BN; c += 32) {
+        uint32_t u[32];
+        tmem_ld32(tq + st * TA_BN + c, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) sv[c + e] = __uint_as_float(u[e]) * scale_log2;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[st]);
+      const bool diag = j == nb - 1, tail = k0 + TA_BN > T;
+      if (diag || tail) {
+#pragma unroll
+        for (int c = 0; c < TA_BN; ++c) {
+          const long key = k0 + c;
+          if (key > qrow || key >= T) sv[c] = -INFINITY;
+        }
+      }
+      float bm = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < TA_BN; ++c) bm = fmaxf(bm, sv[c]);
+      float alpha = 1.f;
+      if (bm > m + kLazy) {                              // raise the reference max (rescale O and l)
+        alpha = exp2f(m - bm);
+        m = bm;
+      }
+      float ps = 0.f;
+      uint32_t pk[TA_BN / 2];
+#pragma unroll
+      for (int c = 0; c < TA_BN; c += 2) {
+        const float p0 = exp2f(sv[c] - m), p1 = exp2f(sv[c + 1] - m);
+        ps += p0 + p1;
+        pk[c / 2] = pack_bf16x2(p0, p1);
+      }
+      l = l * alpha + ps;
+      if (j > 0) mbar_wait(pv_done, (j - 1) & 1);        // PV_{j-1} done: P buffer and O are free
+      if (j > 0 && __any_sync(0xffffffff, alpha != 1.f)) {
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < TA_HD; c += 32) {
+          uint32_t u[32];
+          tmem_ld32(tq + 2 * TA_BN + c, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * alpha);
+          tmem_st32(tq + 2 * TA_BN + c, u);
+        }
+        tmem_st_wait();
+      }
+      // P row r: 16 chunks of 8 bf16, 128B-swizzled K-major (2 atoms of 64 keys)
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int at = c >> 3, cc = c & 7;
+        *reinterpret_cast<uint4*>(sP + at * (TA_TILE / 2) + r * 128 + ((cc ^ (r & 7)) << 4)) =
+            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      }
+      fence_proxy_async_smem_ta();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(pv_done, (nb - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    uint16_t* orow = out + qrow * (long)(Hq * TA_HD) + h * TA_HD;
+#pragma unroll
+    for (int c = 0; c < TA_HD; c += 32) {
+      uint32_t u[32];
+      tmem_ld32(tq + 2 * TA_BN + c, u);
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(__uint_as_float(u[2 * e]) * inv, __uint_as_float(u[2 * e + 1]) * inv);
+      if (qrow < T)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          st_global_v4(orow + c + 8 * e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 ta_get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static bool ta_make_map(CUtensorMap* m, const void* base, long rows, long cols, int box_rows) {
+  auto enc = ta_get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static cudaError_t launch_fa_tc(const uint16_t* qkv, uint16_t* out, int T, int Hq, int Hkv, int seq_len,
+                                cudaStream_t s) {
+  const long ld = (long)(Hq + 2 * Hkv) * TA_HD;
+  CUtensorMap mqk, mv;
+  if (!ta_make_map(&mqk, qkv, T, ld, 128) || !ta_make_map(&mv, qkv, T, ld, 64)) return cudaErrorInvalidValue;
+  static std::atomic<unsigned long long> attr{0};
+  if (cudaError_t e = ensure_smem_attr(flash_attn_tc_kernel, TA_SMEM, attr)) return e;
+  const int nseq = (T + seq_len - 1) / seq_len;
+  dim3 grid(nseq * (seq_len / TA_BM), Hq);
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)TA_HD);
+  ++g_launches;
+  flash_attn_tc_kernel<<<grid, TA_THREADS, TA_SMEM, s>>>(mqk, mv, out, T, Hq, Hkv, seq_len, scale_log2);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_flash_attn(const uint16_t* qkv, uint16_t* out, int T, int Hq, int Hkv, int hd, int seq_len,
                               cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   if (Hkv < 1 || Hq % Hkv) return cudaErrorInvalidValue;
+  // tensor-core path (HD = 128, 128-aligned sequences); FSC_ATTN_MMA_SYNC=1 forces the mma.sync one (A/B)
+  static const bool force_sync = getenv("FSC_ATTN_MMA_SYNC") && atoi(getenv("FSC_ATTN_MMA_SYNC"));
+  if (hd == TA_HD && seq_len % TA_BM == 0 && !force_sync) return launch_fa_tc(qkv, out, T, Hq, Hkv, seq_len, s);
   switch (hd) {
     case 16: return launch_fa_t<16>(qkv, out, T, Hq, Hkv, seq_len, s);
     case 32: return launch_fa_t<32>(qkv, out, T, Hq, Hkv, seq_len, s);

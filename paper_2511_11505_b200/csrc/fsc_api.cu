@@ -1055,6 +1055,18 @@ extern "C" int fsc_op_grouped_gemm_gather(fsc_ctx* ctx, int epi, const void* A, 
   return FSC_OK;
 }
 
+extern "C" int fsc_op_attention(fsc_ctx* ctx, const void* qkv, void* out, int T, int Hq, int Hkv, int hd, int seq_len,
+                                void* stream) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  REQUIRE(T >= 0 && Hkv >= 1 && Hq % Hkv == 0 && seq_len >= 1, FSC_ERR_CONFIG, "bad attention shape");
+  REQUIRE(hd == 16 || hd == 32 || hd == 64 || hd == 128, FSC_ERR_CONFIG, "head_dim must be 16/32/64/128");
+  REQUIRE(T == 0 || (qkv && out), FSC_ERR_SHAPE, "null attention buffer");
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_flash_attn(static_cast<const uint16_t*>(qkv), static_cast<uint16_t*>(out), T, Hq, Hkv, hd, seq_len,
+                       static_cast<cudaStream_t>(stream)));
+  return FSC_OK;
+}
+
 extern "C" int fsc_op_unpermute(fsc_ctx* ctx, const void* y, const int* pos, const float* w, const float* resid,
                                 float* out, int T, int k, int d, void* stream) {
   if (!ctx) return FSC_ERR_SHAPE;

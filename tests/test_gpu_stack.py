@@ -130,3 +130,29 @@ def test_zero_wo_makes_hybrid_equal_regular():
         outs.append(oL.cpu().numpy())
     np.testing.assert_array_equal(outs[0], outs[1])
     ctx.close()
+
+
+@pytest.mark.parametrize("T,Hq,Hkv,seq_len", [(640, 4, 2, 256), (600, 2, 1, 256), (384, 3, 3, 128), (1024, 2, 2, 1024),
+                                              (130, 1, 1, 128)])
+def test_attention_core_parity(T, Hq, Hkv, seq_len):
+    """Core attention (P:198 part (b) without W_o) on the GPU - the tcgen05 kernel for
+    hd = 128 - against oracle.attention_core with W_o = I on the same bf16 q, k, v: causal
+    within packed sequences, GQA head sharing, ragged last tile."""
+    from oracle import attention as oa
+    from paper_2511_11505_b200 import Context
+    from tests.gpu_util import dev_bf16, host_bf16_to_f64
+    hd = 128
+    rng = np.random.default_rng(T + Hq)
+    qkv = synth.f32_to_bf16_bits((rng.standard_normal((T, (Hq + 2 * Hkv) * hd)) * 1.5).astype(np.float32))
+    ctx = Context(d=128, n_experts=4, top_k=2, ffn=128, shared_ffn=0, max_tokens=T)
+    out = torch.zeros(T, Hq * hd, dtype=torch.bfloat16, device="cuda")
+    ctx.op_attention(dev_bf16(qkv), out, Hq, Hkv, hd, seq_len)
+    torch.cuda.synchronize()
+    f = synth.bf16_bits_to_f64(qkv)
+    q = f[:, :Hq * hd].reshape(T, Hq, hd)
+    k = f[:, Hq * hd:(Hq + Hkv) * hd].reshape(T, Hkv, hd)
+    v = f[:, (Hq + Hkv) * hd:].reshape(T, Hkv, hd)
+    ref = oa.attention_core(q, k, v, np.eye(Hq * hd), seq_len)
+    got = host_bf16_to_f64(out)
+    assert rel_l2(got, ref) < 1e-2, rel_l2(got, ref)
+    ctx.close()
