@@ -627,8 +627,8 @@ def stack_measure(ctx, shape, wd, x, L, steps, world, dev, rank, seed):
     attn = {"flop_part_a": fa, "flop_part_b": fb,
             "tflops_part_a": fa / (fs["attn_a"] * 1e-3) / 1e12 if fs.get("attn_a") else None,
             "tflops_part_b": fb / (fs["attn_b"] * 1e-3) / 1e12 if fs.get("attn_b") else None,
-            "note": "attention filler (QKV / core+o-proj) TFLOP/s inside the FarSkip stack; the core is mma.sync "
-                    "(not the hot path)"}
+            "note": "attention filler (QKV / core+o-proj) TFLOP/s inside the FarSkip stack; the core is the tcgen05 "
+                    "flash-attention kernel (hd = 128), the filler, not the graded hot path"}
     # Eq. 9: overlappable compute (attention + shared expert) minus the
     # communication it must hide, per layer, from the serialised (Regular) run's phase times
     rp = res["regular"]["phase_ms_per_layer"]
@@ -638,7 +638,7 @@ def stack_measure(ctx, shape, wd, x, L, steps, world, dev, rank, seed):
     # the same slack with the attention at its tensor-core roofline (FLOPs / measured bf16
     # peak): what a fused attention would leave to hide the all-to-all behind (P:325
     # "fused attention makes comm more critical"), so the overlap is not judged against the
-    # slow mma.sync filler alone
+    # measured filler alone
     peaks, _ = load_peaks()
     attn_roof_ms = (fa + fb) / (peaks["bf16_tflops"] * 1e12) * 1e3
     ovl_roof = attn_roof_ms + sum(rp.get(k, 0.0) for k in ("shared1", "shared2"))
