@@ -293,7 +293,7 @@ static cudaError_t launch_fa_t(const uint16_t* qkv, uint16_t* out, int T, int Hq
 // enough in fp32 / bf16 and O is rescaled in TMEM only then), then O / l -> bf16.
 namespace {
 constexpr int TA_BM = 128, TA_BN = 128, TA_HD = 128;
-constexpr int TA_THREADS = 192;
+constexpr int TA_THREADS = 320;            // warp 0 TMA, warp 1 MMA, warps 2-9 softmax (2 per lane quarter)
 constexpr int TA_TILE = TA_BM * TA_HD * 2;     // 32 KB: Q / K / V / P tiles
 constexpr int TA_SMEM = 1024 + 6 * TA_TILE + 256;
 constexpr float kLazy = 8.f;                   // log2 units: rescale O when the max grows by more
@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
   uint64_t* p_full = bar + 13;
   uint64_t* pv_done = bar + 14;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 15);
+  __shared__ float s_red[2][TA_BM];                    // the two column halves' row maxima / sums
 
   const int warp = warp_id(), lane = lane_id();
   const int h = blockIdx.y, kvh = h / (Hq / Hkv);
@@ -355,9 +356,9 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], 4);
+      mbar_init(&s_empty[s], 8);
     }
-    mbar_init(p_full, 4);
+    mbar_init(p_full, 8);
     mbar_init(pv_done, 1);
     fence_barrier_init();
   } else if (warp == 1) {
@@ -432,21 +433,25 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ---------------- softmax / epilogue: thread = query row (its TMEM lane)
-    const int q = warp & 3, r = q * 32 + lane;
+    // ---------------- softmax / epilogue: thread = query row (its TMEM lane) x one half of the
+    // 128 key columns (8 warps, two per lane quarter); the halves exchange their row maxima
+    // through shared memory, keep separate partial row sums, and each writes its half of P
+    // (one 64-key atom) and rescales / stores its half of O's 128 dims
+    const int q = warp & 3, hh = (warp - 2) >> 2, r = q * 32 + lane;
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     const long qrow = q0 + r;
+    constexpr int HC = TA_BN / 2;
     float m = -1e30f, l = 0.f;
     for (int j = 0; j < nb; ++j) {
       const int st = j & 1;
-      const long k0 = seq0 + (long)j * TA_BN;
+      const long k0 = seq0 + (long)j * TA_BN + hh * HC;
       mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
-      float sv[TA_BN];
+      float sv[HC];
 #pragma unroll
-      for (int c = 0; c < TA_BN; c += 32) {
+      for (int c = 0; c < HC; c += 32) {
         uint32_t u[32];
-        tmem_ld32(tq + st * TA_BN + c, u);
+        tmem_ld32(tq + st * TA_BN + hh * HC + c, u);
         tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; ++e) sv[c + e] = __uint_as_float(u[e]) * scale_log2;
@@ -454,65 +459,70 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[st]);
-      const bool diag = j == nb - 1, tail = k0 + TA_BN > T;
+      const bool diag = j == nb - 1, tail = k0 + HC > T;
       if (diag || tail) {
 #pragma unroll
-        for (int c = 0; c < TA_BN; ++c) {
+        for (int c = 0; c < HC; ++c) {
           const long key = k0 + c;
           if (key > qrow || key >= T) sv[c] = -INFINITY;
         }
       }
       float bm = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < TA_BN; ++c) bm = fmaxf(bm, sv[c]);
+      for (int c = 0; c < HC; ++c) bm = fmaxf(bm, sv[c]);
+      s_red[hh][r] = bm;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      bm = fmaxf(bm, s_red[hh ^ 1][r]);
+      asm volatile("bar.sync 1, 256;" ::: "memory");   // s_red is rewritten next block
       float alpha = 1.f;
       if (bm > m + kLazy) {                              // raise the reference max (rescale O and l)
         alpha = exp2f(m - bm);
         m = bm;
       }
       float ps = 0.f;
-      uint32_t pk[TA_BN / 2];
+      uint32_t pk[HC / 2];
 #pragma unroll
-      for (int c = 0; c < TA_BN; c += 2) {
+      for (int c = 0; c < HC; c += 2) {
         const float p0 = exp2f(sv[c] - m), p1 = exp2f(sv[c + 1] - m);
         ps += p0 + p1;
         pk[c / 2] = pack_bf16x2(p0, p1);
       }
-      l = l * alpha + ps;
+      l = l * alpha + ps;                                // this half's partial row sum
       if (j > 0) mbar_wait(pv_done, (j - 1) & 1);        // PV_{j-1} done: P buffer and O are free
       if (j > 0 && __any_sync(0xffffffff, alpha != 1.f)) {
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < TA_HD; c += 32) {
+        for (int c = 0; c < TA_HD / 2; c += 32) {
           uint32_t u[32];
-          tmem_ld32(tq + 2 * TA_BN + c, u);
+          tmem_ld32(tq + 2 * TA_BN + hh * (TA_HD / 2) + c, u);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * alpha);
-          tmem_st32(tq + 2 * TA_BN + c, u);
+          tmem_st32(tq + 2 * TA_BN + hh * (TA_HD / 2) + c, u);
         }
         tmem_st_wait();
       }
-      // P row r: 16 chunks of 8 bf16, 128B-swizzled K-major (2 atoms of 64 keys)
+      // this half of P row r: atom hh (keys hh*64 ..), 8 chunks of 8 bf16, 128B-swizzled
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int at = c >> 3, cc = c & 7;
-        *reinterpret_cast<uint4*>(sP + at * (TA_TILE / 2) + r * 128 + ((cc ^ (r & 7)) << 4)) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      }
+      for (int cc = 0; cc < 8; ++cc)
+        *reinterpret_cast<uint4*>(sP + hh * (TA_TILE / 2) + r * 128 + ((cc ^ (r & 7)) << 4)) =
+            make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
       fence_proxy_async_smem_ta();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
     }
+    s_red[hh][r] = l;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const float lt = s_red[0][r] + s_red[1][r];
     mbar_wait(pv_done, (nb - 1) & 1);
     tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    uint16_t* orow = out + qrow * (long)(Hq * TA_HD) + h * TA_HD;
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    uint16_t* orow = out + qrow * (long)(Hq * TA_HD) + h * TA_HD + hh * (TA_HD / 2);
 #pragma unroll
-    for (int c = 0; c < TA_HD; c += 32) {
+    for (int c = 0; c < TA_HD / 2; c += 32) {
       uint32_t u[32];
-      tmem_ld32(tq + 2 * TA_BN + c, u);
+      tmem_ld32(tq + 2 * TA_BN + hh * (TA_HD / 2) + c, u);
       tmem_ld_wait();
       uint32_t pk[16];
 #pragma unroll
