@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
         tmem_ld32(tq + st * TA_BN + hh * HC + c, u);
         tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) sv[c + e] = __uint_as_float(u[e]) * scale_log2;
+        for (int e = 0; e < 32; ++e) sv[c + e] = __uint_as_float(u[e]);   // raw scores (scale > 0 folded below)
       }
       tc_fence_before();
       __syncwarp();
@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       float bm = -INFINITY;
 #pragma unroll
       for (int c = 0; c < HC; ++c) bm = fmaxf(bm, sv[c]);
+      bm *= scale_log2;                                  // max of the scaled scores
       s_red[hh][r] = bm;
       asm volatile("bar.sync 1, 256;" ::: "memory");
       bm = fmaxf(bm, s_red[hh ^ 1][r]);
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       uint32_t pk[HC / 2];
 #pragma unroll
       for (int c = 0; c < HC; c += 2) {
-        const float p0 = exp2f(sv[c] - m), p1 = exp2f(sv[c + 1] - m);
+        const float p0 = exp2f(fmaf(sv[c], scale_log2, -m)), p1 = exp2f(fmaf(sv[c + 1], scale_log2, -m));
         ps += p0 + p1;
         pk[c / 2] = pack_bf16x2(p0, p1);
       }
