@@ -21,8 +21,9 @@ def launches(csv_path, out_md):
     h = rows[hi]
     ki, vi, ii = h.index("Kernel Name"), h.index("Metric Value"), h.index("ID")
     ks = [(int(r[ii]), short(r[ki]), float(r[vi]) / 1e3) for r in rows[hi + 1:] if len(r) == len(h)]
-    # one step = from one router_kernel launch to the next
-    starts = [i for i, (_, n, _) in enumerate(ks) if "router_kernel<" in n]
+    # one step = from one router launch (its first kernel: the W' quantisation of the
+    # tensor-core router, or the SIMT router's prescale) to the next
+    starts = [i for i, (_, n, _) in enumerate(ks) if "router_tc_quant_w" in n or "router_prescale" in n]
     step = ks[starts[-2]:starts[-1]] if len(starts) >= 2 else ks
     tot = sum(t for _, _, t in step)
     lines = [f"# Launch list of one bench step (ncu gpu__time_duration.sum, --clock-control none)",
