@@ -772,7 +772,7 @@ constexpr int TC_THREADS = 64 + 32 * TC_WORKERS;       // 320
 constexpr int TC_A_PLANE = TC_BM * TC_BK;              // 8 KB (64-byte rows)
 constexpr int TC_XBOX = TC_BM * TC_BK * 4;             // 32 KB: 128 rows x 64 fp32
 constexpr int TC_NXS = 3;                              // x boxes in flight
-constexpr int TC_MAX_CS = 8;
+constexpr int TC_MAX_CS = 16;                         // 16: non-portable cluster size (small T)
 constexpr float kTcMagic = 12582912.0f;                // 1.5 * 2^23
 
 template <int EP>
@@ -833,6 +833,7 @@ FSC_DEVINL void st_cluster_v2_f64(uint32_t a, double x, double y) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1,%2};" ::"r"(a), "d"(x), "d"(y) : "memory");
 }
 FSC_DEVINL void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+FSC_DEVINL void cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 FSC_DEVINL void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 FSC_DEVINL void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 FSC_DEVINL void worker_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_WORKERS) : "memory"); }
@@ -1602,8 +1603,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // every CTA's partial sum over its d-slice, v = sum_a acc_a 2^-(14 + 7a), is exact in fp64
     // (a multiple of 2^-35 below 2^13), and so is any sum of them: the owner adds the CS
     // partials in rank order and the result is the full-d value, bit for bit
+    // (no barrier before the local stores: only this CTA's own TMA and MMAs used this shared
+    // memory, and they are complete once tfull fired)
     double* part = reinterpret_cast<double*>(smem);      // this CTA's partials [tile row][RSTRD]
-    cluster_sync();                                      // every CTA of the cluster is done with its stages
     if (warp >= 2) {                                     // my partials, expert half `half`, local stores
       double* dst = part + trow * C::RSTRD;
 #pragma unroll 1
@@ -1639,8 +1641,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         lg[lr * C::LGS + e] = (float)(sc * (double)sh.se[e] * v0);
         lg[lr * C::LGS + e + 1] = (float)(sc * (double)sh.se[e + 1] * v1);
       }
+      cluster_arrive_release();                          // done reading the peers' partials; the wait
+    } else {                                             // comes before this CTA overwrites / leaves
+      cluster_sync();
     }
-    cluster_sync();                                      // no CTA leaves while its partials are read
   }
   tc_fence_before();
   __syncthreads();                                       // logits of the owned rows in shared memory
@@ -1676,9 +1680,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   worker_bar();
   TCSTAMP(6);
   const int nf = sh.nflag;
+  constexpr bool kInRecv = sizeof(TcRefine) <= (size_t)C::RECV;
+  bool waited = CS == 1;
   if (nf > 0) {                                          // block-uniform
-    // refinement scratch: the receive buffer (free by now) when it is large enough, else after the logits
-    constexpr bool kInRecv = sizeof(TcRefine) <= (size_t)C::RECV;
+    // refinement scratch: the partials buffer (once every peer has read it) when it is large
+    // enough, else after the logits
+    if (!waited && kInRecv) {
+      cluster_wait();
+      waited = true;
+    }
     uint8_t* rbase = (CS > 1 && kInRecv) ? smem : smem + (CS > 1 ? C::RECV : 0) + RPO * C::LGS * 4;
     static_assert((kInRecv || C::RECV + (TC_BM / 2) * C::LGS * 4 + sizeof(TcRefine) <= (size_t)C::BYTES) &&
                       TC_BM * C::LGS * 4 + sizeof(TcRefine) <= (size_t)C::BYTES,
@@ -1686,6 +1696,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     TcRefine& R = *reinterpret_cast<TcRefine*>(rbase);
     refine_tc<QN>(L, lg, C::LGS, sh.flist, sh.thr, nf, t0 + own0, wk, lane, R, &sh.np);
   }
+  if (!waited) cluster_wait();                           // no CTA leaves while its partials are read
 #ifdef FSC_ROUTER_PROF
   worker_bar();
   TCSTAMP(7);
@@ -1718,15 +1729,17 @@ static bool tc_make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Cluster size: the largest power of two (<= 8, dividing the 64-column k-blocks) that keeps
-// the grid within one wave of the SMs (one CTA per SM); FSC_ROUTER_CS overrides (A/B runs).
+// Cluster size: the largest power of two (<= 16, dividing the 64-column k-blocks, leaving each
+// CTA >= 4 of them) that keeps the grid within one wave of the SMs (one CTA per SM); 16 is a
+// non-portable cluster size (Scout decode: d = 5120). FSC_ROUTER_CS overrides (A/B runs).
 static int router_tc_cluster(int T, int d) {
   const int tiles = (T + TC_BM - 1) / TC_BM, nkb = d / TC_BK;
   int cs = 0;
   if (const char* env = getenv("FSC_ROUTER_CS")) cs = atoi(env);
   if (cs >= 1 && cs <= TC_MAX_CS && !(cs & (cs - 1)) && nkb % cs == 0) return cs;
   cs = 1;
-  while (2 * cs <= TC_MAX_CS && nkb % (2 * cs) == 0 && (long)tiles * 2 * cs <= kNumSMs) cs *= 2;
+  while (2 * cs <= TC_MAX_CS && nkb % (2 * cs) == 0 && nkb / (2 * cs) >= 4 && (long)tiles * 2 * cs <= kNumSMs)
+    cs *= 2;   // (>= 4 k-blocks per CTA: below that the cluster exchange costs more than it saves)
   return cs;
 }
 
@@ -1742,7 +1755,20 @@ static cudaError_t launch_router_tc_t(const RouterLaunch& L, cudaStream_t s) {
     return cudaErrorInvalidValue;
   static std::atomic<unsigned long long> attr{0};
   if (cudaError_t e = ensure_smem_attr(router_tc_kernel<EP>, C::SMEM, attr)) return e;
-  const int cs = router_tc_cluster(L.T, L.d);
+  int cs = router_tc_cluster(L.T, L.d);
+  if (cs > 8) {
+    static std::atomic<unsigned long long> np{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(np.load() & bit)) {
+      if (cudaFuncSetAttribute(router_tc_kernel<EP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
+        np.fetch_or(bit);
+      else
+        cs = 8;
+    }
+    if (cs > 8 && !(np.load() & bit)) cs = 8;
+  }
   const int tiles = (L.T + TC_BM - 1) / TC_BM;
   router_tc_quant_w_kernel<<<EP, TC_QW_THREADS, 0, s>>>(L, EP);
   cudaLaunchConfig_t cfg = {};
