@@ -198,6 +198,15 @@ FSC_API int fsc_set_gemm_dynamic(fsc_ctx* ctx, int on);
  * wherever the shape allows it; 0: the fp32 SIMT router. The digit workspace
  * (3 x 128 x d int8) is allocated at fsc_init. */
 FSC_API int fsc_set_router_int8(fsc_ctx* ctx, int on);
+/* Router (K1) for small batches in fp64 (router_f64_kernel; d % 64 == 0, d <= 8192,
+ * E <= 128): the same definition (RMSNorm C-amb-5; top-k, exact ties to the
+ * lower id, slots ascending by id, renormalised gates) with every product and sum in
+ * fp64 in a fixed order, so the selection is the fp64 oracle's with no error bound or
+ * refinement (n_refined is not written). on = 1: every call; 0: never; -1 (default,
+ * auto): calls with T x EP x d <= 2e8 (EP = E padded to 32 / 64 / 128: decode batches) unless fsc_set_router_int8(ctx, 0) selected the
+ * fp32 SIMT router. Workspace (d x 136 doubles, gamma (.) W_R) allocated at fsc_init. Returns FSC_ERR_CONFIG for on = 1 on an unsupported
+ * shape. */
+FSC_API int fsc_set_router_f64(fsc_ctx* ctx, int on);
 /* Select the EP data movement (FSC_EP_ALLTOALL default, FSC_EP_ALLREDUCE). Must be
  * called before fsc_bootstrap_export (it re-creates the peer region). In
  * FSC_EP_ALLREDUCE the shared expert is computed replicated on every rank (no

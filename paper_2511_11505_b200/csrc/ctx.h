@@ -33,6 +33,7 @@ struct fsc_ctx {
   int ep_mode = 0;             // FSC_EP_ALLTOALL (dispatch / combine) or FSC_EP_ALLREDUCE (replicated tokens)
   int gemm_dyn = -1;           // dynamic GEMM tile schedule: 1 on, 0 off, -1 auto (EP > 1)
   int router_i8 = -1;          // exact int8 tensor-core router: 1 on, 0 off, -1 auto (fsc_set_router_int8)
+  int router_f64 = -1;         // fp64 small-batch router: 1 on, 0 off, -1 auto (fsc_set_router_f64)
   int gather_a = 0;            // EP = 1: GEMM1 gathers A through src_row (fused permute)
   int combine_mode = 0;        // FSC_COMBINE_STREAM (comm-stream push after GEMM2) or FSC_COMBINE_FUSED
   int blocking_mode = 0;       // fsc_moe_forward_blocking: FSC_BLOCKING_REGULAR_PLUS or FSC_BLOCKING_SERIAL
@@ -65,6 +66,7 @@ struct fsc_ctx {
   float* r_part = nullptr;     // [kRouterSplitRows, 128] split-d partial logits (small T)
   double* r_part_sq = nullptr; // [kRouterSplitRows]      split-d partial sums of x^2
   float* w_scaled = nullptr;   // [E, d]             gamma * W_R
+  double* f64_w = nullptr;     // [d, 136]           fp64 router: gamma (.) W_R, k-major (E <= 128)
   float* w_sq = nullptr;       // [E]                ||gamma * W_R[e]||^2
   uint16_t* xs = nullptr;      // bf16 [T*k, d]      expert-sorted send buffer
   uint16_t* h = nullptr;       // bf16 [max_recv, c] SwiGLU activations
@@ -153,6 +155,8 @@ inline int* gemm_sched_slot(const fsc_ctx* ctx, int slot) {
 }
 // the exact tensor-core router (router_tc_kernel) is used for this context's forward and backward
 bool router_tc_on(const fsc_ctx* ctx);
+// fp64 small-batch router for this call (fsc_set_router_f64: forced, off, or auto = T small)
+bool router_f64_on(const fsc_ctx* ctx, int T, int d, int E, int k);
 int fsc_check_finite(fsc_ctx* ctx, const float* out, long n, cudaStream_t s, const char* what);
 
 // transport (EP > 1). All return fsc_status.

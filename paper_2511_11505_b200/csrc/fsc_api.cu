@@ -165,6 +165,7 @@ extern "C" int fsc_init(fsc_ctx** out, int rank, int ep_size, int device, const 
   CK(dalloc(&ctx->r_part_sq, (long)kRouterSplitRows));
   CK(dalloc(&ctx->w_scaled, (E > 128 ? E : 128) * d));  // e-major [E][d] or k-major [d][EP<=128]
   CK(dalloc(&ctx->w_sq, E));
+  if (E <= 128) CK(dalloc(&ctx->f64_w, (long)d * 136));
   CK(dalloc(&ctx->xs, (T * k > ctx->max_recv ? T * k : ctx->max_recv) * d));
   CK(dalloc(&ctx->h, ctx->max_recv * (long)c.ffn));
   CK(dalloc(&ctx->y, (T * k > ctx->max_recv ? T * k : ctx->max_recv) * d));
@@ -204,7 +205,7 @@ extern "C" int fsc_finalize(fsc_ctx* ctx) {
   cudaDeviceSynchronize();
   fsc_transport_finalize(ctx);
   void* bufs[] = {ctx->xn, ctx->topk_idx, ctx->topk_w, ctx->pos, ctx->src_row, ctx->hist, ctx->base, ctx->counts,
-                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->gemm_sched, ctx->i8_w, ctx->i8_exp, ctx->w_scaled, ctx->w_sq, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2], ctx->nf_count, ctx->b_gb, ctx->b_duv, ctx->b_hg, ctx->b_dgpart, ctx->b_dlrow, ctx->b_rtok, ctx->b_gr, ctx->b_gate, ctx->b_colpart};
+                  ctx->offsets, ctx->xs, ctx->h, ctx->y, ctx->hs, ctx->tmp, ctx->io_in, ctx->io_out, ctx->r_part, ctx->r_part_sq, ctx->comb_cnt, ctx->gemm_sched, ctx->i8_w, ctx->i8_exp, ctx->w_scaled, ctx->w_sq, ctx->f64_w, ctx->hn, ctx->qkv, ctx->ao, ctx->rbuf[0], ctx->rbuf[1], ctx->rbuf[2], ctx->nf_count, ctx->b_gb, ctx->b_duv, ctx->b_hg, ctx->b_dgpart, ctx->b_dlrow, ctx->b_rtok, ctx->b_gr, ctx->b_gate, ctx->b_colpart};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -417,6 +418,26 @@ bool router_tc_on(const fsc_ctx* ctx) {
   return ctx->i8_w && router_i8_ok(ctx) && ctx->router_i8 != 0;
 }
 
+// The fp64 router (router_f64_kernel) for small batches, where the tensor-core router's
+// phases are latency-bound: auto = T x EP x d <= 2e8 fp64 FMAs (EP = E padded to 32 / 64 /
+// 128; measured crossover: Qwen3 ~768 tokens, DS-V2-Lite ~1500, Scout ~1200) unless the fp32
+// SIMT router was selected (fsc_set_router_int8(ctx, 0), the A/B reference); on = any T.
+bool router_f64_on(const fsc_ctx* ctx, int T, int d, int E, int k) {
+  if (ctx->router_f64 == 0 || !ctx->f64_w || !router_f64_supported(d, E, k)) return false;
+  if (ctx->router_f64 > 0) return true;
+  const long ep = E <= 32 ? 32 : E <= 64 ? 64 : 128;
+  return ctx->router_i8 != 0 && (double)T * ep * d <= 2e8;
+}
+
+extern "C" int fsc_set_router_f64(fsc_ctx* ctx, int on) {
+  if (!ctx) return FSC_ERR_SHAPE;
+  const fsc_moe_config& c = ctx->cfg;
+  REQUIRE(on <= 0 || router_f64_supported(c.d, c.n_experts, c.top_k), FSC_ERR_CONFIG,
+          "fp64 router needs d %% 64 == 0, d <= 8192, E <= 128");
+  ctx->router_f64 = on < 0 ? -1 : (on ? 1 : 0);
+  return FSC_OK;
+}
+
 extern "C" int fsc_set_router_int8(fsc_ctx* ctx, int on) {
   if (!ctx) return FSC_ERR_SHAPE;
   if (!on) {
@@ -514,6 +535,8 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
                     dbg ? dbg->logits : nullptr, dbg ? dbg->n_refined : nullptr,
                     ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, TB_DEFAULT,
                     ctx->i8_w, ctx->i8_exp, router_tc_on(ctx) ? 1 : 0};
+    rl.f64 = router_f64_on(ctx, T, d, E, k) ? 1 : 0;
+    rl.f64_w = ctx->f64_w;
     CK(launch_router(rl, s));
   }
   PH_END(PH_ROUTER);
@@ -1004,6 +1027,8 @@ extern "C" int fsc_op_router(fsc_ctx* ctx, const float* x, const float* gamma, c
   RouterLaunch rl{x, gamma, w_router, T, d, E, k, ctx->cfg.rms_eps, static_cast<uint16_t*>(xn), topk_idx, topk_w,
                   logits, n_refined, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, TB_DEFAULT,
                   ctx->i8_w, ctx->i8_exp, (router_tc_on(ctx) && d == ctx->cfg.d && E <= 128) ? 1 : 0};
+  rl.f64 = router_f64_on(ctx, T, d, E, k) ? 1 : 0;
+  rl.f64_w = ctx->f64_w;
   CK(launch_router(rl, static_cast<cudaStream_t>(stream)));
   return FSC_OK;
 }

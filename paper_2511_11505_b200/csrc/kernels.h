@@ -142,10 +142,15 @@ struct RouterLaunch {
   int8_t* i8_w;          // workspace [3, EP, d]: base-2^7 digit planes of floor((gamma W_R)_e 2^21 / s_e)
   float* i8_exp;         // workspace [3, EP]: s_e and the two per-expert error-bound coefficients
   int tc;
+  int f64 = 0;           // fp64 small-batch router (router_f64_kernel), chosen by the caller
+  double* f64_w = nullptr;  // its workspace [d, 136]: gamma (.) W_R in fp64, k-major
 };
 // split-d partials: (token blocks) x (d splits) <= 2 x 148 CTAs of <= 32 rows
 constexpr int kRouterSplitRows = 2 * 148 * 32;
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s);
+// fp64 router for small batches (router_f64.cu): d % 64 == 0, d <= 8192, E <= 128
+bool router_f64_supported(int d, int E, int k);
+cudaError_t launch_router_f64(const RouterLaunch& L, cudaStream_t s);
 
 // K2: deterministic histogram / scan / positions
 //   hist   [n_chunks, E] per 32-token chunk; base [n_chunks, E]

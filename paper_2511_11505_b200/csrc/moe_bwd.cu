@@ -316,6 +316,8 @@ extern "C" int fsc_moe_backward(fsc_ctx* ctx, const fsc_moe_weights* w, int T, c
   RouterLaunch rl{x_in, w->gamma, w->w_router, T, d, E, k, c.rms_eps, ctx->xn, ctx->topk_idx, ctx->topk_w,
                   nullptr, nullptr, ctx->r_part, ctx->r_part_sq, ctx->w_scaled, ctx->w_sq, 32,
                   ctx->i8_w, ctx->i8_exp, router_tc_on(ctx) ? 1 : 0};   // the forward's router
+  rl.f64 = router_f64_on(ctx, T, d, E, k) ? 1 : 0;
+  rl.f64_w = ctx->f64_w;
   BCK(launch_router(rl, s));
   PermLaunch pl{ctx->topk_idx, T, k, E, ctx->hist, ctx->base, ctx->counts, ctx->offsets, ctx->pos, ctx->src_row};
   BCK(launch_perm_maps(pl, s));

@@ -1843,6 +1843,7 @@ static cudaError_t launch_router_t(const RouterLaunch& L, cudaStream_t s) {
 
 cudaError_t launch_router(const RouterLaunch& L, cudaStream_t s) {
   if (L.T == 0) return cudaSuccess;
+  if (L.f64) return launch_router_f64(L, s);
   if (L.d % DC || L.d > kMaxD || L.E < 1 || L.E > 128 || L.k < 1 || L.k > L.E) return cudaErrorInvalidValue;
   if (!L.part || !L.part_sq || !L.w_scaled || !L.w_sq)
     return cudaErrorInvalidValue;

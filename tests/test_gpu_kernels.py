@@ -203,6 +203,17 @@ def ctx_i8():
     from paper_2511_11505_b200 import Context
     c = Context(d=5120, n_experts=128, top_k=8, ffn=128, shared_ffn=0, max_tokens=16384)
     c.set_router_int8(True)
+    c.set_router_f64(False)   # the tensor-core kernel at every T (auto would pick fp64 at T <= 1024)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_f64():
+    """The fp64 small-batch router (router_f64_kernel), forced at every T."""
+    from paper_2511_11505_b200 import Context
+    c = Context(d=5120, n_experts=128, top_k=8, ffn=128, shared_ffn=0, max_tokens=16384)
+    c.set_router_f64(True)
     yield c
     c.close()
 
@@ -229,6 +240,33 @@ def test_router_parity_int8(ctx_i8, name, T):
     # E = 128, k = 8: ~4.4% of the tokens are within the band)
     E = synth.CONFIGS[name].n_experts
     assert nref <= max(4, T * E // 1600), (nref, T, E)
+
+
+@pytest.mark.parametrize("name,T", ROUTER_CASES + [("qwen3", 7), ("dsv2lite", 33), ("scout", 65), ("qwen3", 1000),
+                                                 ("qwen3", 1025), ("scout", 512), ("dsv2lite", 300)])
+def test_router_parity_f64(ctx_f64, name, T):
+    """fp64 router (every product and sum in fp64, fixed order): the oracle's selection
+    with no refinement; logits are fp64 values rounded once to fp32."""
+    nref, e_max = _router_parity(ctx_f64, name, T)
+    assert nref == 0
+    assert e_max < 2e-6
+
+
+@pytest.mark.parametrize("simt", ["0", "1"])
+@pytest.mark.parametrize("plan", ["4,1", "4,2", "2,4", "1,8", "1,16", "2,16"])
+def test_router_f64_every_tile_and_cluster_shape(ctx_f64, plan, simt, monkeypatch):
+    """Every (token-tile height, cluster size) the cost model can pick, forced through
+    FSC_ROUTER_F64_PLAN, on ragged batches of the Qwen3 / DS / Scout router shapes, with
+    the fp64 tensor-core (DMMA) contraction and the DFMA one (FSC_ROUTER_F64_SIMT)."""
+    monkeypatch.setenv("FSC_ROUTER_F64_PLAN", plan)
+    monkeypatch.setenv("FSC_ROUTER_F64_SIMT", simt)
+    for name, T in (("qwen3", 77), ("dsv2lite", 45), ("scout", 70)):
+        _router_parity(ctx_f64, name, T)
+
+
+@pytest.mark.parametrize("skew", [synth.SKEW_DEFAULT])
+def test_router_parity_f64_skewed(ctx_f64, skew):
+    _router_parity(ctx_f64, "dsv2lite", 512, skew)
 
 
 def _router_parity(ctx, name, T, skew=0.0):
@@ -270,9 +308,9 @@ def dataclass_replace_small(shape):
     return dataclasses.replace(shape, ffn=1, shared_ffn=0)
 
 
-@pytest.mark.parametrize("which", ["simt", "tc"])
-def test_router_exact_ties_go_to_lower_index(ctx, ctx_i8, which):
-    ctx = ctx if which == "simt" else ctx_i8
+@pytest.mark.parametrize("which", ["simt", "tc", "f64"])
+def test_router_exact_ties_go_to_lower_index(ctx, ctx_i8, ctx_f64, which):
+    ctx = {"simt": ctx, "tc": ctx_i8, "f64": ctx_f64}[which]
     rng = np.random.default_rng(5)
     T, d, E, k = 64, 128, 16, 3
     x = rng.standard_normal((T, d)).astype(np.float32)
@@ -307,6 +345,32 @@ def test_router_all_experts_tied(ctx_i8):
     np.testing.assert_array_equal(idx.cpu().numpy(), np.tile(np.arange(k, dtype=np.int32), (T, 1)))
     np.testing.assert_allclose(gw.cpu().numpy(), 1.0 / k, rtol=0, atol=1e-6)
     assert int(nref.item()) == T
+
+
+def test_router_f64_all_tied_and_non_finite(ctx_f64):
+    """fp64 router: every logit of a token tied -> experts 0..k-1, gates 1/k; a token with a
+    non-finite input still gets k valid, distinct ids and finite gates summing to 1."""
+    rng = np.random.default_rng(6)
+    T, d, E, k = 300, 256, 128, 8
+    x = rng.standard_normal((T, d)).astype(np.float32)
+    gamma = (1.0 + 0.1 * rng.standard_normal(d)).astype(np.float32)
+    W = np.repeat((rng.standard_normal((1, d)) / np.sqrt(d)).astype(np.float32), E, axis=0)
+    xn = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    gw = torch.empty(T, k, dtype=torch.float32, device="cuda")
+    ctx_f64.op_router(dev_f32(x), dev_f32(gamma), dev_f32(W), k, xn, idx, gw)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(idx.cpu().numpy(), np.tile(np.arange(k, dtype=np.int32), (T, 1)))
+    np.testing.assert_allclose(gw.cpu().numpy(), 1.0 / k, rtol=0, atol=1e-7)
+    W = (rng.standard_normal((E, d)) / np.sqrt(d)).astype(np.float32)
+    x[3, 7] = np.nan
+    x[5, 1] = np.inf
+    ctx_f64.op_router(dev_f32(x), dev_f32(gamma), dev_f32(W), k, xn, idx, gw)
+    torch.cuda.synchronize()
+    gi, g = idx.cpu().numpy(), gw.cpu().numpy()
+    assert np.all((gi >= 0) & (gi < E))
+    assert all(len(set(row)) == k and list(row) == sorted(row) for row in gi)
+    assert np.all(np.isfinite(g)) and np.allclose(g.sum(1), 1.0, atol=1e-6)
 
 
 # ----------------------------------------------------------------------------- K2 / K3 / K5

@@ -269,8 +269,9 @@ def test_fused_unpermute_is_bitwise_identical(name, T):
     ctx.close()
 
 
+@pytest.mark.parametrize("router", ["tc", "f64"])
 @pytest.mark.parametrize("name,T", [("dsv2lite", 512), ("scout", 300), ("qwen3", 2048)])
-def test_int8_router_moe_parity(name, T):
+def test_int8_router_moe_parity(name, T, router):
     """The whole MoE block with the int8 tensor-core router: routing bit-exact against
     the fp64 oracle and the output within tolerance; identical to the SIMT-router run
     whenever both select the same experts (they do here: both equal the oracle)."""
@@ -282,6 +283,7 @@ def test_int8_router_moe_parity(name, T):
     ctx.set_router_int8(False)                          # fp32 SIMT router
     ref_out, ref_dbg = run_blocking(ctx, wd, x)
     ctx.set_router_int8(True)
+    ctx.set_router_f64(router == "f64")                 # fp64 router / tensor-core router at any T
     out, dbg = run_blocking(ctx, wd, x)
     ctx.close()
     np.testing.assert_array_equal(dbg["topk_idx"], ref_dbg["topk_idx"])
