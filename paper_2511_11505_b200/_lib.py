@@ -79,6 +79,7 @@ _SIGS = {
     "fsc_set_gemm_gather": (_I, [_P, _I]),
     "fsc_set_fused_unpermute": (_I, [_P, _I]),
     "fsc_set_router_int8": (_I, [_P, _I]),
+    "fsc_set_router_f64": (_I, [_P, _I]),
     "fsc_set_gemm_dynamic": (_I, [_P, _I]),
     "fsc_set_ep_mode": (_I, [_P, _I]),
     "fsc_set_dispatch_fp8": (_I, [_P, _I]),
@@ -328,6 +329,11 @@ class Context:
         k <= 8): True / None (auto, the default: wherever the shape allows) or False (the fp32
         SIMT router)."""
         self._ck(self.lib.fsc_set_router_int8(self.h, -1 if on is None else int(on)))
+
+    def set_router_f64(self, on):
+        """fp64 small-batch router (router_f64_kernel): True (every call), False (never) or
+        None (auto, the default: T x EP x d <= 2e8 unless the fp32 SIMT router was selected)."""
+        self._ck(self.lib.fsc_set_router_f64(self.h, -1 if on is None else int(on)))
 
     def set_fused_unpermute(self, on):
         """Blocking EP = 1: gate-weighted unpermute fused into the down GEMM epilogue
