@@ -72,6 +72,17 @@ FSC_DEVINL void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+#ifdef FSC_ROUTER_PROF   // per-CTA phase stamps (%globaltimer) into L.logits (tools/router_f64_prof.py)
+#define F64STAMP(kk)                                                                          \
+  if (threadIdx.x == 0) {                                                                     \
+    unsigned long long g__;                                                                   \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g__));                                   \
+    reinterpret_cast<unsigned long long*>(L.logits)[blockIdx.x * 8 + (kk)] = g__;             \
+  }
+#else
+#define F64STAMP(kk)
+#endif
+
 template <int EP, int WT>
 struct F64Cfg {
   static constexpr int TE = EP / 32;                // experts per lane (SIMT variant)
@@ -104,6 +115,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
   __shared__ double s_r[C::TT];       // r_t (identical in every CTA of the cluster)
   __shared__ __align__(8) uint64_t s_full[2];   // W' chunk buffers filled (bulk copy tx)
 
+  F64STAMP(0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = cs > 1 ? (int)cluster_ctarank() : 0;
   const int tile = blockIdx.x / cs;
@@ -166,6 +178,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
   }
   stage(0);
   __syncthreads();
+  F64STAMP(1);
   for (int ch = 0; ch < nch; ++ch) {
     const int b = ch & 1;
     if (ch + 1 < nch) {
@@ -216,6 +229,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
     __syncthreads();
   }
 
+  F64STAMP(2);
   // ---- this CTA's partials: [kp][token][EP] over the W' buffers (free after the last sync),
   // then summed over kp (ascending) into slot 0 so the cluster reduction reads one value
   double* part = wbuf;
@@ -245,6 +259,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
   }
   __syncthreads();
   if (cs > 1) cluster_sync();   // every CTA's partials and sums are in its shared memory
+  F64STAMP(3);
 
   // ---- r_t of every token of the tile (rank order: the same value in every CTA); the
   // remote loads are all issued before the adds (one DSMEM latency, not cs of them)
@@ -295,15 +310,18 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
       v0 *= r;
       v1 *= r;
       const long tg = t0 + t;
+#ifndef FSC_ROUTER_PROF
       if (L.logits && tg < T) {
         if (e < E) L.logits[tg * E + e] = (float)v0;
         if (e + 1 < E) L.logits[tg * E + e + 1] = (float)v1;
       }
+#endif
       lg[i * EP + e] = sanitize(v0);
       lg[i * EP + e + 1] = sanitize(v1);
     }
   }
   __syncthreads();
+  F64STAMP(4);
   if (cs > 1) cl_arrive_release();   // done reading the peers (their exit waits for it)
 
   // ---- selection: one warp per owned token; rank_e = #{e' : l_e' > l_e or (= and e' < e)}
@@ -320,30 +338,38 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
       v[j] = lane + 32 * j < E ? row[lane + 32 * j] : -INFINITY;   // (non-finite logits: -DBL_MAX)
       sel[j] = false;
     }
-    // k rounds of a warp argmax over (value desc, id asc) of the unselected experts
+    // k rounds of a warp argmax over (value desc, id asc) of the unselected experts: the
+    // order-preserving 64-bit key of the fp64 value (0 = unavailable), reduced exactly in
+    // three warp reductions (high word, low word, lowest id among the equal keys)
+    unsigned long long key[C::TE];
+#pragma unroll
+    for (int j = 0; j < C::TE; ++j) {
+      const unsigned long long u = (unsigned long long)__double_as_longlong(v[j]);
+      key[j] = lane + 32 * j < E ? ((u >> 63) ? ~u : (u | 0x8000000000000000ull)) : 0ull;
+    }
     double vmax = 0.0;
     for (int r = 0; r < k; ++r) {
-      double bv = -INFINITY;
-      int bi = 0x7fffffff;
+      unsigned long long bk = 0ull;
+      int bj = -1;
 #pragma unroll
       for (int j = 0; j < C::TE; ++j)
-        if (!sel[j] && lane + 32 * j < E && (v[j] > bv || bi == 0x7fffffff)) {
-          bv = v[j];
-          bi = lane + 32 * j;
+        if (!sel[j] && key[j] > bk) {
+          bk = key[j];
+          bj = j;
         }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-        }
+      const uint32_t hi = (uint32_t)(bk >> 32), lo = (uint32_t)bk;
+      const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+      const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      const bool cand = bj >= 0 && hi == mh && lo == ml;
+      const uint32_t wid = __reduce_min_sync(0xffffffffu, cand ? (uint32_t)(lane + 32 * bj) : 0xffffffffu);
+      if (r == 0) {
+        const unsigned long long wk = ((unsigned long long)mh << 32) | ml;
+        const unsigned long long ub = (wk >> 63) ? (wk & 0x7fffffffffffffffull) : ~wk;
+        vmax = __longlong_as_double((long long)ub);
       }
-      if (r == 0) vmax = bv;
 #pragma unroll
       for (int j = 0; j < C::TE; ++j)
-        if (bi == lane + 32 * j) sel[j] = true;
+        if (wid == (uint32_t)(lane + 32 * j)) sel[j] = true;
     }
     int slot0[C::TE + 1];
     slot0[0] = 0;
@@ -368,6 +394,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
     }
   }
 
+  F64STAMP(5);
   // ---- xn = bf16(x gamma r) of this CTA's d-slice (x re-read, L2 hits; 8 loads in flight)
   {
     const int dv = dsl / 4, n = C::TT * dv;
@@ -392,7 +419,9 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
       }
     }
   }
+  F64STAMP(6);
   if (cs > 1) cl_wait();   // no CTA leaves while a peer may still read its partials
+  F64STAMP(7);
 }
 
 // W'T[i][e] = gamma_i W_R[e][i] in fp64 (exact: a product of two fp32 values), zero for
@@ -401,20 +430,41 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
 // first W' copy.
 __global__ void __launch_bounds__(256) router_f64_prep_kernel(const float* __restrict__ W,
                                                               const float* __restrict__ gamma, int E, int d, int WS,
-                                                              double* __restrict__ wt) {
+                                                              double* __restrict__ wt
+#ifdef FSC_ROUTER_PROF
+                                                              , unsigned long long* st
+#endif
+) {
   gdc_launch();
+#ifdef FSC_ROUTER_PROF
+  unsigned long long g0__;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0__));
+  if (threadIdx.x == 0) atomicMin(st + 148 * 64 - 2, g0__);
+#endif
   constexpr int PC = 16;   // columns per CTA (d / 16 CTAs: the copy is latency-bound)
   __shared__ float tile[128][PC + 1];
   const int k0 = blockIdx.x * PC, tid = threadIdx.x;
-  for (int i = tid; i < 128 * PC; i += 256) {
-    const int e = i / PC, c = i - e * PC;
-    tile[e][c] = e < E ? W[(long)e * d + k0 + c] : 0.f;
+  float v[128 * PC / 256];   // every load in flight before the shared-memory stores
+#pragma unroll
+  for (int u = 0; u < 128 * PC / 256; ++u) {
+    const int i = tid + 256 * u, e = i / PC, c = i - e * PC;
+    v[u] = e < E ? __ldg(W + (long)e * d + k0 + c) : 0.f;
+  }
+#pragma unroll
+  for (int u = 0; u < 128 * PC / 256; ++u) {
+    const int i = tid + 256 * u, e = i / PC, c = i - e * PC;
+    tile[e][c] = v[u];
   }
   __syncthreads();
   for (int i = tid; i < PC * WS; i += 256) {
     const int c = i / WS, e = i - c * WS;
     wt[(long)(k0 + c) * WS + e] = e < 128 ? (double)gamma[k0 + c] * (double)tile[e][c] : 0.0;
   }
+#ifdef FSC_ROUTER_PROF
+  __syncthreads();
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0__));
+  if (threadIdx.x == 0) atomicMax(st + 148 * 64 - 1, g0__);
+#endif
 }
 
 namespace {
@@ -509,7 +559,22 @@ cudaError_t launch_f64_t(const RouterLaunch& L, int cs, cudaStream_t s) {
     }
   }
   const int tiles = (L.T + C::TT - 1) / C::TT;
-  router_f64_prep_kernel<<<L.d / 16, 256, 0, s>>>(L.w_router, L.gamma, L.E, L.d, C::WS, L.f64_w);
+  {   // the prep kernel runs with the maximum shared-memory carveout: an SM holding a prep CTA
+      // with a small-smem configuration could not take the router's CTA (PDL overlap lost)
+    static std::atomic<unsigned long long> co{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(co.load() & bit) &&
+        cudaFuncSetAttribute(router_f64_prep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100) ==
+            cudaSuccess)
+      co.fetch_or(bit);
+  }
+  router_f64_prep_kernel<<<L.d / 16, 256, 0, s>>>(L.w_router, L.gamma, L.E, L.d, C::WS, L.f64_w
+#ifdef FSC_ROUTER_PROF
+                                                   , reinterpret_cast<unsigned long long*>(L.logits)
+#endif
+  );
   ++g_launches;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles * cs);
