@@ -11,5 +11,6 @@ for c in dsv2lite qwen3 scout qwen3_decode64 qwen3_decode512 scout_decode64 scou
 done
 python bench.py --config qwen3 --stack-layers 4 --no-cpu-baseline --no-backward > gpurun_out/sweep_$R/qwen3_stack.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv python bench.py --steps 2 --warmup 3 --no-graph --no-cpu-baseline --stack-layers 0 --no-backward > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches_decode.csv python bench.py --config qwen3_decode512 --steps 2 --warmup 3 --no-graph --no-cpu-baseline --stack-layers 0 --no-backward > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k "regex:grouped_gemm|router|permute|unpermute|perm_" -s 12 -c 12 -o gpurun_out/${R}_full python bench.py --steps 1 --warmup 3 --no-graph --no-cpu-baseline --stack-layers 0 --no-backward > gpurun_out/${R}_full.log 2>&1
 ls gpurun_out/ | head -50
