@@ -422,6 +422,7 @@ def run_gpu(args):
     roof["traffic"] = traffic
     if bound == "tensor" and achieved:
         roof["frac_of_sustained_peak"] = achieved / peaks.get("bf16_tflops_sustained", peak)
+        roof["frac_of_spec_peak"] = achieved / BF16_SPEC_TFLOPS   # NVIDIA's dense bf16 figure
     exp_flop = 2.0 * R * shape.d * 3 * shape.ffn + 2.0 * T * shape.d * 3 * shape.shared_ffn
     a2a_bytes = 2.0 * 2 * R * shape.d * (ep - 1) / ep          # dispatch + combine bytes leaving a rank
     if args.dispatch_fp8 and not allreduce:                    # dispatch: 1 B / element + scales
@@ -520,6 +521,7 @@ def backward_measure(ctx, shape, wd, x, steps, world, dev, e_loc, seed, rank):
 
 
 # ----------------------------------------------------------------------------- stack (FarSkip vs blocking)
+BF16_SPEC_TFLOPS = 2250.0    # B200 dense bf16 (spec; the measured burst peak is the roofline denominator)
 NVLINK_GBS = 900.0          # NVLink 5 per direction per GPU (spec; not measurable on the one-GPU dev box)
 COMPUTE_PHASES = {"router", "perm_maps", "gemm1", "gemm2", "shared1", "shared2", "unpermute", "attn_a", "attn_b"}
 COMM_PHASES = {"dispatch", "combine", "dispatch_stall", "combine_wait"}
