@@ -323,6 +323,13 @@ FSC_DEVINL uint4 ld_keep_u4(const uint4* p) {
                : "l"(p), "l"(kEvictLast));
   return v;
 }
+FSC_DEVINL uint4 ld_stream_u4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(kEvictFirst));
+  return v;
+}
 FSC_DEVINL void st_stream_u4(uint4* p, uint4 v) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w), "l"(kEvictFirst)

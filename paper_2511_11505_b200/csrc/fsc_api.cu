@@ -610,7 +610,7 @@ static int moe_route_and_experts(fsc_ctx* ctx, const fsc_moe_weights* w, int T, 
     // EP = 1: explicit permute into the expert-sorted send buffer (full-bandwidth SM copy)
     if (ep1_async) FUZZ(ps);
     PH_BEGIN_ON(PH_DISPATCH, ps);
-    CK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, R, d, ps));
+    CK(launch_permute_ep1(ctx->xn, ctx->src_row, ctx->pos, ctx->xs, T, k, d, ps));
     PH_END_ON(PH_DISPATCH, ps);
     if (ep1_async) {
       CK(cudaEventRecord(ctx->ev_b, ps));

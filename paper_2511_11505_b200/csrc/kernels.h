@@ -170,6 +170,12 @@ inline int perm_chunks(int T) { return (T + 31) / 32; }
 
 // K3: xs[p] = xn[src_row[p]]  (bf16 rows of d); rng != nullptr: only rows p in
 // [rng[0], rng[rng_n]) (device offsets of a range of experts)
+// EP = 1 permute (picks scatter or gather by the size of xn against L2)
+cudaError_t launch_permute_ep1(const uint16_t* xn, const int* src_row, const int* pos, uint16_t* xs, int T, int k,
+                               int d, cudaStream_t s);
+// xs[pos[t, j]] = xn[t] by source token (EP = 1 dispatch): each xn row read once
+cudaError_t launch_permute_scatter(const uint16_t* xn, const int* pos, uint16_t* xs, int T, int k, int d,
+                                   cudaStream_t s);
 cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t* xs, int R, int d,
                                 cudaStream_t s, const int* rng = nullptr, int rng_n = 0);
 

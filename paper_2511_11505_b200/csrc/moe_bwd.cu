@@ -340,7 +340,7 @@ extern "C" int fsc_moe_backward(fsc_ctx* ctx, const fsc_moe_weights* w, int T, c
   float* dgs = nullptr;
   BCK(fsc_phase_begin(ctx, PH_DISPATCH, ctx->comm));
   if (ctx->ep == 1) {
-    BCK(launch_permute_rows(ctx->xn, ctx->src_row, ctx->xs, (int)R, d, ctx->comm));
+    BCK(launch_permute_ep1(ctx->xn, ctx->src_row, ctx->pos, ctx->xs, T, k, d, ctx->comm));
     g_rows = ctx->b_gr;
     g_gate = ctx->b_gate;
     ++g_launches;

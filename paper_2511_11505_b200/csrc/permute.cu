@@ -13,6 +13,8 @@
 // K5: out[t] = resid[t] + (sum_j w[t,j] * y[pos[t,j]]) with the inner sum
 // started at 0 and taken in slot order (C-amb-12), fp32. In the FarSkip wiring
 // resid = attn-in_{k+1} and out = mlp-in_{k+1} = o_k.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -140,8 +142,16 @@ __global__ void __launch_bounds__(1024) perm_fused_kernel(const int* __restrict_
   for (int e = lane; e < E; e += 32) mask[w][e] = 0;
   __syncwarp();
   const int t = w * 32 + lane;
-  if (w < n_chunks && t < T)
-    for (int j = 0; j < k; ++j) atomicOr(&mask[w][idx[(long)t * k + j]], 1u << lane);
+  const bool valid = w < n_chunks && t < T;
+  int ids[8];                             // the token's first 8 slots stay in registers
+#pragma unroll
+  for (int j = 0; j < 8; ++j) ids[j] = valid && j < k ? idx[(long)t * k + j] : 0;
+  if (valid) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < k) atomicOr(&mask[w][ids[j]], 1u << lane);
+    for (int j = 8; j < k; ++j) atomicOr(&mask[w][idx[(long)t * k + j]], 1u << lane);
+  }
   __syncthreads();
   if (tid < E) {                          // column scan over the chunks, chunk order
     int run = 0;
@@ -183,9 +193,17 @@ __global__ void __launch_bounds__(1024) perm_fused_kernel(const int* __restrict_
     }
   }
   __syncthreads();
-  if (w < n_chunks && t < T) {
+  if (valid) {
     const uint32_t below = (1u << lane) - 1u;
-    for (int j = 0; j < k; ++j) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < k) {
+        const int e = ids[j];
+        const int p = s_off[e] + base[w][e] + __popc(mask[w][e] & below);
+        pos[(long)t * k + j] = p;
+        src_row[p] = t;
+      }
+    for (int j = 8; j < k; ++j) {
       const int e = idx[(long)t * k + j];
       const int p = s_off[e] + base[w][e] + __popc(mask[w][e] & below);
       pos[(long)t * k + j] = p;
@@ -242,6 +260,59 @@ __global__ void __launch_bounds__(256) permute_rows_kernel(const uint4* __restri
     for (int u = 0; u < 8; ++u)
       if (i0 + 32 * u < dv) st_stream_u4(b + i0 + 32 * u, v[u]);
   }
+}
+
+// Same result as permute_rows_kernel (xs[pos[t, j]] = xn[t]), by SOURCE token: a warp reads
+// row t of xn once (streamed, evict-first) and writes it to its k destination rows. Every
+// xn byte leaves HBM once whatever the L2 holds: the gather order re-reads xn k times and
+// relies on L2 keeping it (Qwen3: 67 MB of xn, evicted by the 537 MB of permuted rows).
+__global__ void __launch_bounds__(256) permute_scatter_kernel(const uint4* __restrict__ xn,
+                                                              const int* __restrict__ pos,
+                                                              uint4* __restrict__ xs, int T, int k, int dv) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long t = (long)blockIdx.x * 8 + w;
+  if (t >= T) return;
+  int p[8];
+  for (int j0 = 0; j0 < k; j0 += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = j0 + j < k ? pos[t * k + j0 + j] : -1;
+    const uint4* a = xn + t * dv;
+    for (int i0 = lane; i0 < dv; i0 += 256) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i0 + 32 * u < dv) v[u] = ld_stream_u4(a + i0 + 32 * u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (p[j] < 0) continue;
+        uint4* b = xs + (long)p[j] * dv;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + 32 * u < dv) st_stream_u4(b + i0 + 32 * u, v[u]);
+      }
+    }
+  }
+}
+
+cudaError_t launch_permute_scatter(const uint16_t* xn, const int* pos, uint16_t* xs, int T, int k, int d,
+                                   cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  ++g_launches;
+  permute_scatter_kernel<<<(T + 7) / 8, 256, 0, s>>>(reinterpret_cast<const uint4*>(xn), pos,
+                                                     reinterpret_cast<uint4*>(xs), T, k, d / 8);
+  return cudaGetLastError();
+}
+
+// EP = 1 permute: by source token when xn is too large to stay in L2 between its k reads
+// (A/B on the B200: Qwen3 prefill, xn 67 MB, 128 -> 103 us, step -24 us), by destination
+// row otherwise (DS-V2-Lite, xn 34 MB, beside the shared expert: gather 23 us faster per
+// step; decode: more CTAs in flight). FSC_PERMUTE_GATHER=0/1 forces one (A/B runs).
+cudaError_t launch_permute_ep1(const uint16_t* xn, const int* src_row, const int* pos, uint16_t* xs, int T, int k,
+                               int d, cudaStream_t s) {
+  const char* env = getenv("FSC_PERMUTE_GATHER");
+  const bool scatter = env ? atoi(env) == 0 : (long)T * d * 2 > (48l << 20);
+  return scatter ? launch_permute_scatter(xn, pos, xs, T, k, d, s)
+                 : launch_permute_rows(xn, src_row, xs, T * k, d, s);
 }
 
 cudaError_t launch_permute_rows(const uint16_t* xn, const int* src_row, uint16_t* xs, int R, int d,

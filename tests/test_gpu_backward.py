@@ -201,9 +201,15 @@ def test_moe_backward_matches_oracle(name):
                   shared_ffn=shape.shared_ffn, max_tokens=T)
     got = run_backward(ctx, shape, w, x, G, shape.n_experts)
     got2 = run_backward(ctx, shape, w, x, G, shape.n_experts)       # repeatable (workspace reuse)
+    os.environ["FSC_PERMUTE_GATHER"] = "0"                          # recompute permute by source token
+    try:
+        got3 = run_backward(ctx, shape, w, x, G, shape.n_experts)
+    finally:
+        del os.environ["FSC_PERMUTE_GATHER"]
     ctx.close()
     for k in got:
         np.testing.assert_array_equal(got[k], got2[k])
+        np.testing.assert_array_equal(got[k], got3[k])
     ref = ob.moe_block_backward(x, om.layer_from_synth(w, shape.top_k), G)
     errs = check_grads(got, ref, shape)
     print(name, {k: f"{v:.1e}" for k, v in errs.items()})

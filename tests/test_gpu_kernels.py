@@ -377,7 +377,7 @@ def test_router_f64_all_tied_and_non_finite(ctx_f64):
 # T <= 1024 with E <= 128 runs the single-CTA fused kernel, larger T the three-kernel path
 @pytest.mark.parametrize("T,E,k,hot", [(1, 4, 2, 0), (32, 4, 2, 0), (33, 8, 3, 0), (1000, 64, 6, 0), (4096, 128, 8, 0),
                                        (777, 16, 1, 0), (512, 128, 8, 0), (1024, 128, 8, 0), (1025, 128, 8, 0),
-                                       (1024, 128, 8, 1), (3000, 64, 6, 1)])
+                                       (1024, 128, 8, 1), (3000, 64, 6, 1), (300, 64, 10, 0), (700, 32, 12, 1)])
 def test_perm_maps_exact(ctx, T, E, k, hot):
     rng = np.random.default_rng(T + E)
     if hot:   # every token on the same k experts (extreme skew): one expert block holds all copies

@@ -251,6 +251,23 @@ def test_fused_gather_permute_is_bitwise_identical(name, T):
     assert np.array_equal(out0, out1)
 
 
+@pytest.mark.parametrize("name,T", [("tiny", 33), ("dsv2lite", 700), ("qwen3", 2049), ("scout", 200)])
+def test_permute_scatter_equals_gather(name, T, monkeypatch):
+    """EP = 1 permute by source token (scatter: xs[pos[t, j]] = xn[t]) and by destination
+    row (gather: xs[r] = xn[src_row[r]]) write the same buffer: forward output and the
+    backward's gradients bitwise equal."""
+    shape = synth.CONFIGS[name]
+    ctx = make_ctx(shape, T)
+    w = moe_weights_dev(synth.moe_weights(shape, seed=10))
+    x = synth.tokens(shape, seed=10, T=T)
+    outs = []
+    for g in ("0", "1"):
+        monkeypatch.setenv("FSC_PERMUTE_GATHER", g)
+        outs.append(run_blocking(ctx, w, x)[0])
+    ctx.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("name,T", [("tiny", 32), ("dsv2lite", 300), ("qwen3", 257), ("scout", 200)])
 def test_fused_unpermute_is_bitwise_identical(name, T):
     """Blocking EP = 1 fuses the gate-weighted unpermute into the down GEMM's epilogue
