@@ -160,6 +160,10 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
   };
 
   const int g = warp % WT, kp = warp / WT;
+  // PAIR (fp64 tensor cores, tiles of >= 16 tokens): warp (g2, eh) of column part kp owns
+  // tokens 16 g2 .. 16 g2 + 15 and experts [eh EP/2, (eh + 1) EP/2)
+  constexpr bool PAIR = MMA && WT >= 2;
+  const int g2 = (warp % WT) % (WT / 2 > 0 ? WT / 2 : 1), eh = (warp % WT) / (WT / 2 > 0 ? WT / 2 : 1);
   constexpr int NACC = MMA ? 2 * C::NT : 8 * C::TE;
   double acc[NACC];
 #pragma unroll
@@ -188,7 +192,26 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
     mbar_wait(&s_full[b], (ch >> 1) & 1);
     const double* xb = xbuf + b * C::XBUF + (g * 8) * F_XS + kp * C::KWC;
     const double* wb = wbuf + b * C::WBUF + kp * C::KWC * C::WS;
-    if constexpr (MMA) {
+    if constexpr (PAIR) {
+      // warp = 16 tokens (two 8-row MMA tiles) x one half of the experts: each B fragment
+      // feeds two MMAs (2 + NT/2 shared-memory loads per NT MMAs instead of 1 + NT)
+      const int gq = lane >> 2, q = lane & 3;
+      const double* xa0 = xbuf + b * C::XBUF + (g2 * 16 + gq) * F_XS + kp * C::KWC + q;
+      const double* xa1 = xa0 + 8 * F_XS;
+      const double* wq = wb + q * C::WS + eh * (EP / 2) + gq;
+#pragma unroll 2
+      for (int kk = 0; kk < C::KWC; kk += 4) {
+        const double a0 = xa0[kk], a1 = xa1[kk];
+        double bv[C::NT / 2];
+#pragma unroll
+        for (int n = 0; n < C::NT / 2; ++n) bv[n] = wq[kk * C::WS + 8 * n];
+#pragma unroll
+        for (int n = 0; n < C::NT / 2; ++n) {
+          dmma_8x8x4(*reinterpret_cast<double(*)[2]>(&acc[2 * n]), a0, bv[n]);
+          dmma_8x8x4(*reinterpret_cast<double(*)[2]>(&acc[C::NT + 2 * n]), a1, bv[n]);
+        }
+      }
+    } else if constexpr (MMA) {
       const int gq = lane >> 2, q = lane & 3;
       const double* xa = xb + gq * F_XS + q;
       const double* wq = wb + q * C::WS + gq;
@@ -233,7 +256,16 @@ __global__ void __launch_bounds__(F_THREADS, 1) router_f64_kernel(RouterLaunch L
   // ---- this CTA's partials: [kp][token][EP] over the W' buffers (free after the last sync),
   // then summed over kp (ascending) into slot 0 so the cluster reduction reads one value
   double* part = wbuf;
-  if constexpr (MMA) {
+  if constexpr (PAIR) {
+    const int gq = lane >> 2, q = lane & 3;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      double* pr = part + (kp * C::TT + g2 * 16 + mt * 8 + gq) * EP + eh * (EP / 2) + 2 * q;
+#pragma unroll
+      for (int n = 0; n < C::NT / 2; ++n)
+        *reinterpret_cast<double2*>(pr + 8 * n) = make_double2(acc[mt * C::NT + 2 * n], acc[mt * C::NT + 2 * n + 1]);
+    }
+  } else if constexpr (MMA) {
     const int gq = lane >> 2, q = lane & 3;
     double* pr = part + (kp * C::TT + g * 8 + gq) * EP + 2 * q;
 #pragma unroll
