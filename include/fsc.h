@@ -203,7 +203,7 @@ FSC_API int fsc_set_router_int8(fsc_ctx* ctx, int on);
  * lower id, slots ascending by id, renormalised gates) with every product and sum in
  * fp64 in a fixed order, so the selection is the fp64 oracle's with no error bound or
  * refinement (n_refined is not written). on = 1: every call; 0: never; -1 (default,
- * auto): calls with T x EP x d <= 2e8 (EP = E padded to 32 / 64 / 128: decode batches) unless fsc_set_router_int8(ctx, 0) selected the
+ * auto): calls with T x EP x d <= 2.7e8 (EP = E padded to 32 / 64 / 128: decode batches) unless fsc_set_router_int8(ctx, 0) selected the
  * fp32 SIMT router. Workspace (d x 136 doubles, gamma (.) W_R) allocated at fsc_init. Returns FSC_ERR_CONFIG for on = 1 on an unsupported
  * shape. */
 FSC_API int fsc_set_router_f64(fsc_ctx* ctx, int on);

@@ -332,7 +332,7 @@ class Context:
 
     def set_router_f64(self, on):
         """fp64 small-batch router (router_f64_kernel): True (every call), False (never) or
-        None (auto, the default: T x EP x d <= 2e8 unless the fp32 SIMT router was selected)."""
+        None (auto, the default: T x EP x d <= 2.7e8 unless the fp32 SIMT router was selected)."""
         self._ck(self.lib.fsc_set_router_f64(self.h, -1 if on is None else int(on)))
 
     def set_fused_unpermute(self, on):

@@ -419,14 +419,14 @@ bool router_tc_on(const fsc_ctx* ctx) {
 }
 
 // The fp64 router (router_f64_kernel) for small batches, where the tensor-core router's
-// phases are latency-bound: auto = T x EP x d <= 2e8 fp64 FMAs (EP = E padded to 32 / 64 /
-// 128; measured crossover: Qwen3 ~768 tokens, DS-V2-Lite ~1500, Scout ~1200) unless the fp32
+// phases are latency-bound: auto = T x EP x d <= 2.7e8 fp64 FMAs (EP = E padded to 32 / 64 /
+// 128; measured: Qwen3 up to ~1024 tokens, DS-V2-Lite ~2048, Scout ~1600) unless the fp32
 // SIMT router was selected (fsc_set_router_int8(ctx, 0), the A/B reference); on = any T.
 bool router_f64_on(const fsc_ctx* ctx, int T, int d, int E, int k) {
   if (ctx->router_f64 == 0 || !ctx->f64_w || !router_f64_supported(d, E, k)) return false;
   if (ctx->router_f64 > 0) return true;
   const long ep = E <= 32 ? 32 : E <= 64 ? 64 : 128;
-  return ctx->router_i8 != 0 && (double)T * ep * d <= 2e8;
+  return ctx->router_i8 != 0 && (double)T * ep * d <= 2.7e8;
 }
 
 extern "C" int fsc_set_router_f64(fsc_ctx* ctx, int on) {

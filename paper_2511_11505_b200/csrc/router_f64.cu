@@ -538,8 +538,8 @@ int f64_max_clusters(int d, int cs) {
 
 // Plan = (WT warps of 8 tokens per tile, cluster size CS). Cost model fitted to a sweep of
 // every plan on the B200 (tools/f64_plans.sh): a fixed ~10 us plus, per wave of
-// co-resident clusters, the chunks of one CTA at 0.1 us + 0.06 us per token x EP / 128
-// (the fp64 tensor-core work of a 64-column chunk). Cluster sizes above 8 are not used
+// co-resident clusters, ~5 us of CTA prologue / epilogue and the chunks of one CTA at 0.1 us +
+// 0.06 us per token x EP / 128 (the fp64 tensor-core work of a 64-column chunk). Cluster sizes above 8 are not used
 // (16-CTA clusters measured slower: few fit at once).
 struct F64Plan {
   int wt, cs;
@@ -562,7 +562,7 @@ F64Plan f64_plan(int T, int d) {
                                 : wt == 2 ? f64_max_clusters<EP, 2>(d, cs) : f64_max_clusters<EP, 4>(d, cs);
       const int waves = (tiles + maxc - 1) / maxc;
       const int nch = d / cs / F_DK;
-      const double cost = waves * nch * (0.1 + 0.06 * tt * EP / 128.0);
+      const double cost = waves * (5.0 + nch * (0.1 + 0.06 * tt * EP / 128.0));   // + per-wave prologue / epilogue
       if (cost < best_cost * 0.999) {
         best_cost = cost;
         best = {wt, cs};
